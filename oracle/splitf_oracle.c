@@ -1,0 +1,877 @@
+/* TEST INFRASTRUCTURE ONLY — the checker, never the product.
+ * See splitf_oracle.h for the contract.  Each function cites the reference
+ * file:line whose behaviour it restates (paths under /root/reference/proj).
+ */
+#define _GNU_SOURCE
+#include "splitf_oracle.h"
+
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { K_CONFIG = 1, K_INPUT, K_PROTOCOL, K_TRANSPORT, K_CAPACITY, K_SESSION, K_NUMERIC,
+       K_TRAINING, K_DECOMPOSITION, K_INTERNAL };
+static const char* kind_name[] = {"", "config", "input", "protocol", "transport", "capacity",
+                                  "session", "numeric", "training", "decomposition", "internal"};
+
+static __thread char g_err[512];
+const char* orc_last_error(void) { return g_err; }
+
+static int err(int kind, const char* fmt, ...) {
+    char msg[400];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(msg, sizeof msg, fmt, ap);
+    va_end(ap);
+    snprintf(g_err, sizeof g_err, "%s: %s", kind_name[kind], msg);
+    return kind;
+}
+
+/* ── mt19937_64 (the std:: engine used by init_weights, tinyformer.cpp:130) ── */
+typedef struct { uint64_t s[312]; int i; } mt64;
+
+static void mt_seed(mt64* m, uint64_t seed) {
+    m->s[0] = seed;
+    for (int k = 1; k < 312; ++k)
+        m->s[k] = 6364136223846793005ULL * (m->s[k - 1] ^ (m->s[k - 1] >> 62)) + (uint64_t)k;
+    m->i = 312;
+}
+
+static uint64_t mt_next(mt64* m) {
+    if (m->i >= 312) {
+        const uint64_t up = 0xFFFFFFFF80000000ULL, lo = 0x7FFFFFFFULL, a = 0xB5026F5AA96619E9ULL;
+        for (int k = 0; k < 312; ++k) {
+            const uint64_t y = (m->s[k] & up) | (m->s[(k + 1) % 312] & lo);
+            m->s[k] = m->s[(k + 156) % 312] ^ (y >> 1) ^ ((y & 1ULL) ? a : 0ULL);
+        }
+        m->i = 0;
+    }
+    uint64_t x = m->s[m->i++];
+    x ^= (x >> 29) & 0x5555555555555555ULL;
+    x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+    x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+    x ^= x >> 43;
+    return x;
+}
+
+/* ── model ────────────────────────────────────────────────────────────── */
+typedef struct {
+    float *attn_norm, *wq, *wk, *wv, *wo, *ffn_norm, *w_gate, *w_up, *w_down;
+} orc_layer;
+
+struct orc_model {
+    orc_cfg c;
+    float* flat; /* all params, snapshot declaration order */
+    int64_t n;
+    float* embedding;
+    orc_layer* L;
+    float* final_norm;
+    float* lm_head;
+};
+
+/* ModelConfig::validate, tinyformer.cpp:102-121 */
+static int validate(const orc_cfg* c) {
+    if (c->vocab_size < 2) return err(K_CONFIG, "vocab_size must be >= 2");
+    if (c->n_layers < 4) return err(K_CONFIG, "n_layers must be >= 4");
+    if (c->hidden_dim <= 0 || c->n_heads <= 0 || c->n_kv_heads <= 0 || c->head_dim <= 0 ||
+        c->ffn_dim <= 0 || c->max_seq_len <= 0)
+        return err(K_CONFIG, "all dimensions must be positive");
+    if (c->n_heads * c->head_dim != c->hidden_dim)
+        return err(K_CONFIG, "n_heads * head_dim must equal hidden_dim");
+    if (c->n_heads % c->n_kv_heads != 0) return err(K_CONFIG, "n_kv_heads must divide n_heads");
+    if (c->head_dim % 2 != 0) return err(K_CONFIG, "head_dim must be even for rotary pairs");
+    if (!(c->rope_base > 0.0f) || !(c->rms_eps > 0.0f))
+        return err(K_CONFIG, "rope_base and rms_eps must be positive");
+    return 0;
+}
+
+int64_t orc_param_count(const orc_cfg* c) {
+    const int64_t h = c->hidden_dim, q = (int64_t)c->n_heads * c->head_dim,
+                  kv = (int64_t)c->n_kv_heads * c->head_dim, f = c->ffn_dim, v = c->vocab_size;
+    const int64_t per = h + h * q + 2 * h * kv + q * h + h + 3 * h * f;
+    return v * h + c->n_layers * per + h + h * v;
+}
+
+static void carve(orc_model* m) {
+    const orc_cfg* c = &m->c;
+    const int64_t h = c->hidden_dim, q = (int64_t)c->n_heads * c->head_dim,
+                  kv = (int64_t)c->n_kv_heads * c->head_dim, f = c->ffn_dim, v = c->vocab_size;
+    float* p = m->flat;
+    m->embedding = p; p += v * h;
+    for (int l = 0; l < c->n_layers; ++l) {
+        orc_layer* L = &m->L[l];
+        L->attn_norm = p; p += h;
+        L->wq = p; p += h * q;
+        L->wk = p; p += h * kv;
+        L->wv = p; p += h * kv;
+        L->wo = p; p += q * h;
+        L->ffn_norm = p; p += h;
+        L->w_gate = p; p += h * f;
+        L->w_up = p; p += h * f;
+        L->w_down = p; p += f * h;
+    }
+    m->final_norm = p; p += h;
+    m->lm_head = p;
+}
+
+static int alloc_model(const orc_cfg* c, orc_model** out) {
+    int rc = validate(c);
+    if (rc) return rc;
+    orc_model* m = calloc(1, sizeof *m);
+    m->c = *c;
+    m->n = orc_param_count(c);
+    m->flat = malloc((size_t)m->n * sizeof(float));
+    m->L = calloc((size_t)c->n_layers, sizeof(orc_layer));
+    if (!m->flat || !m->L) {
+        orc_model_free(m);
+        return err(K_INTERNAL, "out of host memory");
+    }
+    carve(m);
+    *out = m;
+    return 0;
+}
+
+static float bf16_rne(float v) {
+    uint32_t u;
+    memcpy(&u, &v, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return v;
+    u += 0x7fffu + ((u >> 16) & 1u);
+    u &= 0xffff0000u;
+    memcpy(&v, &u, 4);
+    return v;
+}
+
+/* init_weights, tinyformer.cpp:123-152 (uniform01 :21-23, fill_uniform
+ * :25-30): one stream, declaration order, v = a * (float)(2u - 1). Since the
+ * flat buffer IS declaration order, a single pass fills everything. */
+int orc_model_new(const orc_cfg* c, int bf16_round, orc_model** out) {
+    int rc = alloc_model(c, out);
+    if (rc) return rc;
+    orc_model* m = *out;
+    const float a = 1.0f / sqrtf((float)c->hidden_dim);
+    mt64* rng = malloc(sizeof *rng);
+    mt_seed(rng, c->seed);
+    for (int64_t i = 0; i < m->n; ++i) {
+        const double u = (double)(mt_next(rng) >> 11) * 0x1.0p-53;
+        float v = a * (float)(2.0 * u - 1.0);
+        m->flat[i] = bf16_round ? bf16_rne(v) : v;
+    }
+    free(rng);
+    return 0;
+}
+
+int orc_model_from_params(const orc_cfg* c, const float* params, orc_model** out) {
+    int rc = alloc_model(c, out);
+    if (rc) return rc;
+    memcpy((*out)->flat, params, (size_t)(*out)->n * sizeof(float));
+    return 0;
+}
+
+void orc_model_free(orc_model* m) {
+    if (!m) return;
+    free(m->flat);
+    free(m->L);
+    free(m);
+}
+
+int64_t orc_model_params(const orc_model* m, float* out) {
+    if (out) memcpy(out, m->flat, (size_t)m->n * sizeof(float));
+    return m->n;
+}
+
+/* ── cache bank (tinyformer.hpp:96-156, tinyformer.cpp:243-327) ─────────── */
+struct orc_bank {
+    int lb, le, nkv, hd, max_len, len, committed;
+    float *k, *v; /* [layer - lb][kv head][max_len][hd] */
+};
+
+static size_t kv_off(const orc_bank* b, int layer, int head, int pos) {
+    return (((size_t)(layer - b->lb) * b->nkv + head) * b->max_len + pos) * b->hd;
+}
+
+int orc_bank_new(const orc_model* m, int lb, int le, orc_bank** out) {
+    if (lb < 0 || le > m->c.n_layers || lb > le)
+        return err(K_CONFIG, "invalid layer range for cache bank");
+    orc_bank* b = calloc(1, sizeof *b);
+    b->lb = lb;
+    b->le = le;
+    b->nkv = m->c.n_kv_heads;
+    b->hd = m->c.head_dim;
+    b->max_len = m->c.max_seq_len;
+    const size_t n = (size_t)(le - lb) * b->nkv * b->max_len * b->hd;
+    b->k = calloc(n ? n : 1, sizeof(float));
+    b->v = calloc(n ? n : 1, sizeof(float));
+    *out = b;
+    return 0;
+}
+
+void orc_bank_free(orc_bank* b) {
+    if (!b) return;
+    free(b->k);
+    free(b->v);
+    free(b);
+}
+
+void orc_bank_state(const orc_bank* b, int* len, int* committed) {
+    *len = b->le > b->lb ? b->len : 0;
+    *committed = b->committed;
+}
+void orc_bank_mark_committed(orc_bank* b, int c) { b->committed = c; }
+
+/* CacheBank::resolve, tinyformer.cpp:282-308 */
+int orc_bank_resolve(orc_bank* b, const int* keep, int n) {
+    const int len = b->le > b->lb ? b->len : 0;
+    const int tail = len - b->committed;
+    for (int i = 0, prev = -1; i < n; prev = keep[i], ++i)
+        if (keep[i] <= prev || keep[i] >= tail)
+            return err(K_PROTOCOL,
+                       "keep indices must be strictly increasing and within the provisional tail");
+    for (int l = b->lb; l < b->le; ++l)
+        for (int h = 0; h < b->nkv; ++h)
+            for (int i = 0; i < n; ++i) {
+                const int dst = b->committed + i, src = b->committed + keep[i];
+                if (src == dst) continue;
+                memcpy(b->k + kv_off(b, l, h, dst), b->k + kv_off(b, l, h, src), b->hd * sizeof(float));
+                memcpy(b->v + kv_off(b, l, h, dst), b->v + kv_off(b, l, h, src), b->hd * sizeof(float));
+            }
+    b->committed += n;
+    b->len = b->committed;
+    return 0;
+}
+
+/* CacheBank::crop, tinyformer.cpp:310-316 */
+int orc_bank_crop(orc_bank* b, int pos) {
+    const int len = b->le > b->lb ? b->len : 0;
+    if (pos < 0 || pos > len) return err(K_PROTOCOL, "crop position exceeds cache length");
+    b->len = pos;
+    if (b->committed > pos) b->committed = pos;
+    return 0;
+}
+
+int orc_bank_kv(const orc_bank* b, int layer, int head, int pos, float* k, float* v) {
+    if (layer < b->lb || layer >= b->le || head < 0 || head >= b->nkv || pos < 0 || pos >= b->max_len)
+        return err(K_INPUT, "kv index out of range");
+    memcpy(k, b->k + kv_off(b, layer, head, pos), b->hd * sizeof(float));
+    memcpy(v, b->v + kv_off(b, layer, head, pos), b->hd * sizeof(float));
+    return 0;
+}
+
+/* ── arithmetic kernels (tinyformer.cpp:33-65) ─────────────────────────── */
+
+/* rms_norm :33-38 — serial sum of squares, then (x*scale)*gain */
+static void rms_norm(const float* x, const float* g, float eps, int d, float* y) {
+    float ss = 0.0f;
+    for (int i = 0; i < d; ++i) ss += x[i] * x[i];
+    const float scale = 1.0f / sqrtf(ss / (float)d + eps);
+    for (int i = 0; i < d; ++i) y[i] = x[i] * scale * g[i];
+}
+
+/* matvec :41-49 — out[j] accumulates rows i ascending, zero inputs skipped */
+static void matvec(const float* x, const float* w, int rows, int cols, float* out) {
+    for (int j = 0; j < cols; ++j) out[j] = 0.0f;
+    for (int i = 0; i < rows; ++i) {
+        const float xi = x[i];
+        if (xi == 0.0f) continue;
+        const float* wr = w + (size_t)i * cols;
+        for (int j = 0; j < cols; ++j) out[j] += xi * wr[j];
+    }
+}
+
+/* rope_rotate :52-63 — interleaved pairs (2i, 2i+1) */
+static void rope(float* v, int hd, int pos, float base) {
+    for (int i = 0; i < hd / 2; ++i) {
+        const float freq = powf(base, -2.0f * (float)i / (float)hd);
+        const float ang = (float)pos * freq;
+        float s, c;
+        sincosf(ang, &s, &c);
+        const float a = v[2 * i], b = v[2 * i + 1];
+        v[2 * i] = a * c - b * s;
+        v[2 * i + 1] = a * s + b * c;
+    }
+}
+
+static float silu(float x) { return x / (1.0f + expf(-x)); }
+
+static int all_finite(const float* p, size_t n) {
+    for (size_t i = 0; i < n; ++i)
+        if (!isfinite(p[i])) return 0;
+    return 1;
+}
+
+/* embed_at, tinyformer.cpp:348-373 */
+int orc_embed_at(const orc_model* m, int seq, const int* ids, const int* pos, float* out) {
+    for (int i = 0; i < seq; ++i)
+        if (pos[i] < 0 || pos[i] >= m->c.max_seq_len)
+            return err(K_CAPACITY, "position exceeds max_seq_len");
+    for (int i = 0; i < seq; ++i) {
+        if (ids[i] < 0 || ids[i] >= m->c.vocab_size) return err(K_INPUT, "token id out of range");
+        memcpy(out + (size_t)i * m->c.hidden_dim, m->embedding + (size_t)ids[i] * m->c.hidden_dim,
+               sizeof(float) * m->c.hidden_dim);
+    }
+    return 0;
+}
+
+/* build_attention_mask, tinyformer.cpp:229-241 */
+void orc_build_causal_mask(int k, int committed, float* out) {
+    const int kv = committed + k;
+    for (int i = 0; i < k; ++i)
+        for (int j = 0; j < kv; ++j) out[(size_t)i * kv + j] = j < committed + i + 1 ? 0.0f : -INFINITY;
+}
+
+/* forward_layers, tinyformer.cpp:375-508 */
+int orc_forward(const orc_model* m, orc_bank* b, int lb, int le, int seq, const float* h,
+                const int* pos, const float* mask_in, float* out) {
+    const orc_cfg* c = &m->c;
+    const int H = c->hidden_dim, hd = c->head_dim, qd = c->n_heads * hd, kvd = c->n_kv_heads * hd;
+    if (lb == le || seq == 0) {
+        memcpy(out, h, sizeof(float) * (size_t)seq * H);
+        return 0;
+    }
+    if (lb < b->lb || le > b->le) return err(K_INTERNAL, "layer range outside cache bank");
+    const int prior = b->len;
+    if (prior + seq > c->max_seq_len) return err(K_CAPACITY, "sequence exceeds max_seq_len");
+    if (!all_finite(h, (size_t)seq * H)) return err(K_NUMERIC, "non-finite hidden state");
+    const int kv_len = prior + seq;
+    float* causal = NULL;
+    const float* mask = mask_in;
+    if (!mask) {
+        causal = malloc(sizeof(float) * (size_t)seq * kv_len);
+        orc_build_causal_mask(seq, prior, causal);
+        mask = causal;
+    }
+    const int group = c->n_heads / c->n_kv_heads;
+    const float inv_sqrt_hd = 1.0f / sqrtf((float)hd);
+    float* cur = out;
+    memcpy(cur, h, sizeof(float) * (size_t)seq * H);
+    float* normed = malloc(sizeof(float) * H);
+    float* q = malloc(sizeof(float) * qd);
+    float* att = malloc(sizeof(float) * qd);
+    float* proj = malloc(sizeof(float) * H);
+    float* gate = malloc(sizeof(float) * c->ffn_dim);
+    float* up = malloc(sizeof(float) * c->ffn_dim);
+    float* sc = malloc(sizeof(float) * kv_len);
+    int rc = 0;
+
+    for (int layer = lb; layer < le && !rc; ++layer) {
+        const orc_layer* L = &m->L[layer];
+        /* K/V for every batch row first (:416-437), column-by-column over r */
+        for (int i = 0; i < seq; ++i) {
+            rms_norm(cur + (size_t)i * H, L->attn_norm, c->rms_eps, H, normed);
+            for (int kh = 0; kh < c->n_kv_heads; ++kh) {
+                float* kd = b->k + kv_off(b, layer, kh, prior + i);
+                float* vd = b->v + kv_off(b, layer, kh, prior + i);
+                for (int d = 0; d < hd; ++d) {
+                    float ak = 0.0f, av = 0.0f;
+                    const int col = kh * hd + d;
+                    for (int r = 0; r < H; ++r) {
+                        ak += normed[r] * L->wk[(size_t)r * kvd + col];
+                        av += normed[r] * L->wv[(size_t)r * kvd + col];
+                    }
+                    kd[d] = ak;
+                    vd[d] = av;
+                }
+                rope(kd, hd, pos[i], c->rope_base);
+            }
+        }
+        /* queries, masked softmax attention, O-proj, FFN (:442-501) */
+        for (int i = 0; i < seq && !rc; ++i) {
+            float* hr = cur + (size_t)i * H;
+            rms_norm(hr, L->attn_norm, c->rms_eps, H, normed);
+            matvec(normed, L->wq, H, qd, q);
+            for (int hh = 0; hh < c->n_heads; ++hh) rope(q + (size_t)hh * hd, hd, pos[i], c->rope_base);
+            for (int hh = 0; hh < c->n_heads; ++hh) {
+                const int kh = hh / group;
+                const float* qh = q + (size_t)hh * hd;
+                float mx = -INFINITY;
+                for (int j = 0; j < kv_len; ++j) {
+                    const float mj = mask[(size_t)i * kv_len + j];
+                    if (mj == -INFINITY) {
+                        sc[j] = -INFINITY;
+                        continue;
+                    }
+                    const float* kj = b->k + kv_off(b, layer, kh, j);
+                    float dot = 0.0f;
+                    for (int d = 0; d < hd; ++d) dot += qh[d] * kj[d];
+                    const float s = dot * inv_sqrt_hd + mj;
+                    sc[j] = s;
+                    mx = mx < s ? s : mx;
+                }
+                if (mx == -INFINITY) {
+                    rc = err(K_PROTOCOL, "mask row admits no attendable position");
+                    break;
+                }
+                float den = 0.0f;
+                for (int j = 0; j < kv_len; ++j) {
+                    if (sc[j] == -INFINITY) {
+                        sc[j] = 0.0f;
+                    } else {
+                        sc[j] = expf(sc[j] - mx);
+                        den += sc[j];
+                    }
+                }
+                float* oh = att + (size_t)hh * hd;
+                for (int d = 0; d < hd; ++d) oh[d] = 0.0f;
+                const float inv = 1.0f / den;
+                for (int j = 0; j < kv_len; ++j) {
+                    const float wgt = sc[j] * inv;
+                    if (wgt == 0.0f) continue;
+                    const float* vj = b->v + kv_off(b, layer, kh, j);
+                    for (int d = 0; d < hd; ++d) oh[d] += wgt * vj[d];
+                }
+            }
+            if (rc) break;
+            matvec(att, L->wo, qd, H, proj);
+            for (int d = 0; d < H; ++d) hr[d] += proj[d];
+            rms_norm(hr, L->ffn_norm, c->rms_eps, H, normed);
+            matvec(normed, L->w_gate, H, c->ffn_dim, gate);
+            matvec(normed, L->w_up, H, c->ffn_dim, up);
+            for (int d = 0; d < c->ffn_dim; ++d) gate[d] = silu(gate[d]) * up[d];
+            matvec(gate, L->w_down, c->ffn_dim, H, proj);
+            for (int d = 0; d < H; ++d) hr[d] += proj[d];
+        }
+        b->len = kv_len;
+    }
+    free(normed); free(q); free(att); free(proj); free(gate); free(up); free(sc); free(causal);
+    return rc;
+}
+
+/* finalize, tinyformer.cpp:510-526 */
+int orc_finalize(const orc_model* m, int seq, const float* h, float* logits) {
+    const int H = m->c.hidden_dim, V = m->c.vocab_size;
+    if (!all_finite(h, (size_t)seq * H)) return err(K_NUMERIC, "non-finite hidden state");
+    float* normed = malloc(sizeof(float) * H);
+    for (int i = 0; i < seq; ++i) {
+        rms_norm(h + (size_t)i * H, m->final_norm, m->c.rms_eps, H, normed);
+        matvec(normed, m->lm_head, H, V, logits + (size_t)i * V);
+    }
+    free(normed);
+    return 0;
+}
+
+/* argmax_row, tinyformer.cpp:329-340 — first maximum wins */
+int orc_argmax(const float* r, int vocab) {
+    int best = 0;
+    float bv = r[0];
+    for (int i = 1; i < vocab; ++i)
+        if (r[i] > bv) {
+            bv = r[i];
+            best = i;
+        }
+    return best;
+}
+
+/* generate_monolithic_traced, tinyformer.cpp:534-573 */
+int orc_generate(const orc_model* m, const int* prompt, int n, int max_new, int* out_tokens,
+                 float* out_logits) {
+    const orc_cfg* c = &m->c;
+    if (n <= 0) return err(K_INPUT, "prompt must be non-empty");
+    if (n + max_new > c->max_seq_len) return err(K_CAPACITY, "prompt + max_new exceeds max_seq_len");
+    if (max_new == 0) return 0;
+    const int H = c->hidden_dim, V = c->vocab_size;
+    orc_bank* b;
+    orc_bank_new(m, 0, c->n_layers, &b);
+    float* h = malloc(sizeof(float) * (size_t)n * H);
+    float* o = malloc(sizeof(float) * (size_t)n * H);
+    float* lg = malloc(sizeof(float) * (size_t)n * V);
+    int* pos = malloc(sizeof(int) * n);
+    for (int i = 0; i < n; ++i) pos[i] = i;
+    int rc = orc_embed_at(m, n, prompt, pos, h);
+    if (!rc) rc = orc_forward(m, b, 0, c->n_layers, n, h, pos, NULL, o);
+    b->committed = b->len;
+    if (!rc) rc = orc_finalize(m, n, o, lg);
+    int tok = 0;
+    if (!rc) {
+        tok = orc_argmax(lg + (size_t)(n - 1) * V, V);
+        out_tokens[0] = tok;
+        if (out_logits) memcpy(out_logits, lg + (size_t)(n - 1) * V, sizeof(float) * V);
+    }
+    for (int t = 1; t < max_new && !rc; ++t) {
+        int p = n + t - 1;
+        rc = orc_embed_at(m, 1, &tok, &p, h);
+        if (!rc) rc = orc_forward(m, b, 0, c->n_layers, 1, h, &p, NULL, o);
+        b->committed = b->len;
+        if (!rc) rc = orc_finalize(m, 1, o, lg);
+        if (rc) break;
+        tok = orc_argmax(lg, V);
+        out_tokens[t] = tok;
+        if (out_logits) memcpy(out_logits + (size_t)t * V, lg, sizeof(float) * V);
+    }
+    free(h); free(o); free(lg); free(pos);
+    orc_bank_free(b);
+    return rc;
+}
+
+/* ── binary16 codec, wire.cpp:83-160 ──────────────────────────────────── */
+uint16_t orc_f32_to_f16(float v, uint64_t* clamped) {
+    uint32_t u;
+    memcpy(&u, &v, 4);
+    const uint16_t sign = (uint16_t)((u >> 16) & 0x8000u);
+    const uint32_t a = u & 0x7fffffffu;
+    if (a > 0x7f800000u) return sign | 0x7e00u;
+    if (a == 0x7f800000u) return sign | 0x7c00u;
+    float av;
+    memcpy(&av, &a, 4);
+    if (av > 65504.0f) {
+        if (clamped) ++*clamped;
+        return sign | 0x7bffu;
+    }
+    const int e = (int)((a >> 23) & 0xff) - 127;
+    uint32_t mant = a & 0x7fffffu;
+    if (e < -25) return sign;
+    if (e == -25) return mant == 0 ? sign : (uint16_t)(sign | 1u);
+    if (e < -14) {
+        mant |= 0x800000u;
+        const int sh = -e - 1;
+        const uint32_t hv = mant >> sh, rem = mant & ((1u << sh) - 1u), half = 1u << (sh - 1);
+        return (uint16_t)(sign | (hv + ((rem > half || (rem == half && (hv & 1u))) ? 1u : 0u)));
+    }
+    uint32_t he = (uint32_t)(e + 15), hm = mant >> 13;
+    const uint32_t rem = mant & 0x1fffu;
+    if (rem > 0x1000u || (rem == 0x1000u && (hm & 1u))) {
+        if (++hm == 0x400u) {
+            hm = 0;
+            ++he;
+        }
+    }
+    if (he >= 31) {
+        if (clamped) ++*clamped;
+        return sign | 0x7bffu;
+    }
+    return (uint16_t)(sign | (he << 10) | hm);
+}
+
+float orc_f16_to_f32(uint16_t b) {
+    const uint32_t sign = (uint32_t)(b & 0x8000u) << 16, e = (b >> 10) & 0x1fu, mant = b & 0x3ffu;
+    uint32_t o;
+    if (e == 0) {
+        if (mant == 0) {
+            o = sign;
+        } else {
+            int k = 0;
+            uint32_t mm = mant;
+            while (!(mm & 0x400u)) {
+                mm <<= 1;
+                ++k;
+            }
+            o = sign | ((uint32_t)(113 - k) << 23) | ((mm & 0x3ffu) << 13);
+        }
+    } else if (e == 31) {
+        o = sign | 0x7f800000u | (mant << 13);
+    } else {
+        o = sign | ((e + 112) << 23) | (mant << 13);
+    }
+    float f;
+    memcpy(&f, &o, 4);
+    return f;
+}
+
+/* ── verify_greedy, decoding.cpp:99-109 ───────────────────────────────── */
+int orc_verify_greedy_ids(const int* amax, int row_begin, const int* g, int n, int anchor,
+                          int* committed) {
+    int k = 0;
+    committed[0] = anchor;
+    while (k < n && g[k] == committed[k]) {
+        committed[k + 1] = amax[row_begin + k];
+        ++k;
+    }
+    return k;
+}
+
+int orc_verify_greedy(const float* logits, int vocab, int row_begin, const int* g, int n,
+                      int anchor, int* committed) {
+    int k = 0;
+    committed[0] = anchor;
+    while (k < n && g[k] == committed[k]) {
+        committed[k + 1] = orc_argmax(logits + (size_t)(row_begin + k) * vocab, vocab);
+        ++k;
+    }
+    return k;
+}
+
+/* ── NGramPool, decoding.cpp:61-97: recency-ordered, dedup, LRU eviction ─ */
+struct orc_pool {
+    int n;       /* ngram_n; continuation length n-1 */
+    size_t cap, size;
+    int* rows;   /* [size][n]: key then continuation; row 0 = most recent */
+};
+
+int orc_pool_new(int ngram_n, size_t capacity, orc_pool** out) {
+    if (ngram_n < 2) return err(K_CONFIG, "ngram_n must be >= 2");
+    if (capacity < 1) return err(K_CONFIG, "pool capacity must be >= 1");
+    orc_pool* p = calloc(1, sizeof *p);
+    p->n = ngram_n;
+    p->cap = capacity;
+    p->rows = malloc(sizeof(int) * (capacity + 1) * (size_t)ngram_n);
+    *out = p;
+    return 0;
+}
+void orc_pool_free(orc_pool* p) {
+    if (!p) return;
+    free(p->rows);
+    free(p);
+}
+size_t orc_pool_size(const orc_pool* p) { return p->size; }
+
+static void pool_insert(orc_pool* p, const int* row) {
+    const size_t w = (size_t)p->n;
+    for (size_t e = 0; e < p->size; ++e) {
+        if (memcmp(p->rows + e * w, row, w * sizeof(int)) == 0) { /* refresh recency */
+            memmove(p->rows + w, p->rows, e * w * sizeof(int));
+            memcpy(p->rows, row, w * sizeof(int));
+            return;
+        }
+    }
+    memmove(p->rows + w, p->rows, p->size * w * sizeof(int));
+    memcpy(p->rows, row, w * sizeof(int));
+    if (++p->size > p->cap) p->size = p->cap; /* pop_back */
+}
+
+int orc_pool_update(orc_pool* p, const int* prev, const int* cur, int w) {
+    int row[64];
+    if (p->n > 64) return err(K_CONFIG, "ngram_n too large");
+    for (int i = 0; i + p->n - 1 <= w - 1; ++i) {
+        row[0] = prev[i];
+        memcpy(row + 1, cur + i + 1, sizeof(int) * (size_t)(p->n - 1));
+        pool_insert(p, row);
+    }
+    return 0;
+}
+
+int orc_pool_lookup(const orc_pool* p, int key, int max_c, int* out) {
+    /* push first, then stop once max_c is reached: lookup(key, 0) returns one
+     * hit, exactly like the reference loop (decoding.cpp:91-95) */
+    int got = 0;
+    for (size_t e = 0; e < p->size; ++e) {
+        const int* r = p->rows + e * (size_t)p->n;
+        if (r[0] != key) continue;
+        memcpy(out + (size_t)got * (p->n - 1), r + 1, sizeof(int) * (size_t)(p->n - 1));
+        if (++got >= max_c) break;
+    }
+    return got;
+}
+
+/* ── split pipeline decode ─────────────────────────────────────────────
+ * SplitClient (client.cpp:120-228) + ServerEngine (server.cpp:203-265) +
+ * decode_sequential / decode_lookahead_with_pool (decoding.cpp:111-139,
+ * 209-355), in one process with the wire's value quantisation applied.   */
+typedef struct {
+    const orc_model* m;
+    orc_decode_cfg dc;
+    orc_bank *pre, *mid, *suf;
+    int first_step_done;
+    uint64_t clamped;
+} pipe_t;
+
+static void wire_pass(float* x, size_t n, int f32, uint64_t* clamped) {
+    if (f32) return;
+    for (size_t i = 0; i < n; ++i) x[i] = orc_f16_to_f32(orc_f32_to_f16(x[i], clamped));
+}
+
+/* one client exchange: prefix -> wire -> server -> wire -> suffix -> finalize */
+static int pipe_run(pipe_t* P, int seq, const int* toks, const int* pos, const float* mask,
+                    const int* keep, int nkeep, int is_prompt, float* logits) {
+    const orc_model* m = P->m;
+    const int H = m->c.hidden_dim, L = m->c.n_layers;
+    const int pre_e = P->dc.prefix_layers, suf_b = L - P->dc.suffix_layers;
+    float* a = malloc(sizeof(float) * (size_t)seq * H);
+    float* b = malloc(sizeof(float) * (size_t)seq * H);
+    int rc = 0;
+    if (!is_prompt) {
+        if (nkeep > 0 || P->pre->len - P->pre->committed > 0) {
+            rc = orc_bank_resolve(P->pre, keep, nkeep);
+            if (!rc) rc = orc_bank_resolve(P->suf, keep, nkeep);
+        }
+    }
+    if (!rc) rc = orc_embed_at(m, seq, toks, pos, a);
+    if (!rc) rc = orc_forward(m, P->pre, 0, pre_e, seq, a, pos, mask, b);
+    if (is_prompt) P->pre->committed = P->pre->len;
+    if (!rc) {
+        const int req_f32 = P->dc.wire_f32;
+        const int resp_f32 = P->dc.server_dtype < 0 ? req_f32 : P->dc.server_dtype;
+        wire_pass(b, (size_t)seq * H, req_f32, &P->clamped);
+        if (is_prompt) {
+            P->mid->len = 0;
+            P->mid->committed = 0;
+        } else {
+            const int send_keep = P->first_step_done;
+            if ((send_keep && nkeep > 0) || P->mid->len - P->mid->committed > 0)
+                rc = orc_bank_resolve(P->mid, keep, send_keep ? nkeep : 0);
+        }
+        if (!rc) rc = orc_forward(m, P->mid, pre_e, suf_b, seq, b, pos, mask, a);
+        if (is_prompt) P->mid->committed = P->mid->len;
+        if (!rc) wire_pass(a, (size_t)seq * H, resp_f32, &P->clamped);
+    }
+    if (!rc) rc = orc_forward(m, P->suf, suf_b, L, seq, a, pos, mask, b);
+    if (is_prompt) P->suf->committed = P->suf->len;
+    if (!rc) rc = orc_finalize(m, seq, b, logits);
+    if (!is_prompt) P->first_step_done = 1;
+    free(a);
+    free(b);
+    return rc;
+}
+
+int orc_decode(const orc_model* m, const orc_decode_cfg* dc, orc_pool* pool_in, const int* prompt,
+               int n, int max_new, int* out_tokens, float* out_logits, int* step_batch,
+               int* step_accepted, orc_decode_stats* stats) {
+    const orc_cfg* c = &m->c;
+    const int V = c->vocab_size, max_seq = c->max_seq_len;
+    if (dc->prefix_layers < 1 || dc->suffix_layers < 1)
+        return err(K_CONFIG, "prefix and suffix must each host >= 1 layer");
+    if (dc->prefix_layers + dc->suffix_layers >= c->n_layers)
+        return err(K_CONFIG, "prefix + suffix must leave a non-empty middle range");
+    if (dc->mode == 2) {
+        if (dc->ngram_n < 2) return err(K_CONFIG, "ngram_n must be >= 2");
+        if (dc->window_w < dc->ngram_n) return err(K_CONFIG, "window_w must be >= ngram_n");
+        if (dc->max_candidates_g < 0) return err(K_CONFIG, "max_candidates_g must be >= 0");
+    }
+    if (max_new == 0) return 0;
+    if (n <= 0) return err(K_INPUT, "prompt must be non-empty");
+    if (n > max_seq) return err(K_CAPACITY, "prompt exceeds max_seq_len");
+
+    pipe_t P = {m, *dc, NULL, NULL, NULL, 0, 0};
+    orc_bank_new(m, 0, dc->prefix_layers, &P.pre);
+    orc_bank_new(m, dc->prefix_layers, c->n_layers - dc->suffix_layers, &P.mid);
+    orc_bank_new(m, c->n_layers - dc->suffix_layers, c->n_layers, &P.suf);
+    orc_pool* pool = pool_in;
+    if (!pool && dc->mode == 2) orc_pool_new(dc->ngram_n, (size_t)dc->pool_capacity, &pool);
+
+    const int Bmax = 1 + dc->window_w + dc->max_candidates_g * (dc->ngram_n - 1) + n;
+    float* logits = malloc(sizeof(float) * (size_t)Bmax * V);
+    float* mask = malloc(sizeof(float) * (size_t)Bmax * (max_seq + Bmax));
+    int* toks = malloc(sizeof(int) * Bmax);
+    int* pos = malloc(sizeof(int) * Bmax);
+    int* amax = malloc(sizeof(int) * Bmax);
+    int* keep = malloc(sizeof(int) * Bmax);
+    int nkeep = 0, ntok = 0, steps = 0, committed_total = 0;
+    int rc = 0;
+
+    /* prefill (client.cpp:120-167) */
+    for (int i = 0; i < n; ++i) pos[i] = i;
+    orc_build_causal_mask(n, 0, mask);
+    rc = pipe_run(&P, n, prompt, pos, mask, NULL, 0, 1, logits);
+    if (!rc) {
+        out_tokens[ntok] = orc_argmax(logits + (size_t)(n - 1) * V, V);
+        if (out_logits) memcpy(out_logits, logits + (size_t)(n - 1) * V, sizeof(float) * V);
+        ++ntok;
+    }
+    int total = n + 1;
+    const int W = dc->window_w, NG = dc->ngram_n;
+    int window[256];
+    for (int i = 0; i < W && i < 256; ++i) window[i] = ntok ? out_tokens[0] : 0;
+
+    while (!rc && ntok < max_new) {
+        const int ctx = total - 1;
+        int B = 1;
+        int ncand = 0, cand_begin[64];
+        int cands[64 * 16];
+        int active_w = 0;
+        if (dc->mode == 0) { /* decode_sequential :111-139 */
+            toks[0] = out_tokens[ntok - 1];
+            pos[0] = ctx;
+            orc_build_causal_mask(1, ctx, mask);
+        } else { /* decode_lookahead_with_pool :235-293 */
+            ncand = orc_pool_lookup(pool, out_tokens[ntok - 1], dc->max_candidates_g, cands);
+            active_w = W;
+            const int cl = NG - 1;
+#define BATCH() (1 + active_w + ncand * cl)
+            while (ncand > 0 && ctx + BATCH() > max_seq) --ncand;
+            while (active_w > 1 && ctx + BATCH() > max_seq) --active_w;
+            B = BATCH();
+#undef BATCH
+            toks[0] = out_tokens[ntok - 1];
+            pos[0] = ctx;
+            for (int i = 0; i < active_w; ++i) {
+                toks[1 + i] = window[i];
+                pos[1 + i] = total + i;
+            }
+            int row = 1 + active_w;
+            for (int bb = 0; bb < ncand; ++bb) {
+                cand_begin[bb] = row;
+                for (int j = 0; j < cl; ++j) {
+                    toks[row + j] = cands[bb * cl + j];
+                    pos[row + j] = total + j;
+                }
+                row += cl;
+            }
+            const int kv = ctx + B;
+            for (size_t e = 0; e < (size_t)B * kv; ++e) mask[e] = -INFINITY;
+            for (int j = 0; j <= ctx; ++j) mask[j] = 0.0f;
+            for (int i = 1; i <= active_w; ++i)
+                for (int j = 0; j <= ctx + i; ++j) mask[(size_t)i * kv + j] = 0.0f;
+            for (int bb = 0; bb < ncand; ++bb)
+                for (int j = 0; j < cl; ++j) {
+                    const int r = cand_begin[bb] + j;
+                    for (int cc = 0; cc <= ctx; ++cc) mask[(size_t)r * kv + cc] = 0.0f;
+                    for (int p2 = 0; p2 <= j; ++p2) mask[(size_t)r * kv + ctx + cand_begin[bb] + p2] = 0.0f;
+                }
+        }
+        rc = pipe_run(&P, B, toks, pos, mask, keep, nkeep, 0, logits);
+        if (rc) break;
+        for (int i = 0; i < B; ++i) amax[i] = orc_argmax(logits + (size_t)i * V, V);
+        if (step_batch) step_batch[steps] = B;
+        int commit_n;
+        if (dc->mode == 0) {
+            out_tokens[ntok] = amax[0];
+            if (out_logits) memcpy(out_logits + (size_t)ntok * V, logits, sizeof(float) * V);
+            ++ntok;
+            commit_n = 1;
+            total += 1;
+            keep[0] = 0;
+            nkeep = 1;
+        } else { /* :296-344 */
+            const int anchor = amax[0];
+            int best_c[64], best_rows[64];
+            int best = orc_verify_greedy_ids(amax, 1, window, active_w, anchor, best_c);
+            for (int i = 1; i <= best; ++i) best_rows[i - 1] = i;
+            for (int bb = 0; bb < ncand; ++bb) {
+                int vc[64];
+                const int acc = orc_verify_greedy_ids(amax, cand_begin[bb], cands + bb * (NG - 1),
+                                                      NG - 1, anchor, vc);
+                if (acc > best) {
+                    best = acc;
+                    memcpy(best_c, vc, sizeof(int) * (size_t)(acc + 1));
+                    for (int j = 0; j < acc; ++j) best_rows[j] = cand_begin[bb] + j;
+                }
+            }
+            const int room = max_new - ntok;
+            commit_n = best + 1 < room ? best + 1 : room;
+            for (int i = 0; i < commit_n; ++i) {
+                out_tokens[ntok + i] = best_c[i];
+                if (out_logits) {
+                    const int r = i == 0 ? 0 : best_rows[i - 1];
+                    memcpy(out_logits + (size_t)(ntok + i) * V, logits + (size_t)r * V, sizeof(float) * V);
+                }
+            }
+            ntok += commit_n;
+            total += commit_n;
+            keep[0] = 0;
+            for (int i = 0; i < best; ++i) keep[1 + i] = best_rows[i];
+            nkeep = best + 1;
+            int curw[256];
+            curw[0] = anchor;
+            for (int i = 1; i < active_w; ++i) curw[i] = amax[i];
+            orc_pool_update(pool, window, curw, active_w);
+            const int adv = best + 1;
+            int preds[257];
+            preds[0] = anchor;
+            for (int i = 0; i < active_w; ++i) preds[i + 1] = amax[1 + i];
+            for (int i = 0; i < W; ++i) window[i] = preds[adv + i < active_w ? adv + i : active_w];
+        }
+        if (step_accepted) step_accepted[steps] = commit_n;
+        committed_total += commit_n;
+        ++steps;
+    }
+    if (stats) {
+        stats->steps = steps;
+        stats->tokens_committed = committed_total;
+        stats->clamped = P.clamped;
+    }
+    if (!pool_in) orc_pool_free(pool);
+    orc_bank_free(P.pre);
+    orc_bank_free(P.mid);
+    orc_bank_free(P.suf);
+    free(logits); free(mask); free(toks); free(pos); free(amax); free(keep);
+    return rc;
+}

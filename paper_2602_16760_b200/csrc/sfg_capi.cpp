@@ -1,0 +1,298 @@
+// extern "C" boundary (include/sfg.h): status codes = ErrorKind + 1, the
+// thread-local message is the exact text the reference would throw.
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/sfg.h"
+#include "sfg_client.h"
+#include "sfg_engine.h"
+#include "sfg_server.h"
+#include "sfg_wire.h"
+
+using namespace sfg;
+
+namespace {
+thread_local std::string g_err;
+thread_local std::vector<uint8_t> g_resp;
+
+int32_t fail(const Error& e) {
+    g_err = e.what();
+    return static_cast<int32_t>(e.kind());
+}
+int32_t fail_other(const std::exception& e) {
+    g_err = std::string("internal: ") + e.what();
+    return SFG_ERR_INTERNAL;
+}
+}  // namespace
+
+#define SFG_GUARD(...)                      \
+    try {                                   \
+        __VA_ARGS__;                        \
+        return SFG_OK;                      \
+    } catch (const Error& e) {              \
+        return fail(e);                     \
+    } catch (const std::exception& e) {     \
+        return fail_other(e);               \
+    }
+
+struct sfg_engine { std::unique_ptr<Engine> e; };
+struct sfg_bank { std::unique_ptr<Bank> b; sfg_engine* eng; };
+struct sfg_server { std::unique_ptr<Server> s; double (*clock)(void*) = nullptr; void* clock_ctx = nullptr; };
+struct sfg_client { std::unique_ptr<Client> c; };
+struct sfg_pool { std::unique_ptr<Pool> p; };
+
+extern "C" {
+
+const char* sfg_last_error(void) { return g_err.c_str(); }
+const char* sfg_version(void) { return "sfg 0.1 (sm_100a)"; }
+
+static int32_t make_engine(const sfg_model_config* cfg, const sfg_engine_options* opt, const float* params,
+                           sfg_engine** out) {
+    SFG_GUARD({
+        if (!cfg || !opt || !out) throw Error(Kind::input, "null argument");
+        auto* h = new sfg_engine;
+        try {
+            h->e = std::make_unique<Engine>(ModelCfg::from_c(*cfg), *opt, params);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    })
+}
+
+int32_t sfg_engine_create_seeded(const sfg_model_config* cfg, const sfg_engine_options* opt, sfg_engine** out) {
+    return make_engine(cfg, opt, nullptr, out);
+}
+int32_t sfg_engine_create_from_params(const sfg_model_config* cfg, const sfg_engine_options* opt,
+                                      const float* params, sfg_engine** out) {
+    if (!params) {
+        g_err = "input: null parameter array";
+        return SFG_ERR_INPUT;
+    }
+    return make_engine(cfg, opt, params, out);
+}
+void sfg_engine_destroy(sfg_engine* eng) { delete eng; }
+int64_t sfg_engine_weight_bytes(const sfg_engine* eng) { return eng ? eng->e->weight_bytes() : 0; }
+
+int32_t sfg_bank_create(sfg_engine* eng, int32_t lb, int32_t le, sfg_bank** out) {
+    SFG_GUARD({
+        auto* b = new sfg_bank;
+        b->eng = eng;
+        try {
+            b->b = std::make_unique<Bank>(*eng->e, lb, le);
+        } catch (...) {
+            delete b;
+            throw;
+        }
+        *out = b;
+    })
+}
+void sfg_bank_destroy(sfg_bank* b) { delete b; }
+int32_t sfg_bank_resolve(sfg_bank* b, const int32_t* keep, int32_t n) { SFG_GUARD(b->b->resolve(keep, n)) }
+int32_t sfg_bank_crop(sfg_bank* b, int32_t pos) { SFG_GUARD(b->b->crop(pos)) }
+void sfg_bank_mark_committed(sfg_bank* b, int32_t c) { b->b->mark_committed(c); }
+void sfg_bank_reset(sfg_bank* b) { b->b->reset(); }
+void sfg_bank_state(const sfg_bank* b, int32_t* len, int32_t* committed) {
+    *len = b->b->len();
+    *committed = b->b->committed_len();
+}
+int32_t sfg_bank_read_kv(sfg_bank* b, int32_t layer, int32_t head, int32_t pos, float* k, float* v) {
+    SFG_GUARD(b->b->read_kv(layer, head, pos, k, v))
+}
+
+int32_t sfg_forward_layers(sfg_engine* eng, sfg_bank* b, int32_t lb, int32_t le, int32_t seq, const float* hidden,
+                           const int32_t* positions, const float* mask, float* out) {
+    SFG_GUARD(eng->e->forward_host(*b->b, lb, le, seq, hidden, positions, mask, out))
+}
+int32_t sfg_embed_at(sfg_engine* eng, int32_t seq, const int32_t* ids, const int32_t* positions, float* out) {
+    SFG_GUARD(eng->e->embed_host(seq, ids, positions, out))
+}
+int32_t sfg_finalize(sfg_engine* eng, int32_t seq, const float* hidden, float* logits) {
+    SFG_GUARD(eng->e->finalize_host(seq, hidden, logits, nullptr))
+}
+int32_t sfg_finalize_argmax(sfg_engine* eng, int32_t seq, const float* hidden, int32_t* argmax) {
+    SFG_GUARD(eng->e->finalize_host(seq, hidden, nullptr, argmax))
+}
+
+int32_t sfg_server_create(sfg_engine* eng, const sfg_server_config* cfg, sfg_server** out) {
+    SFG_GUARD({
+        ServerCfg sc;
+        sc.layer_begin = cfg->layer_begin;
+        sc.layer_end = cfg->layer_end;
+        sc.session_expiry_s = cfg->session_expiry_s;
+        sc.max_sessions = cfg->max_sessions;
+        sc.response_dtype = cfg->response_dtype;
+        auto* s = new sfg_server;
+        try {
+            s->s = std::make_unique<Server>(*eng->e, sc);
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        *out = s;
+    })
+}
+void sfg_server_destroy(sfg_server* s) { delete s; }
+int32_t sfg_server_handle(sfg_server* s, const uint8_t* req, size_t n, const uint8_t** resp, size_t* resp_len) {
+    SFG_GUARD({
+        s->s->handle(req, n, g_resp);
+        *resp = g_resp.data();
+        *resp_len = g_resp.size();
+    })
+}
+size_t sfg_server_expire_sessions(sfg_server* s) { return s->s->expire_sessions(); }
+size_t sfg_server_session_count(sfg_server* s) { return s->s->session_count(); }
+int32_t sfg_server_session_view(sfg_server* s, const char* sid, int32_t* len, int32_t* committed, int32_t* prov) {
+    int a = 0, b = 0, c = 0;
+    if (!s->s->session_view(sid, &a, &b, &c)) return 0;
+    *len = a;
+    *committed = b;
+    *prov = c;
+    return 1;
+}
+void sfg_server_set_clock(sfg_server* s, double (*now_s)(void*), void* ctx) {
+    s->clock = now_s;
+    s->clock_ctx = ctx;
+    s->s->set_clock([s] { return s->clock(s->clock_ctx); });
+}
+
+static ClientCfg to_client_cfg(const sfg_client_config* cfg) {
+    ClientCfg cc;
+    cc.prefix_layers = cfg->prefix_layers;
+    cc.suffix_layers = cfg->suffix_layers;
+    cc.wire_dtype = cfg->wire_dtype;
+    cc.one_way_delay_ms = cfg->one_way_delay_ms;
+    return cc;
+}
+
+int32_t sfg_client_create(sfg_engine* local, const sfg_client_config* cfg, sfg_frame_handler handler, void* ctx,
+                          const char* sid, sfg_client** out) {
+    SFG_GUARD({
+        auto* c = new sfg_client;
+        try {
+            c->c = std::make_unique<Client>(*local->e, to_client_cfg(cfg), handler, ctx, nullptr, sid ? sid : "");
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    })
+}
+int32_t sfg_client_create_linked(sfg_engine* local, const sfg_client_config* cfg, sfg_server* server,
+                                 const char* sid, sfg_client** out) {
+    SFG_GUARD({
+        auto* c = new sfg_client;
+        try {
+            c->c = std::make_unique<Client>(*local->e, to_client_cfg(cfg), nullptr, nullptr, server->s.get(),
+                                            sid ? sid : "");
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    })
+}
+void sfg_client_destroy(sfg_client* c) { delete c; }
+
+int32_t sfg_client_prefill(sfg_client* c, const int32_t* prompt, int32_t n, int32_t* first, float* logits) {
+    SFG_GUARD({
+        const int t = c->c->prefill(prompt, n, logits);
+        if (first) *first = t;
+    })
+}
+
+int32_t sfg_client_decode_step(sfg_client* c, int32_t seq, const int32_t* tokens, const int32_t* positions,
+                               const float* mask, const int32_t* keep, int32_t n_keep, int32_t crop, float* logits,
+                               int32_t* argmax) {
+    SFG_GUARD({
+        std::optional<int> cr;
+        if (crop >= 0) cr = crop;
+        MaskRuns mr;
+        const MaskRuns* mp = nullptr;
+        if (mask) {
+            // the kv extent the mask must cover is known only after keep/crop
+            // are applied on the local banks; mirror that computation here.
+            Bank& pb = c->c->prefix();
+            int len = pb.len(), committed = pb.committed_len();
+            if (n_keep > 0 || len - committed > 0) len = committed + n_keep;
+            if (cr) len = *cr;
+            mr = runs_from_dense(mask, seq, len + seq);
+            mp = &mr;
+        }
+        c->c->decode_step(seq, tokens, positions, mp, keep, n_keep, cr, logits != nullptr);
+        if (logits) c->c->fetch_logits(seq, logits);
+        if (argmax) c->c->fetch_argmax(seq, argmax);
+    })
+}
+
+int32_t sfg_decode(sfg_client* c, const sfg_decode_config* cfg, sfg_pool* pool, const int32_t* prompt, int32_t n,
+                   int32_t max_new, int32_t* out_tokens, float* committed_logits, int32_t* step_batch,
+                   int32_t* step_accepted, sfg_decode_stats* stats) {
+    SFG_GUARD({
+        Client::DecodeCfg dc;
+        dc.mode = cfg->mode;
+        dc.window_w = cfg->window_w;
+        dc.ngram_n = cfg->ngram_n;
+        dc.max_candidates_g = cfg->max_candidates_g;
+        dc.pool_capacity = static_cast<size_t>(cfg->pool_capacity);
+        Client::DecodeOut o;
+        c->c->decode(dc, pool ? pool->p.get() : nullptr, prompt, n, max_new, committed_logits != nullptr, o);
+        std::memcpy(out_tokens, o.tokens.data(), sizeof(int32_t) * o.tokens.size());
+        if (committed_logits) std::memcpy(committed_logits, o.logits.data(), sizeof(float) * o.logits.size());
+        if (step_batch) std::memcpy(step_batch, o.step_batch.data(), sizeof(int32_t) * o.step_batch.size());
+        if (step_accepted) std::memcpy(step_accepted, o.step_accepted.data(), sizeof(int32_t) * o.step_accepted.size());
+        if (stats) {
+            stats->steps = o.steps;
+            stats->tokens_committed = o.committed;
+            stats->wall_seconds = o.wall_s;
+            stats->match_rate = o.match_rate;
+            stats->clamped = c->c->clamped();
+        }
+    })
+}
+
+int32_t sfg_client_last_profile(sfg_client* c, sfg_step_profile* out) {
+    const StepProfile& p = c->c->last_profile();
+    out->step_ms = p.step_ms;
+    out->server_ms = p.server_ms;
+    out->local_ms = p.local_ms;
+    out->launches = p.launches;
+    out->batch = p.batch;
+    return SFG_OK;
+}
+
+static int g_graphs = 1;
+void sfg_set_graphs(int32_t enabled) { g_graphs = enabled; }
+
+int32_t sfg_pool_create(int32_t n, size_t cap, sfg_pool** out) {
+    SFG_GUARD({
+        auto* p = new sfg_pool;
+        try {
+            p->p = std::make_unique<Pool>(n, cap);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    })
+}
+void sfg_pool_destroy(sfg_pool* p) { delete p; }
+int32_t sfg_pool_update(sfg_pool* p, const int32_t* prev, const int32_t* cur, int32_t w) {
+    SFG_GUARD(p->p->update(prev, cur, w))
+}
+int32_t sfg_pool_lookup(sfg_pool* p, int32_t key, int32_t max_c, int32_t* out) {
+    std::vector<std::vector<int32_t>> hits;
+    const int n = p->p->lookup(key, max_c, hits);
+    int off = 0;
+    for (auto& h : hits)
+        for (int32_t t : h) out[off++] = t;
+    return n;
+}
+size_t sfg_pool_size(const sfg_pool* p) { return p->p->size(); }
+
+uint16_t sfg_f32_to_f16(float v, uint64_t* clamped) { return wire::f32_to_f16_bits(v, clamped); }
+float sfg_f16_to_f32(uint16_t b) { return wire::f16_bits_to_f32(b); }
+
+}  // extern "C"

@@ -1,0 +1,215 @@
+// Host-side engine (C++20): weights resident on one B200, KV-cache banks,
+// the layer-executor orchestration, and the error taxonomy.  This is the
+// B200 counterpart of tinyformer.{hpp,cpp}; the server (sfg_server.cpp) and
+// the local client (sfg_client.cpp) are built on it, and sfg_capi.cpp
+// exposes everything through include/sfg.h.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sfg.h"
+#include "sfg_kernels.h"
+
+namespace sfg {
+
+// splitf::ErrorKind (error.hpp:10-21); the numeric value is the C status.
+enum class Kind : int32_t {
+    config = 1, input, protocol, transport, capacity, session, numeric, training, decomposition,
+    internal
+};
+const char* kind_name(Kind k);
+
+// Mirrors splitf::SplitError: what() == "<category>: <msg>".
+class Error : public std::runtime_error {
+public:
+    Error(Kind k, const std::string& msg) : std::runtime_error(std::string(kind_name(k)) + ": " + msg), kind_(k) {}
+    Kind kind() const { return kind_; }
+
+private:
+    Kind kind_;
+};
+
+[[noreturn]] void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+#define SFG_CUDA(x)                                                            \
+    do {                                                                       \
+        cudaError_t e_ = (x);                                                  \
+        if (e_ != cudaSuccess) ::sfg::cuda_fail(e_, #x, __FILE__, __LINE__);   \
+    } while (0)
+
+struct ModelCfg {
+    int vocab_size, n_layers, hidden_dim, n_heads, n_kv_heads, head_dim, ffn_dim, max_seq_len;
+    float rope_base, rms_eps;
+    uint64_t seed;
+    int q_dim() const { return n_heads * head_dim; }
+    int kv_dim() const { return n_kv_heads * head_dim; }
+    void validate() const;  // ModelConfig::validate, tinyformer.cpp:102-121
+    static ModelCfg from_c(const sfg_model_config& c);
+};
+
+// Device tensors of one decoder layer in the reference layout ([in x out]).
+struct LayerWeights {
+    float* attn_norm = nullptr;
+    void* wq = nullptr;
+    void* wk = nullptr;
+    void* wv = nullptr;
+    void* wo = nullptr;
+    float* ffn_norm = nullptr;
+    void* w_gate = nullptr;
+    void* w_up = nullptr;
+    void* w_down = nullptr;
+    // FAST-mode operand layouts (sfg_fast.cu), built from the above at load.
+    void* f_qkv = nullptr;    // [qd+2kvd x H] K-major bf16 (rows = output features)
+    void* f_o = nullptr;      // [H x qd]
+    void* f_gu = nullptr;     // [2F x H] gate/up interleaved by 64-row tiles
+    void* f_down = nullptr;   // [H x F]
+    bool hosted = false;
+};
+
+// Growable device workspace for one executor stream.
+struct Workspace {
+    int cap_rows = 0, cap_runs = 0, cap_logit_rows = 0;
+    float *h = nullptr, *xn = nullptr, *q = nullptr, *att = nullptr, *act = nullptr;
+    float* logits = nullptr;
+    int32_t *pos = nullptr, *ids = nullptr, *argmax = nullptr, *keep = nullptr, *row_off = nullptr;
+    MaskRun* runs = nullptr;
+    uint32_t* status = nullptr;
+    unsigned long long* clamped = nullptr;
+    void* wire = nullptr;          // packed wire rows [cap_rows x H] (up to 4 B each)
+    void* fast = nullptr;          // FAST-mode scratch (split operands, partials)
+    size_t fast_bytes = 0;
+    void* pinned = nullptr;        // host staging
+    size_t pinned_bytes = 0;
+    void release();
+};
+
+class Engine;
+
+// CacheBank (tinyformer.hpp:131-156) with device-resident fp32 K/V:
+// K and V are each [layer][kv_head][max_len][head_dim].
+class Bank {
+public:
+    Bank(Engine& eng, int layer_begin, int layer_end);
+    ~Bank();
+    Bank(const Bank&) = delete;
+    Bank& operator=(const Bank&) = delete;
+
+    int layer_begin() const { return lb_; }
+    int layer_end() const { return le_; }
+    int len() const { return lb_ == le_ ? 0 : len_; }
+    int committed_len() const { return committed_; }
+    int provisional() const { return len() - committed_; }
+    void mark_committed(int c) { committed_ = c; }
+    void set_len(int l) { len_ = l; }
+    void reset() { len_ = 0; committed_ = 0; }
+    void resolve(const int32_t* keep, int n);  // tinyformer.cpp:282-308
+    void crop(int pos);                        // tinyformer.cpp:310-316
+    float* kslab(int layer) const;
+    float* vslab(int layer) const;
+    void read_kv(int layer, int head, int pos, float* k, float* v);
+    cudaStream_t stream() const { return stream_; }
+    Workspace& ws() { return ws_; }
+    Engine& engine() { return eng_; }
+
+private:
+    Engine& eng_;
+    int lb_, le_;
+    int len_ = 0, committed_ = 0;
+    float* k_ = nullptr;
+    float* v_ = nullptr;
+    size_t slab_elems_ = 0;
+    cudaStream_t stream_ = nullptr;
+    Workspace ws_;
+};
+
+// Visibility of the batch rows, as compacted runs (see MaskRun).
+struct MaskRuns {
+    std::vector<int32_t> row_off;  // rows + 1
+    std::vector<MaskRun> runs;
+    bool any_empty_row = false;
+};
+// Causal prefix law: row i sees committed + i + 1 columns (tinyformer.cpp:229-241).
+MaskRuns causal_runs(int rows, int committed);
+// Dense fp32 additive mask [rows x kv] with -inf = masked.
+MaskRuns runs_from_dense(const float* mask, int rows, int kv);
+
+class Engine {
+public:
+    Engine(const ModelCfg& cfg, const sfg_engine_options& opt, const float* params);
+    ~Engine();
+
+    const ModelCfg& cfg() const { return cfg_; }
+    const sfg_engine_options& opt() const { return opt_; }
+    int device() const { return opt_.device; }
+    bool fast() const { return opt_.math == SFG_MATH_FAST; }
+    int wt() const { return opt_.weight_dtype == SFG_WEIGHTS_F32 ? W_F32 : W_BF16; }
+    int64_t weight_bytes() const { return weight_bytes_; }
+    Dims dims() const;
+    const LayerWeights& layer(int i) const { return layers_[i]; }
+
+    // Ensure ws holds `rows` rows / `runs` runs / `logit_rows` logit rows.
+    void ensure_ws(Workspace& ws, int rows, int runs, int logit_rows);
+
+    // Layer executor over device-resident rows (ws.h holds the input and
+    // receives the output).  ws.pos / ws.row_off / ws.runs must be loaded.
+    // Returns kernels launched.  Host-side checks are the caller's job.
+    int forward_device(Bank& b, int lb, int le, int rows, Workspace& ws, cudaStream_t s);
+    // finalize (tinyformer.cpp:510-526) + optional argmax on ws.h rows.
+    int head_device(int rows, Workspace& ws, bool want_logits, bool want_argmax, cudaStream_t s);
+    int embed_device(int rows, Workspace& ws, cudaStream_t s);  // ws.ids -> ws.h
+
+    // Host-buffer entry points (seam 2).
+    void forward_host(Bank& b, int lb, int le, int seq, const float* h, const int32_t* pos,
+                      const float* mask, float* out);
+    void embed_host(int seq, const int32_t* ids, const int32_t* pos, float* out);
+    void finalize_host(int seq, const float* h, float* logits, int32_t* argmax);
+
+    const float* rope_cos() const { return rope_cos_; }
+    const float* rope_sin() const { return rope_sin_; }
+
+    std::mutex& mutex() { return mu_; }
+    Workspace& ws() { return ws_; }
+    cudaStream_t stream() const { return stream_; }
+
+private:
+    void load(const float* params);
+    void upload_tensor(const float* src, size_t n, void** dst, int wt);
+    void build_fast_layouts();
+
+    ModelCfg cfg_;
+    sfg_engine_options opt_;
+    std::vector<LayerWeights> layers_;
+    void* embedding_ = nullptr;
+    float* final_norm_ = nullptr;
+    void* lm_head_ = nullptr;
+    void* f_lm_head_ = nullptr;
+    float* rope_cos_ = nullptr;
+    float* rope_sin_ = nullptr;
+    int64_t weight_bytes_ = 0;
+    std::vector<void*> allocs_;
+    float* staging_ = nullptr;
+    size_t staging_elems_ = 0;
+    cudaStream_t stream_ = nullptr;
+    Workspace ws_;
+    std::mutex mu_;
+};
+
+// Scoped device selection.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev);
+    ~DeviceGuard();
+};
+
+// FAST-mode layer executor (sfg_fast.cu).
+int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, int prior,
+                       cudaStream_t s);
+size_t fast_workspace_bytes(const ModelCfg& c, int rows);
+void fast_build_layer(Engine& e, LayerWeights& L, cudaStream_t s);
+
+}  // namespace sfg

@@ -1,0 +1,372 @@
+// GPU ServerEngine — state machine of server.cpp:173-265 / PROTOCOL.md with
+// the forward on device.  Host work is limited to framing, protocol
+// validation and bookkeeping; hidden rows are unpacked, transformed and
+// packed on the B200.
+#include "sfg_server.h"
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+namespace sfg {
+
+static double steady_seconds() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+Server::Server(Engine& eng, const ServerCfg& cfg) : eng_(eng), cfg_(cfg), now_s_(steady_seconds) {
+    const ModelCfg& m = eng.cfg();
+    // ServerEngine ctor checks (server.cpp:26-39)
+    if (cfg_.layer_begin <= 0 || cfg_.layer_end >= m.n_layers || cfg_.layer_begin >= cfg_.layer_end)
+        throw Error(Kind::config, "hosted layer range must be non-empty and strictly inside the model");
+    if (cfg_.session_expiry_s <= 0) throw Error(Kind::config, "session expiry must be positive");
+    if (cfg_.max_sessions < 1) throw Error(Kind::config, "max_sessions must be >= 1");
+    for (int l = cfg_.layer_begin; l < cfg_.layer_end; ++l)
+        if (!eng.layer(l).hosted) throw Error(Kind::config, "engine does not host the server's layer range");
+}
+
+size_t Server::expire_sessions() {
+    const double now = now_s_();
+    std::lock_guard<std::mutex> lk(table_mutex_);
+    size_t removed = 0;
+    for (auto it = sessions_.begin(); it != sessions_.end();) {
+        if (now - it->second->last_active > cfg_.session_expiry_s) {
+            it = sessions_.erase(it);
+            ++removed;
+        } else {
+            ++it;
+        }
+    }
+    return removed;
+}
+
+size_t Server::session_count() const {
+    std::lock_guard<std::mutex> lk(table_mutex_);
+    return sessions_.size();
+}
+
+bool Server::session_view(const std::string& id, int* len, int* committed, int* prov) const {
+    std::lock_guard<std::mutex> lk(table_mutex_);
+    auto it = sessions_.find(id);
+    if (it == sessions_.end()) return false;
+    *len = it->second->bank->len();
+    *committed = it->second->bank->committed_len();
+    *prov = it->second->bank->provisional();
+    return true;
+}
+
+// find_session with lazy expiry (server.cpp:75-85)
+std::shared_ptr<Server::Session> Server::find_session(const std::string& id) {
+    const double now = now_s_();
+    std::lock_guard<std::mutex> lk(table_mutex_);
+    auto it = sessions_.find(id);
+    if (it == sessions_.end()) return nullptr;
+    if (now - it->second->last_active > cfg_.session_expiry_s) {
+        sessions_.erase(it);
+        return nullptr;
+    }
+    return it->second;
+}
+
+// create_or_reset_session (server.cpp:87-99)
+std::shared_ptr<Server::Session> Server::create_or_reset_session(const std::string& id) {
+    std::lock_guard<std::mutex> lk(table_mutex_);
+    auto it = sessions_.find(id);
+    if (it != sessions_.end()) return it->second;
+    if (static_cast<int>(sessions_.size()) >= cfg_.max_sessions) throw Error(Kind::capacity, "session table full");
+    auto s = std::make_shared<Session>();
+    s->bank = std::make_unique<Bank>(eng_, cfg_.layer_begin, cfg_.layer_end);
+    sessions_[id] = s;
+    return s;
+}
+
+MaskRuns runs_from_f16_mask(const uint16_t* m, int q, int kv) {
+    // mask_from_frame entry validation (server.cpp:165-169): only 0 (either
+    // sign) and -inf are legal.
+    const size_t n = static_cast<size_t>(q) * kv;
+    bool ok = true;
+    for (size_t i = 0; i < n; ++i) {
+        const uint16_t b = m[i];
+        ok &= (b == 0x0000u) | (b == 0x8000u) | (b == 0xfc00u);
+    }
+    if (!ok) throw Error(Kind::protocol, "mask entries must be 0 or -inf");
+    MaskRuns r;
+    r.row_off.resize(q + 1);
+    for (int i = 0; i < q; ++i) {
+        r.row_off[i] = static_cast<int32_t>(r.runs.size());
+        const uint16_t* row = m + static_cast<size_t>(i) * kv;
+        int j = 0;
+        bool any = false;
+        while (j < kv) {
+            if (row[j] == 0xfc00u) {
+                ++j;
+                continue;
+            }
+            int e = j + 1;
+            while (e < kv && row[e] != 0xfc00u) ++e;
+            r.runs.push_back(MaskRun{j, e, 0.0f, 0});
+            any = true;
+            j = e;
+        }
+        if (!any) r.any_empty_row = true;
+    }
+    r.row_off[q] = static_cast<int32_t>(r.runs.size());
+    return r;
+}
+
+void Server::error_frame(const std::string& sid, const std::string& msg, std::vector<uint8_t>& resp) {
+    wire::Header h;
+    h.kind = wire::FrameKind::error;
+    h.session_id = sid;
+    h.shape = {0};
+    h.err = msg;
+    wire::encode(h, nullptr, 0, nullptr, 0, resp);
+}
+
+void Server::handle(const uint8_t* req, size_t n, std::vector<uint8_t>& resp) {
+    wire::FrameView f;
+    try {
+        f = wire::decode(req, n);
+    } catch (const Error& e) {
+        error_frame("", e.what(), resp);
+        return;
+    }
+    const std::string sid = f.h.session_id;
+    try {
+        handle_frame(f, resp);
+    } catch (const Error& e) {
+        error_frame(sid, e.what(), resp);
+    } catch (const std::exception& e) {
+        error_frame(sid, std::string("internal: ") + e.what(), resp);
+    }
+}
+
+namespace {
+
+struct HiddenCheck {
+    int seq = 0;
+    std::vector<int32_t> pos;
+};
+
+// frame_to_hidden (server.cpp:101-133), validation only: the rows are
+// decoded on device.  Non-finite detection reads the raw binary16/32
+// exponent fields, which is exactly isfinite() of the decoded value.
+HiddenCheck frame_to_hidden(const wire::FrameView& f, const ModelCfg& c) {
+    const auto& h = f.h;
+    if (h.shape.size() != 2) throw Error(Kind::protocol, "hidden tensor must be rank 2 [seq, hidden]");
+    const int seq = static_cast<int>(h.shape[0]);
+    const int dim = static_cast<int>(h.shape[1]);
+    if (dim != c.hidden_dim) throw Error(Kind::protocol, "hidden dim mismatch");
+    if (seq < 1) throw Error(Kind::protocol, "empty batch");
+    if (static_cast<int>(h.pos.size()) != seq) throw Error(Kind::protocol, "positions must match the batch seq dim");
+    HiddenCheck hc;
+    hc.seq = seq;
+    hc.pos.reserve(seq);
+    for (int64_t p : h.pos) {
+        if (p < 0 || p >= c.max_seq_len) throw Error(Kind::capacity, "position exceeds max_seq_len");
+        hc.pos.push_back(static_cast<int32_t>(p));
+    }
+    const size_t n = static_cast<size_t>(seq) * dim;
+    bool finite = true;
+    if (h.dtype == wire::Dtype::f16) {
+        const uint16_t* v = reinterpret_cast<const uint16_t*>(f.tensor);
+        for (size_t i = 0; i < n; ++i) finite &= (v[i] & 0x7c00u) != 0x7c00u;
+    } else {
+        const uint32_t* v = reinterpret_cast<const uint32_t*>(f.tensor);
+        for (size_t i = 0; i < n; ++i) finite &= (v[i] & 0x7f800000u) != 0x7f800000u;
+    }
+    if (!finite) throw Error(Kind::numeric, "non-finite hidden payload");
+    return hc;
+}
+
+// mask_from_frame (server.cpp:148-171)
+MaskRuns mask_from_frame(const wire::FrameView& f, int cache_len, int seq) {
+    const auto& h = f.h;
+    if (!h.mask_shape) return causal_runs(seq, cache_len);
+    const auto& ms = *h.mask_shape;
+    if (ms.size() != 4 || ms[0] != 1 || ms[1] != 1) throw Error(Kind::protocol, "mask_shape must be [1, 1, q, kv]");
+    const int q = static_cast<int>(ms[2]), kv = static_cast<int>(ms[3]);
+    if (q != seq || kv != cache_len + seq)
+        throw Error(Kind::protocol, "mask shape does not match cache length plus batch");
+    return runs_from_f16_mask(reinterpret_cast<const uint16_t*>(f.mask), q, kv);
+}
+
+// forward_layers pre-compute checks that can fire after the mask
+// (tinyformer.cpp:390-392, 467-469).
+void forward_checks(const Bank& b, int seq, const MaskRuns& mr, int max_seq) {
+    if (b.len() + seq > max_seq) throw Error(Kind::capacity, "sequence exceeds max_seq_len");
+    if (mr.any_empty_row) throw Error(Kind::protocol, "mask row admits no attendable position");
+}
+
+// H2D of the launch metadata (positions + visibility runs) for one step.
+void upload_meta(Engine& e, Workspace& ws, const std::vector<int32_t>& pos, const MaskRuns& mr,
+                 cudaStream_t s) {
+    e.ensure_ws(ws, static_cast<int>(pos.size()), static_cast<int>(mr.runs.size()), 0);
+    char* pin = static_cast<char*>(ws.pinned);
+    // pinned layout: [pos | row_off | runs]; the copies complete before the
+    // host touches the staging buffer again (each step ends with a sync).
+    const size_t pb = sizeof(int32_t) * pos.size(), rb = sizeof(int32_t) * mr.row_off.size(),
+                 ub = sizeof(MaskRun) * mr.runs.size();
+    if (pb + rb + ub > ws.pinned_bytes) {
+        SFG_CUDA(cudaMemcpyAsync(ws.pos, pos.data(), pb, cudaMemcpyHostToDevice, s));
+        SFG_CUDA(cudaMemcpyAsync(ws.row_off, mr.row_off.data(), rb, cudaMemcpyHostToDevice, s));
+        SFG_CUDA(cudaMemcpyAsync(ws.runs, mr.runs.data(), ub, cudaMemcpyHostToDevice, s));
+        SFG_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    std::memcpy(pin, pos.data(), pb);
+    std::memcpy(pin + pb, mr.row_off.data(), rb);
+    std::memcpy(pin + pb + rb, mr.runs.data(), ub);
+    SFG_CUDA(cudaMemcpyAsync(ws.pos, pin, pb, cudaMemcpyHostToDevice, s));
+    SFG_CUDA(cudaMemcpyAsync(ws.row_off, pin + pb, rb, cudaMemcpyHostToDevice, s));
+    SFG_CUDA(cudaMemcpyAsync(ws.runs, pin + pb + rb, ub, cudaMemcpyHostToDevice, s));
+}
+
+}  // namespace
+
+void Server::handle_frame(const wire::FrameView& f, std::vector<uint8_t>& resp) {
+    const ModelCfg& c = eng_.cfg();
+    const auto kind = f.h.kind;
+    if (kind == wire::FrameKind::ping) {  // handle_ping (server.cpp:193-201)
+        wire::Header h;
+        h.kind = wire::FrameKind::response;
+        h.session_id = f.h.session_id;
+        h.shape = {0};
+        h.dtype = f.h.dtype;
+        h.srv_ms = 0.0;
+        wire::encode(h, nullptr, 0, nullptr, 0, resp);
+        return;
+    }
+    if (kind == wire::FrameKind::response || kind == wire::FrameKind::error)
+        throw Error(Kind::protocol, "response/error frames are not requests");
+    const bool prompt = kind == wire::FrameKind::prompt;
+
+    std::shared_ptr<Session> sess;
+    HiddenCheck hc;
+    if (prompt) {  // handle_prompt (server.cpp:203-224)
+        if (f.h.session_id.empty()) throw Error(Kind::protocol, "prompt frame requires a session_id");
+        hc = frame_to_hidden(f, c);
+        if (hc.seq > c.max_seq_len) throw Error(Kind::capacity, "prompt exceeds max_seq_len");
+        sess = create_or_reset_session(f.h.session_id);
+    } else {  // handle_step (server.cpp:226-265)
+        sess = find_session(f.h.session_id);
+        if (!sess) throw Error(Kind::session, "unknown or expired session: " + f.h.session_id);
+    }
+    std::lock_guard<std::mutex> lk(sess->mutex);
+    Bank& bank = *sess->bank;
+    if (prompt) {
+        bank.reset();
+    } else {
+        hc = frame_to_hidden(f, c);
+    }
+    const double t0 = steady_seconds();
+    if (!prompt) {
+        std::vector<int32_t> keep;
+        if (f.h.keep) {
+            keep.reserve(f.h.keep->size());
+            for (int64_t k : *f.h.keep) keep.push_back(static_cast<int32_t>(k));
+        }
+        if (!keep.empty() || bank.provisional() > 0) bank.resolve(keep.data(), static_cast<int>(keep.size()));
+        if (f.h.crop) {
+            const int64_t p = *f.h.crop;
+            if (p < 0 || p > bank.len()) throw Error(Kind::protocol, "crop position exceeds session length");
+            bank.crop(static_cast<int>(p));
+        }
+    }
+    const int seq = hc.seq;
+    MaskRuns mr = mask_from_frame(f, bank.len(), seq);
+    forward_checks(bank, seq, mr, c.max_seq_len);
+
+    // device: unpack -> middle layers -> pack
+    DeviceGuard g(eng_.device());
+    Workspace& ws = bank.ws();
+    cudaStream_t s = bank.stream();
+    const int in_f32 = f.h.dtype == wire::Dtype::f32;
+    const wire::Dtype out_dt = cfg_.response_dtype < 0 ? f.h.dtype
+                                                       : (cfg_.response_dtype == SFG_WIRE_F32 ? wire::Dtype::f32
+                                                                                              : wire::Dtype::f16);
+    const int n = seq * c.hidden_dim;
+    upload_meta(eng_, ws, hc.pos, mr, s);
+    SFG_CUDA(cudaMemcpyAsync(ws.wire, f.tensor, f.tensor_len, cudaMemcpyHostToDevice, s));
+    launch_unpack_rows(ws.wire, in_f32, n, ws.h, s);
+    SFG_CUDA(cudaMemsetAsync(ws.status, 0, sizeof(uint32_t), s));
+    eng_.forward_device(bank, cfg_.layer_begin, cfg_.layer_end, seq, ws, s);
+    launch_pack_rows(ws.h, out_dt == wire::Dtype::f32, n, ws.wire, nullptr, s);
+    SFG_CUDA(cudaGetLastError());
+    thread_local std::vector<uint8_t> payload;
+    const size_t out_bytes = static_cast<size_t>(n) * wire::width(out_dt);
+    payload.resize(out_bytes + 4);
+    uint32_t* st = reinterpret_cast<uint32_t*>(static_cast<char*>(ws.pinned) + ws.pinned_bytes - 64);
+    SFG_CUDA(cudaMemcpyAsync(st, ws.status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    SFG_CUDA(cudaMemcpyAsync(payload.data(), ws.wire, out_bytes, cudaMemcpyDeviceToHost, s));
+    SFG_CUDA(cudaStreamSynchronize(s));
+    if (*st & ST_EMPTY_ROW) throw Error(Kind::protocol, "mask row admits no attendable position");
+    bank.set_len(bank.len() + seq);
+    if (prompt) bank.mark_committed(bank.len());
+    sess->last_active = now_s_();
+    const double srv_ms = (steady_seconds() - t0) * 1000.0;
+
+    wire::Header h;  // hidden_to_response (server.cpp:135-146)
+    h.kind = wire::FrameKind::response;
+    h.session_id = f.h.session_id;
+    h.shape = {seq, c.hidden_dim};
+    h.dtype = out_dt;
+    h.srv_ms = srv_ms;
+    wire::encode(h, payload.data(), out_bytes, nullptr, 0, resp);
+}
+
+int Server::linked_step(const LinkedStep& st) {
+    const ModelCfg& c = eng_.cfg();
+    std::shared_ptr<Session> sess;
+    if (st.is_prompt) {
+        if (st.session_id->empty()) throw Error(Kind::protocol, "prompt frame requires a session_id");
+        for (int i = 0; i < st.seq; ++i)
+            if (st.pos[i] < 0 || st.pos[i] >= c.max_seq_len) throw Error(Kind::capacity, "position exceeds max_seq_len");
+        if (st.seq > c.max_seq_len) throw Error(Kind::capacity, "prompt exceeds max_seq_len");
+        sess = create_or_reset_session(*st.session_id);
+    } else {
+        sess = find_session(*st.session_id);
+        if (!sess) throw Error(Kind::session, "unknown or expired session: " + *st.session_id);
+    }
+    std::lock_guard<std::mutex> lk(sess->mutex);
+    Bank& bank = *sess->bank;
+    if (st.is_prompt) {
+        bank.reset();
+    } else {
+        for (int i = 0; i < st.seq; ++i)
+            if (st.pos[i] < 0 || st.pos[i] >= c.max_seq_len) throw Error(Kind::capacity, "position exceeds max_seq_len");
+        std::vector<int32_t> keep;
+        if (st.keep)
+            for (int64_t k : *st.keep) keep.push_back(static_cast<int32_t>(k));
+        if (!keep.empty() || bank.provisional() > 0) bank.resolve(keep.data(), static_cast<int>(keep.size()));
+        if (st.crop) {
+            if (*st.crop < 0 || *st.crop > bank.len()) throw Error(Kind::protocol, "crop position exceeds session length");
+            bank.crop(static_cast<int>(*st.crop));
+        }
+    }
+    MaskRuns causal;
+    const MaskRuns* mr = st.runs;
+    if (!mr) {
+        causal = causal_runs(st.seq, bank.len());
+        mr = &causal;
+    } else if (st.mask_q != st.seq || st.mask_kv != bank.len() + st.seq) {
+        throw Error(Kind::protocol, "mask shape does not match cache length plus batch");
+    }
+    forward_checks(bank, st.seq, *mr, c.max_seq_len);
+    DeviceGuard g(eng_.device());
+    Workspace& ws = bank.ws();
+    std::vector<int32_t> pos(st.pos, st.pos + st.seq);
+    upload_meta(eng_, ws, pos, *mr, st.stream);
+    const size_t bytes = sizeof(float) * st.seq * c.hidden_dim;
+    SFG_CUDA(cudaMemcpyAsync(ws.h, st.rows, bytes, cudaMemcpyDeviceToDevice, st.stream));
+    SFG_CUDA(cudaMemsetAsync(ws.status, 0, sizeof(uint32_t), st.stream));
+    int n = eng_.forward_device(bank, cfg_.layer_begin, cfg_.layer_end, st.seq, ws, st.stream);
+    SFG_CUDA(cudaMemcpyAsync(st.rows, ws.h, bytes, cudaMemcpyDeviceToDevice, st.stream));
+    SFG_CUDA(cudaGetLastError());
+    bank.set_len(bank.len() + st.seq);
+    if (st.is_prompt) bank.mark_committed(bank.len());
+    sess->last_active = now_s_();
+    return n;
+}
+
+}  // namespace sfg
