@@ -220,6 +220,8 @@ size_t sfg_pool_size(const sfg_pool* p);
 
 /* ── wire codec (wire.cpp:83-187), host reference implementation ───────── */
 uint16_t sfg_f32_to_f16(float v, uint64_t* clamped);
+/* self-test: device f32 -> binary16 -> f32 round trip of n host values */
+int32_t sfg_selftest_wire_roundtrip(const float* in, float* out, int32_t n, uint64_t* clamped);
 float sfg_f16_to_f32(uint16_t bits);
 
 /* ── measurement hooks (bench.py) ──────────────────────────────────────── */

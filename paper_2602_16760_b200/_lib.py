@@ -135,6 +135,7 @@ def lib() -> C.CDLL:
         "sfg_pool_size": (C.c_size_t, [vp]),
         "sfg_f32_to_f16": (C.c_uint16, [C.c_float, C.POINTER(C.c_uint64)]),
         "sfg_f16_to_f32": (C.c_float, [C.c_uint16]),
+        "sfg_selftest_wire_roundtrip": (i32, [f32p, f32p, i32, C.POINTER(C.c_uint64)]),
         "sfg_client_last_profile": (i32, [vp, C.POINTER(StepProfile)]),
         "sfg_set_graphs": (None, [i32]),
     }

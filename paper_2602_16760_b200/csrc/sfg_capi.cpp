@@ -292,6 +292,27 @@ int32_t sfg_pool_lookup(sfg_pool* p, int32_t key, int32_t max_c, int32_t* out) {
 }
 size_t sfg_pool_size(const sfg_pool* p) { return p->p->size(); }
 
+// Self-test hook: runs the device wire round trip (f32 -> binary16 -> f32)
+// on n host values; used by the GPU tests to pin the device codec.
+int32_t sfg_selftest_wire_roundtrip(const float* in, float* out, int32_t n, uint64_t* clamped) {
+    SFG_GUARD({
+        float* d = nullptr;
+        unsigned long long* c = nullptr;
+        SFG_CUDA(cudaMalloc(&d, sizeof(float) * (n > 0 ? n : 1)));
+        SFG_CUDA(cudaMalloc(&c, sizeof(unsigned long long)));
+        SFG_CUDA(cudaMemset(c, 0, sizeof(unsigned long long)));
+        SFG_CUDA(cudaMemcpy(d, in, sizeof(float) * n, cudaMemcpyHostToDevice));
+        launch_wire_roundtrip(d, 0, n, c, 0);
+        SFG_CUDA(cudaGetLastError());
+        SFG_CUDA(cudaMemcpy(out, d, sizeof(float) * n, cudaMemcpyDeviceToHost));
+        unsigned long long hc = 0;
+        SFG_CUDA(cudaMemcpy(&hc, c, sizeof(hc), cudaMemcpyDeviceToHost));
+        if (clamped) *clamped = hc;
+        cudaFree(d);
+        cudaFree(c);
+    })
+}
+
 uint16_t sfg_f32_to_f16(float v, uint64_t* clamped) { return wire::f32_to_f16_bits(v, clamped); }
 float sfg_f16_to_f32(uint16_t b) { return wire::f16_bits_to_f32(b); }
 

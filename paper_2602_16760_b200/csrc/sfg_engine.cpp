@@ -114,6 +114,9 @@ void Workspace::release() {
     *this = Workspace{};
 }
 
+// cudaMemset runs on the legacy stream, which is NOT ordered with the
+// engine's non-blocking streams: every zero-fill here is followed by a
+// device sync before the buffer is handed to stream work (growth is rare).
 static void grow(void** p, size_t bytes) {
     if (*p) cudaFree(*p);
     *p = nullptr;
@@ -123,6 +126,11 @@ static void grow(void** p, size_t bytes) {
 
 void Engine::ensure_ws(Workspace& ws, int rows, int runs, int logit_rows) {
     const ModelCfg& c = cfg_;
+    const bool growing = rows > ws.cap_rows || runs > ws.cap_runs || logit_rows > ws.cap_logit_rows;
+    if (!growing) return;
+    // old buffers may still be read by queued work; new ones are zero-filled
+    // on the legacy stream: fence on both sides.
+    SFG_CUDA(cudaDeviceSynchronize());
     if (rows > ws.cap_rows) {
         const int r = std::max(rows, std::max(16, ws.cap_rows * 2));
         const size_t H = c.hidden_dim, qd = c.q_dim(), F = c.ffn_dim;
@@ -161,6 +169,7 @@ void Engine::ensure_ws(Workspace& ws, int rows, int runs, int logit_rows) {
         grow((void**)&ws.logits, sizeof(float) * r * c.vocab_size);
         ws.cap_logit_rows = r;
     }
+    SFG_CUDA(cudaDeviceSynchronize());
 }
 
 // ── banks ─────────────────────────────────────────────────────────────────
@@ -175,6 +184,7 @@ Bank::Bank(Engine& eng, int lb, int le) : eng_(eng), lb_(lb), le_(le) {
     SFG_CUDA(cudaMemset(k_, 0, n * sizeof(float)));
     SFG_CUDA(cudaMemset(v_, 0, n * sizeof(float)));
     SFG_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    SFG_CUDA(cudaDeviceSynchronize());  // legacy-stream memsets vs non-blocking streams
 }
 
 Bank::~Bank() {
