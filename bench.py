@@ -1,0 +1,399 @@
+#!/usr/bin/env python3
+"""bench.py — lookahead step latency & tok/s at the Mistral-7B shape (BASELINE.json).
+
+Workload (N=1, configs[1]): Mistral-7B shape (32 layers, d=4096, 32q/8kv x 128,
+ffn 14336, V=32768, rope 1e6), random-init weights from the reference init
+stream (seed 1234, bf16), 2+2 local split (28 middle layers on the server
+engine), lookahead W=5 N=3 G=5 with the n-gram pool seeded with G junk
+continuations for every token, so every step runs the worst-case B=16 rows
+(SURVEY §8(d) "forced-B=16").  One step = one iteration of
+decode_lookahead_with_pool: embed -> 2 local layers -> wire (f16) -> 28
+middle layers -> wire -> 2 local layers -> final norm + LM head -> argmax ->
+verify / branch selection.  Client and server share the GPU (the paper's
+cloud + local roles, SimChannel at 0 ms RTT unless --rtt-ms).
+
+value : tok/s from device time (CUDA events on the step's stream) with the
+        client device-linked to the server (rows never leave HBM).
+e2e   : the same step through the frame-level C ABI (sfg_server_handle as the
+        FrameHandler): device->host->frame->host->device every step, wall clock.
+
+Multi-GPU (torchrun): one process per GPU, independent sessions (weak
+scaling, no data-path collective); barrier + max-over-ranks timing.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+H_7B = dict(vocab_size=32768, n_layers=32, hidden_dim=4096, n_heads=32, n_kv_heads=8, head_dim=128, ffn_dim=14336,
+            max_seq_len=4096, rope_base=1e6, rms_eps=1e-5, seed=1234)
+SPLIT = 2
+W, NG, G = 5, 3, 5
+PROMPT_LEN = 24
+KCLASS = ["qkv", "attention", "o_proj", "gate_up", "down", "rmsnorm", "lm_head", "other"]
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, dev):
+        self.dev, self.samples, self.proc = dev, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if len(s) >= 7 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 7 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples if len(s) >= 7 for i in range(4) if s[3 + i] == "Active"})
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier_max(ws, local, x: float) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws, local):
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(local)
+
+
+def dist_sum(ws, local, x: float) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ── CPU baseline: the reference's own forward_layers on the host ─────────
+def cpu_sample(threads: int, ctx: int, rows: int = 16):
+    """One 7B-wide middle layer over `rows` rows per host thread (oracle/_ref =
+    the unmodified reference; port fallback), extrapolated to a full step:
+    (28 middle + 4 local) layers + LM head over the rows."""
+    import pyoracle as po
+    cfg = po.ModelCfg(**H_7B)
+    if po.ref_available():
+        lib, kind = po.Ref(), "reference"
+        m = lib.timing_model(cfg, (2, 3), False)
+        t_layer = lib.lib.ref_time_forward(m.h, 2, 3, rows, ctx, threads)
+        return {"kind": kind, "t_layer_s": t_layer, "model": m, "lib": lib}
+    raise RuntimeError("oracle/_ref not built")
+
+
+def cpu_head_time(lib, threads: int) -> float:
+    """finalize() for one row at 7B width (LM head 4096 x 32768)."""
+    import pyoracle as po
+    cfg = po.ModelCfg(**H_7B)
+    mh = lib.timing_model(cfg, (0, 0), True)
+    return lib.lib.ref_time_finalize(mh.h, 1, threads)
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the reference's CPU path on all host threads, each
+    thread one independent session (how the reference scales)."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    s = cpu_sample(threads, PROMPT_LEN, 16)
+    lib, m = s["lib"], s["model"]
+    t_head1 = cpu_head_time(lib, threads)
+    layers = H_7B["n_layers"]
+    steps = []
+    rows = 4  # rows are independent in forward_layers: 4-row sample x4 = the B=16 step
+    for i in range(args.warmup + args.steps):
+        t_layer = lib.lib.ref_time_forward(m.h, 2, 3, rows, PROMPT_LEN, threads) * (16 / rows)
+        t_step = t_layer * layers + t_head1 * 16
+        if i >= args.warmup:
+            steps.append(t_step)
+    mean = sum(steps) / len(steps)
+    tok_s = threads * 1.0 / mean
+    sample = (f"per step: one 7B-wide middle layer x {rows} rows on each of {threads} host threads "
+              f"(forward_layers, oracle/_ref), scaled to 16 rows and x{layers} layers + LM head x16 rows; "
+              f"1 committed token per step (forced-B16 junk-candidate workload)")
+    line = {"metric": "lookahead step latency (ms) & tok/s at Mistral-7B shape vs HBM roofline",
+            "value": tok_s, "unit": "tok/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": mean * 1000.0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": config_dict(args, ws),
+            "cpu_baseline": {"value": tok_s, "unit": "tok/s", "cores": threads, "kind": s["kind"], "sample": sample},
+            "e2e": {"value": tok_s, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, ws):
+    return {"workload": "mistral7b-shape lookahead step, 2+2 local split (28 middle layers), W=5 N=3 G=5, "
+                        "forced B=16 (seeded n-gram pool)",
+            "model_shape": "mistral-7b (32L d4096 32q/8kv x128 ffn14336 V32768)", "rows_per_step": 16,
+            "prompt_len": PROMPT_LEN, "rtt_ms": args.rtt_ms, "math": args.math, "wire": "f16",
+            "sessions_per_gpu": 1, "parallelism": f"replicas x{ws} (independent sessions)",
+            "l2": "inputs larger than L2 (12.2 GB of middle-layer weights streamed per step)"}
+
+
+def seed_pool(sfg, pool, vocab, g, rng):
+    # G junk continuations for every key -> every lookup returns G candidates
+    import numpy as np
+    conts = rng.integers(0, vocab, size=(vocab, g, NG - 1)).astype(np.int32)
+    L = sfg.lib()
+    prev = np.zeros(3, dtype=np.int32)
+    cur = np.zeros(3, dtype=np.int32)
+    pp = prev.ctypes.data_as(C.POINTER(C.c_int32))
+    cp = cur.ctypes.data_as(C.POINTER(C.c_int32))
+    for key in range(vocab):
+        prev[0] = key
+        for j in range(g):
+            cur[1:] = conts[key, j]
+            L.sfg_pool_update(pool.h, pp, cp, 3)
+
+
+def run_ours(args, ws, rank, local):
+    import numpy as np
+
+    import paper_2602_16760_b200 as sfg
+    from paper_2602_16760_b200 import _lib
+
+    L = _lib.lib()
+    math = sfg.FAST if args.math == "fast" else sfg.EXACT
+    cfg = sfg.ModelConfig(**H_7B)
+    t0 = time.time()
+    eng = sfg.Engine(cfg, math=math, device=local)
+    t_init = time.time() - t0
+    nl = cfg.n_layers
+    srv = sfg.ServerEngine(eng, sfg.ServerConfig(SPLIT, nl - SPLIT, max_sessions=64))
+    rng = np.random.default_rng(101 + rank)
+    prompt = rng.integers(0, cfg.vocab_size, PROMPT_LEN).tolist()
+    la = _lib.DecodeConfig(2, W, NG, G, 1 << 20)
+    pool = sfg.NGramPool(NG, 1 << 20)
+    seed_pool(_lib, pool, cfg.vocab_size, G, np.random.default_rng(7))
+    total_steps = args.warmup + args.steps
+
+    def make_decoder(client):
+        d = C.c_void_p()
+        p = np.asarray(prompt, dtype=np.int32)
+        _lib.check(L.sfg_decoder_create(client.h, C.byref(la), pool.h, p.ctypes.data_as(C.POINTER(C.c_int32)),
+                                        len(p), 8 * total_steps + 64, C.byref(d)))
+        return d
+
+    committed = np.zeros(W + 2, dtype=np.int32)
+    cp = committed.ctypes.data_as(C.POINTER(C.c_int32))
+
+    def step(d):
+        n, b = C.c_int32(), C.c_int32()
+        _lib.check(L.sfg_decoder_step(d, cp, C.byref(n), C.byref(b)))
+        return n.value, b.value
+
+    # ── value: device-linked, device time ────────────────────────────────
+    client = sfg.SplitClient(eng, sfg.SplitConfig(SPLIT, SPLIT, sfg.F16, args.rtt_ms / 2), srv,
+                             session_id=f"bench-{rank}")
+    dec = make_decoder(client)
+    for _ in range(args.warmup):
+        step(dec)
+    prof = _lib.StepProfile()
+    dev_ms, srv_ms, toks, launches, batches = [], [], 0, [], []
+    L.sfg_profiler_reset()
+    L.sfg_profiler_enable(1)
+    barrier(ws, local)
+    with Clocks(local) as clk:
+        tw = time.perf_counter()
+        for _ in range(args.steps):
+            n, b = step(dec)
+            L.sfg_client_last_profile(client.h, C.byref(prof))
+            dev_ms.append(prof.step_ms)
+            srv_ms.append(prof.server_ms)
+            launches.append(prof.launches)
+            batches.append(b)
+            toks += n
+        wall = time.perf_counter() - tw
+    L.sfg_profiler_enable(0)
+    barrier(ws, local)
+    dev_total = sum(dev_ms) / 1000.0
+    dev_total_max = barrier_max(ws, local, dev_total)
+    toks_all = dist_sum(ws, local, float(toks))
+    stats = {}
+    for ci, name in enumerate(KCLASS):
+        cnt, ms, by, fl = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+        L.sfg_profiler_stats(ci, C.byref(cnt), C.byref(ms), C.byref(by), C.byref(fl))
+        stats[name] = (cnt.value, ms.value, by.value, fl.value)
+    L.sfg_decoder_destroy(dec)
+
+    # ── e2e: frame-level C ABI, host buffers, wall clock ─────────────────
+    fclient = sfg.SplitClient(eng, sfg.SplitConfig(SPLIT, SPLIT, sfg.F16, args.rtt_ms / 2), srv,
+                              session_id=f"bench-frames-{rank}", frames=True)
+    fdec = make_decoder(fclient)
+    for _ in range(args.warmup):
+        step(fdec)
+    barrier(ws, local)
+    te = time.perf_counter()
+    etoks, ebatch = 0, []
+    for _ in range(args.steps):
+        n, b = step(fdec)
+        etoks += n
+        ebatch.append(b)
+    e_wall = time.perf_counter() - te
+    e_wall_max = barrier_max(ws, local, e_wall)
+    etoks_all = dist_sum(ws, local, float(etoks))
+    L.sfg_decoder_destroy(fdec)
+
+    # ── RTT sweep on the device-linked path (SimChannel semantics) ───────
+    sweep = {}
+    if not args.no_sweep:
+        for rtt in (0.0, 20.0, 80.0):
+            cl = sfg.SplitClient(eng, sfg.SplitConfig(SPLIT, SPLIT, sfg.F16, rtt / 2), srv,
+                                 session_id=f"bench-rtt{int(rtt)}-{rank}")
+            d = make_decoder(cl)
+            step(d)
+            k = max(3, min(args.steps, 8))
+            tr = time.perf_counter()
+            nt = sum(step(d)[0] for _ in range(k))
+            dt = time.perf_counter() - tr
+            sweep[f"{int(rtt)}ms"] = {"tok_s": nt / dt, "ms_per_step": dt / k * 1000.0}
+            L.sfg_decoder_destroy(d)
+
+    if rank != 0:
+        return
+    hbm, tflops, peak_kind = peaks()
+    # dominant kernel by device time
+    dom = max((n for n in KCLASS if n != "other"), key=lambda n: stats[n][1])
+    cnt, ms, by, fl = stats[dom]
+    avg_ms = ms / max(cnt, 1)
+    achieved = (by / max(cnt, 1)) / (avg_ms / 1000.0) / 1e9 if cnt else 0.0
+    B = batches[-1]
+    H = cfg.hidden_dim
+    mask_kv = PROMPT_LEN + 16 * 8  # order of magnitude; mask is host-side only
+    h2d = 2 * B * H * 2 + 4 * B * 2 + 4700 + 16 * B
+    d2h = 2 * B * H * 2 + 4700
+    step_ms = dev_total_max / args.steps * 1000.0
+    # whole-step algorithmic bytes (all kernel classes) -> step-level fraction
+    step_bytes = sum(v[2] for v in stats.values()) / args.steps
+    line = {
+        "metric": "lookahead step latency (ms) & tok/s at Mistral-7B shape vs HBM roofline",
+        "value": toks_all / dev_total_max, "unit": "tok/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16" if args.math == "fast" else "f32", "data": "synthetic",
+        "config": config_dict(args, ws),
+        "e2e": {"value": etoks_all / e_wall_max, "unit": "tok/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e_wall_max / args.steps * 1000.0,
+                "path": "frames through sfg_server_handle (C ABI), host buffers"},
+        "gpu_launches": int(sum(launches)),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": None,
+                     "launches": cnt, "avg_launch_us": avg_ms * 1000.0,
+                     "algorithmic_bytes_per_launch": by / max(cnt, 1)},
+        "step_roofline": {"algorithmic_bytes_per_step": step_bytes,
+                          "roofline_ms": step_bytes / (hbm * 1e9) * 1000.0,
+                          "frac": (step_bytes / (hbm * 1e9)) / (step_ms / 1000.0)},
+        "kernel_classes": {n: {"launches": v[0], "ms": v[1], "share": v[1] / max(1e-9, sum(x[1] for x in stats.values()))}
+                           for n, v in stats.items() if v[0]},
+        "server_ms_per_step": sum(srv_ms) / len(srv_ms), "wall_ms_per_step": wall / args.steps * 1000.0,
+        "batch_rows": sorted(set(batches)), "acceptance": toks / args.steps, "weights_init_s": t_init,
+        "rtt_sweep": sweep,
+        "clocks": clk.summary(),
+    }
+    if ws == 1 and not args.no_cpu:
+        try:
+            s = cpu_sample(1, PROMPT_LEN, 16)
+            th = cpu_head_time(s["lib"], 1)
+            t_step = s["t_layer_s"] * cfg.n_layers + th * 16
+            line["cpu_baseline"] = {
+                "value": (toks / args.steps) / t_step, "unit": "tok/s", "cores": 1, "kind": s["kind"],
+                "sample": "one 7B-wide middle layer x 16 rows (forward_layers, oracle/_ref, 1 thread) + "
+                          "one LM-head row, extrapolated x32 layers and x16 head rows",
+                "ms_per_step": t_step * 1000.0}
+        except Exception as e:  # the checker must not take the GPU line down
+            line["cpu_baseline"] = {"value": None, "unit": "tok/s", "cores": 1, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--math", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--rtt-ms", type=float, default=0.0)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -211,6 +211,17 @@ int32_t sfg_decode(sfg_client* c, const sfg_decode_config* cfg, sfg_pool* pool_o
                    int32_t* step_batch /* nullable [max_new] */,
                    int32_t* step_accepted /* nullable [max_new] */, sfg_decode_stats* stats);
 
+/* The same loop, resumable one step at a time (bench.py's unit of work):
+ * create runs prefill; each step is one lookahead iteration and returns the
+ * tokens it committed (<= window_w + 1) and its batch size.               */
+typedef struct sfg_decoder sfg_decoder;
+int32_t sfg_decoder_create(sfg_client* c, const sfg_decode_config* cfg, sfg_pool* pool_or_null,
+                           const int32_t* prompt, int32_t n, int32_t max_new, sfg_decoder** out);
+int32_t sfg_decoder_step(sfg_decoder* d, int32_t* committed /* nullable */, int32_t* n_committed,
+                         int32_t* batch);
+int32_t sfg_decoder_done(const sfg_decoder* d);
+void sfg_decoder_destroy(sfg_decoder* d);
+
 /* NGramPool (decoding.hpp:35-60) */
 int32_t sfg_pool_create(int32_t ngram_n, size_t capacity, sfg_pool** out);
 void sfg_pool_destroy(sfg_pool* p);
@@ -235,6 +246,13 @@ typedef struct {
 int32_t sfg_client_last_profile(sfg_client* c, sfg_step_profile* out);
 /* Capture / replay the device part of steps as CUDA graphs (default on). */
 void sfg_set_graphs(int32_t enabled);
+/* Per-kernel-class CUDA-event timing on the launching stream (bench.py's
+ * roofline).  Classes: 0 QKV, 1 attention, 2 O-proj, 3 gate|up, 4 down,
+ * 5 RMSNorm, 6 LM head, 7 other.  bytes/flops are ALGORITHMIC per launch,
+ * summed.                                                                 */
+void sfg_profiler_enable(int32_t on);
+void sfg_profiler_reset(void);
+int32_t sfg_profiler_stats(int32_t cls, int64_t* count, double* ms, double* bytes, double* flops);
 
 #ifdef __cplusplus
 }

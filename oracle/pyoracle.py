@@ -258,6 +258,14 @@ class Ref(_Base):
                                            C.byref(h)))
         return _Model(self, h, cfg, "ref")
 
+    def timing_model(self, cfg: ModelCfg, layers: tuple, with_head: bool):
+        """Tensors of `layers` (+ head) filled with U[-a,a] values without
+        walking the reference stream: for CPU-baseline timing only."""
+        h = C.c_void_p()
+        self._check(self.lib.ref_model_new_timing(C.byref(_ccfg(cfg)), layers[0], layers[1], int(with_head),
+                                                  C.byref(h)))
+        return _Model(self, h, cfg, "ref")
+
     def f32_to_f16(self, v: float, counter=None) -> int:
         c = C.c_uint64(0)
         b = self.lib.ref_f32_to_f16(C.c_float(v), C.byref(c))

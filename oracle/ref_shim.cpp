@@ -84,9 +84,11 @@ void round_all(Weights& w) {
 // single mt19937_64 stream in declaration order, but only the tensors of the
 // requested layers are filled; the rest of the stream is discarded.  Used to
 // time one 7B-wide layer without allocating 29 GB.
+bool g_timing_only = false;  // skipped tensors do not advance the stream
+
 void fill_or_skip(std::vector<float>& dst, size_t n, float a, std::mt19937_64& rng, bool keep) {
     if (!keep) {
-        rng.discard(n);
+        if (!g_timing_only) rng.discard(n);
         return;
     }
     dst.resize(n);
@@ -185,6 +187,22 @@ int ref_model_new(const ref_model_cfg* c, int bf16, int layer_lo, int layer_hi, 
                                                              with_head != 0));
         if (bf16) round_all(*w);
         *out = w;
+    })
+}
+
+// Timing-only model for the CPU baseline: the requested tensors get
+// U[-a, a] values (same distribution, NOT the reference stream positions)
+// without walking the 7.25 G-draw stream; arithmetic cost is identical.
+int ref_model_new_timing(const ref_model_cfg* c, int layer_lo, int layer_hi, int with_head, void** out) {
+    GUARD({
+        g_timing_only = true;
+        try {
+            *out = new Weights(partial_weights(to_cfg(c), layer_lo, layer_hi, with_head != 0));
+        } catch (...) {
+            g_timing_only = false;
+            throw;
+        }
+        g_timing_only = false;
     })
 }
 

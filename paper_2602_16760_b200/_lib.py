@@ -128,6 +128,10 @@ def lib() -> C.CDLL:
         "sfg_client_decode_step": (i32, [vp, i32, i32p, i32p, f32p, i32p, i32, i32, f32p, i32p]),
         "sfg_decode": (i32, [vp, C.POINTER(DecodeConfig), vp, i32p, i32, i32, i32p, f32p, i32p, i32p,
                              C.POINTER(DecodeStats)]),
+        "sfg_decoder_create": (i32, [vp, C.POINTER(DecodeConfig), vp, i32p, i32, i32, C.POINTER(vp)]),
+        "sfg_decoder_step": (i32, [vp, i32p, i32p, i32p]),
+        "sfg_decoder_done": (i32, [vp]),
+        "sfg_decoder_destroy": (None, [vp]),
         "sfg_pool_create": (i32, [i32, C.c_size_t, C.POINTER(vp)]),
         "sfg_pool_destroy": (None, [vp]),
         "sfg_pool_update": (i32, [vp, i32p, i32p, i32]),
@@ -138,6 +142,10 @@ def lib() -> C.CDLL:
         "sfg_selftest_wire_roundtrip": (i32, [f32p, f32p, i32, C.POINTER(C.c_uint64)]),
         "sfg_client_last_profile": (i32, [vp, C.POINTER(StepProfile)]),
         "sfg_set_graphs": (None, [i32]),
+        "sfg_profiler_enable": (None, [i32]),
+        "sfg_profiler_reset": (None, []),
+        "sfg_profiler_stats": (i32, [i32, C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -7,6 +7,7 @@
 #include "../../include/sfg.h"
 #include "sfg_client.h"
 #include "sfg_engine.h"
+#include "sfg_prof.h"
 #include "sfg_server.h"
 #include "sfg_wire.h"
 
@@ -221,37 +222,71 @@ int32_t sfg_client_decode_step(sfg_client* c, int32_t seq, const int32_t* tokens
             mr = runs_from_dense(mask, seq, len + seq);
             mp = &mr;
         }
-        c->c->decode_step(seq, tokens, positions, mp, keep, n_keep, cr, logits != nullptr);
-        if (logits) c->c->fetch_logits(seq, logits);
-        if (argmax) c->c->fetch_argmax(seq, argmax);
+        c->c->decode_step(seq, tokens, positions, mp, keep, n_keep, cr, logits, argmax, nullptr, nullptr);
     })
+}
+
+static Decoder::Cfg to_decoder_cfg(const sfg_decode_config* cfg) {
+    Decoder::Cfg dc;
+    dc.mode = cfg->mode;
+    dc.window_w = cfg->window_w;
+    dc.ngram_n = cfg->ngram_n;
+    dc.max_candidates_g = cfg->max_candidates_g;
+    dc.pool_capacity = static_cast<size_t>(cfg->pool_capacity);
+    return dc;
 }
 
 int32_t sfg_decode(sfg_client* c, const sfg_decode_config* cfg, sfg_pool* pool, const int32_t* prompt, int32_t n,
                    int32_t max_new, int32_t* out_tokens, float* committed_logits, int32_t* step_batch,
                    int32_t* step_accepted, sfg_decode_stats* stats) {
     SFG_GUARD({
-        Client::DecodeCfg dc;
-        dc.mode = cfg->mode;
-        dc.window_w = cfg->window_w;
-        dc.ngram_n = cfg->ngram_n;
-        dc.max_candidates_g = cfg->max_candidates_g;
-        dc.pool_capacity = static_cast<size_t>(cfg->pool_capacity);
-        Client::DecodeOut o;
-        c->c->decode(dc, pool ? pool->p.get() : nullptr, prompt, n, max_new, committed_logits != nullptr, o);
-        std::memcpy(out_tokens, o.tokens.data(), sizeof(int32_t) * o.tokens.size());
-        if (committed_logits) std::memcpy(committed_logits, o.logits.data(), sizeof(float) * o.logits.size());
-        if (step_batch) std::memcpy(step_batch, o.step_batch.data(), sizeof(int32_t) * o.step_batch.size());
-        if (step_accepted) std::memcpy(step_accepted, o.step_accepted.data(), sizeof(int32_t) * o.step_accepted.size());
+        Decoder d(*c->c, to_decoder_cfg(cfg), pool ? pool->p.get() : nullptr, prompt, n, max_new,
+                  committed_logits != nullptr);
+        while (!d.done()) d.step();
+        std::memcpy(out_tokens, d.tokens.data(), sizeof(int32_t) * d.tokens.size());
+        if (committed_logits) std::memcpy(committed_logits, d.logits.data(), sizeof(float) * d.logits.size());
+        if (step_batch) std::memcpy(step_batch, d.step_batch.data(), sizeof(int32_t) * d.step_batch.size());
+        if (step_accepted) std::memcpy(step_accepted, d.step_accepted.data(), sizeof(int32_t) * d.step_accepted.size());
         if (stats) {
-            stats->steps = o.steps;
-            stats->tokens_committed = o.committed;
-            stats->wall_seconds = o.wall_s;
-            stats->match_rate = o.match_rate;
+            stats->steps = d.steps;
+            stats->tokens_committed = d.committed;
+            stats->wall_seconds = d.wall_s;
+            stats->match_rate = d.steps > 0 ? static_cast<double>(d.hits) / d.steps : 0.0;
             stats->clamped = c->c->clamped();
         }
     })
 }
+
+struct sfg_decoder { std::unique_ptr<Decoder> d; };
+
+int32_t sfg_decoder_create(sfg_client* c, const sfg_decode_config* cfg, sfg_pool* pool, const int32_t* prompt,
+                           int32_t n, int32_t max_new, sfg_decoder** out) {
+    SFG_GUARD({
+        auto* h = new sfg_decoder;
+        try {
+            h->d = std::make_unique<Decoder>(*c->c, to_decoder_cfg(cfg), pool ? pool->p.get() : nullptr, prompt, n,
+                                             max_new, false);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    })
+}
+
+int32_t sfg_decoder_step(sfg_decoder* d, int32_t* committed, int32_t* n_committed, int32_t* batch) {
+    SFG_GUARD({
+        if (d->d->done()) throw Error(Kind::input, "decoder finished");
+        const size_t before = d->d->tokens.size();
+        const int k = d->d->step();
+        if (committed) std::memcpy(committed, d->d->tokens.data() + before, sizeof(int32_t) * k);
+        if (n_committed) *n_committed = k;
+        if (batch) *batch = d->d->step_batch.back();
+    })
+}
+
+int32_t sfg_decoder_done(const sfg_decoder* d) { return d->d->done() ? 1 : 0; }
+void sfg_decoder_destroy(sfg_decoder* d) { delete d; }
 
 int32_t sfg_client_last_profile(sfg_client* c, sfg_step_profile* out) {
     const StepProfile& p = c->c->last_profile();
@@ -265,6 +300,15 @@ int32_t sfg_client_last_profile(sfg_client* c, sfg_step_profile* out) {
 
 static int g_graphs = 1;
 void sfg_set_graphs(int32_t enabled) { g_graphs = enabled; }
+
+void sfg_profiler_enable(int32_t on) { KernelProfiler::get().enable(on != 0); }
+void sfg_profiler_reset(void) { KernelProfiler::get().reset(); }
+int32_t sfg_profiler_stats(int32_t cls, int64_t* count, double* ms, double* bytes, double* flops) {
+    SFG_GUARD({
+        cudaDeviceSynchronize();
+        KernelProfiler::get().stats(cls, count, ms, bytes, flops);
+    })
+}
 
 int32_t sfg_pool_create(int32_t n, size_t cap, sfg_pool** out) {
     SFG_GUARD({

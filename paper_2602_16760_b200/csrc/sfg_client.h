@@ -5,9 +5,9 @@
 // device (no host copies; wire quantisation applied on device).
 #pragma once
 #include <chrono>
-#include <list>
 #include <optional>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "sfg_engine.h"
@@ -15,25 +15,40 @@
 
 namespace sfg {
 
-// NGramPool (decoding.hpp:35-60, decoding.cpp:61-97): recency-ordered list,
-// dedup on (key, continuation), capacity eviction from the back.
+// NGramPool (decoding.hpp:35-60, decoding.cpp:61-97): one recency list,
+// dedup on (key, continuation), eviction from the back, lookup returns a
+// key's entries most-recent-first.  Same observable behaviour as the
+// reference's std::list scan, but entries are also threaded on a per-key
+// list so insert/lookup cost O(entries of that key) instead of O(pool):
+// the forced-B=16 benchmark pool holds G continuations for every token.
 class Pool {
 public:
     Pool(int ngram_n, size_t capacity);
+    ~Pool();
+    Pool(const Pool&) = delete;
+    Pool& operator=(const Pool&) = delete;
     void update(const int32_t* prev, const int32_t* cur, int w);
     int lookup(int key, int max_c, std::vector<std::vector<int32_t>>& out) const;
-    size_t size() const { return entries_.size(); }
+    size_t size() const { return size_; }
     int ngram_n() const { return n_; }
 
 private:
-    struct Entry {
+    struct Node {
         int32_t key;
         std::vector<int32_t> cont;
+        Node *gprev = nullptr, *gnext = nullptr;  // global recency list
+        Node *kprev = nullptr, *knext = nullptr;  // per-key recency list
     };
-    void insert(int32_t key, std::vector<int32_t> cont);
+    struct KeyList {
+        Node *head = nullptr, *tail = nullptr;
+    };
+    void insert(int32_t key, const int32_t* cont);
+    void link_front(Node* n);
+    void unlink(Node* n);
     int n_;
-    size_t cap_;
-    std::list<Entry> entries_;
+    size_t cap_, size_ = 0;
+    Node *head_ = nullptr, *tail_ = nullptr;
+    std::unordered_map<int32_t, KeyList> keys_;
 };
 
 struct ClientCfg {
@@ -55,37 +70,22 @@ public:
     ~Client();
 
     int prefill(const int32_t* prompt, int n, float* logits_row);
-    // One exchange; results stay on device (ws.logits if want_logits, ws.argmax).
+    // One exchange (client.cpp:169-228).  Results stay on device unless
+    // requested: logits rows -> logits_out (host), verify tail -> vout.
     void decode_step(int seq, const int32_t* tokens, const int32_t* positions, const MaskRuns* runs,
-                     const int32_t* keep, int n_keep, std::optional<int> crop, bool want_logits);
-    // Host copies of the last step's outputs.
-    void fetch_logits(int rows, float* out);
-    void fetch_argmax(int rows, int32_t* out);
-
-    struct DecodeCfg {
-        int mode = 2, window_w = 8, ngram_n = 3, max_candidates_g = 2;
-        size_t pool_capacity = 4096;
-    };
-    struct DecodeOut {
-        std::vector<int32_t> tokens, step_batch, step_accepted;
-        std::vector<float> logits;  // committed rows (optional)
-        int steps = 0, committed = 0;
-        double wall_s = 0, match_rate = 0;
-    };
-    void decode(const DecodeCfg& cfg, Pool* pool, const int32_t* prompt, int n, int max_new,
-                bool want_logits, DecodeOut& out);
+                     const int32_t* keep, int n_keep, std::optional<int> crop, float* logits_out,
+                     int32_t* argmax_out, const VerifyIn* vin, VerifyOut* vout);
 
     const StepProfile& last_profile() const { return prof_; }
     uint64_t clamped();
     Bank& prefix() { return *prefix_; }
     Bank& suffix() { return *suffix_; }
-    int committed_len() const { return prefix_->committed_len(); }
+    Engine& engine() { return eng_; }
 
 private:
     void exchange(bool prompt, int seq, const int32_t* pos, const MaskRuns* runs, int mask_kv,
                   const int32_t* keep, int n_keep, bool send_keep, std::optional<int> crop);
     void sleep_one_way() const;
-    void run_head(int rows, bool want_logits, VerifyIn* vin);
 
     Engine& eng_;
     ClientCfg cfg_;
@@ -97,12 +97,43 @@ private:
     bool prefilled_ = false, dead_ = false, first_step_done_ = false;
     int prompt_len_ = 0;
     StepProfile prof_;
-    cudaEvent_t ev_[6] = {};
+    cudaEvent_t ev_[4] = {};
     VerifyIn* d_vin_ = nullptr;
     VerifyOut* d_vout_ = nullptr;
     VerifyIn* h_vin_ = nullptr;
     VerifyOut* h_vout_ = nullptr;
-    std::vector<uint8_t> req_, maskbuf_;
+    std::vector<uint8_t> req_, payload_;
+};
+
+// decode_sequential / decode_lookahead_with_pool (decoding.cpp:111-355) as a
+// resumable loop: the constructor runs prefill, step() runs one iteration.
+class Decoder {
+public:
+    struct Cfg {
+        int mode = 2, window_w = 8, ngram_n = 3, max_candidates_g = 2;
+        size_t pool_capacity = 4096;
+    };
+    Decoder(Client& c, const Cfg& cfg, Pool* pool, const int32_t* prompt, int n, int max_new, bool want_logits);
+    bool done() const { return static_cast<int>(tokens.size()) >= max_new_; }
+    int step();  // committed tokens this step
+
+    std::vector<int32_t> tokens, step_batch, step_accepted;
+    std::vector<float> logits;  // committed rows (want_logits)
+    int steps = 0, committed = 0, hits = 0;
+    double wall_s = 0;
+
+private:
+    Client& c_;
+    Cfg cfg_;
+    Pool* pool_;
+    std::unique_ptr<Pool> own_;
+    int max_new_, total_;
+    bool want_logits_;
+    std::vector<int32_t> window_, keep_, batch_, pos_;
+    std::vector<std::vector<int32_t>> cands_;
+    std::vector<float> lbuf_;
+    VerifyIn vin_{};
+    VerifyOut vout_{};
 };
 
 }  // namespace sfg

@@ -2,6 +2,8 @@
 // B200 counterpart of tinyformer.cpp (reference file:line cited per symbol).
 #include "sfg_engine.h"
 
+#include "sfg_prof.h"
+
 #include <cmath>
 #include <cstring>
 #include <random>
@@ -191,6 +193,7 @@ Bank::~Bank() {
     DeviceGuard g(eng_.device());
     if (stream_) cudaStreamSynchronize(stream_);
     ws_.release();
+    if (keep_pin_) cudaFreeHost(keep_pin_);
     cudaFree(k_);
     cudaFree(v_);
     if (stream_) cudaStreamDestroy(stream_);
@@ -199,8 +202,11 @@ Bank::~Bank() {
 float* Bank::kslab(int layer) const { return k_ + slab_elems_ * (layer - lb_); }
 float* Bank::vslab(int layer) const { return v_ + slab_elems_ * (layer - lb_); }
 
-// CacheBank::resolve (tinyformer.cpp:282-308): validate, compact on device.
-void Bank::resolve(const int32_t* keep, int n) {
+// CacheBank::resolve (tinyformer.cpp:282-308): validate on the host, then
+// enqueue the in-place compaction on `s` (the stream that runs the next
+// forward, so no host sync is needed).  s == nullptr: the bank's own stream,
+// synchronised (seam-2 callers).
+void Bank::resolve(const int32_t* keep, int n, cudaStream_t s) {
     const int tail = provisional();
     int prev = -1;
     for (int i = 0; i < n; ++i) {
@@ -213,15 +219,19 @@ void Bank::resolve(const int32_t* keep, int n) {
     for (int i = 0; i < n; ++i) identity = identity && keep[i] == i;
     if (!identity && le_ > lb_) {
         DeviceGuard g(eng_.device());
+        const bool own = s == nullptr;
+        cudaStream_t st = own ? stream_ : s;
         eng_.ensure_ws(ws_, std::max(n, 1), 1, 0);
-        int32_t* hk = static_cast<int32_t*>(ws_.pinned);
-        std::memcpy(hk, keep, sizeof(int32_t) * n);
-        SFG_CUDA(cudaMemcpyAsync(ws_.keep, hk, sizeof(int32_t) * n, cudaMemcpyHostToDevice, stream_));
+        if (!keep_pin_) SFG_CUDA(cudaMallocHost(&keep_pin_, sizeof(int32_t) * 1024));
+        if (n > 1024) throw Error(Kind::protocol, "keep list too long");
+        // the previous resolve's copy has completed: every step ends in a sync
+        std::memcpy(keep_pin_, keep, sizeof(int32_t) * n);
+        SFG_CUDA(cudaMemcpyAsync(ws_.keep, keep_pin_, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
         const ModelCfg& c = eng_.cfg();
         launch_kv_compact(k_, v_, le_ - lb_, c.n_kv_heads, c.max_seq_len, c.head_dim, committed_, ws_.keep,
-                          n, stream_);
+                          n, st);
         SFG_CUDA(cudaGetLastError());
-        SFG_CUDA(cudaStreamSynchronize(stream_));
+        if (own) SFG_CUDA(cudaStreamSynchronize(st));
     }
     committed_ += n;
     len_ = committed_;
@@ -458,15 +468,39 @@ int Engine::forward_device(Bank& b, int lb, int le, int rows, Workspace& ws, cud
         }
         float* kc = b.kslab(layer);
         float* vc = b.vslab(layer);
-        n += launch_rmsnorm_exact(ws.h, L.attn_norm, ws.xn, rows, d.H, d.eps, s);
-        n += launch_qkv_exact(ws.xn, rows, d, wt(), L.wq, L.wk, L.wv, ws.pos, rope_cos_, rope_sin_, ws.q, kc,
-                              vc, prior, s);
-        n += launch_attention_exact(ws.q, kc, vc, ws.row_off, ws.runs, rows, prior + rows, d, ws.att,
-                                    ws.status, s);
-        n += launch_matvec_residual_exact(ws.att, rows, d.qd, wt(), L.wo, d.H, ws.h, s);
-        n += launch_rmsnorm_exact(ws.h, L.ffn_norm, ws.xn, rows, d.H, d.eps, s);
-        n += launch_gateup_exact(ws.xn, rows, d.H, d.F, wt(), L.w_gate, L.w_up, ws.act, s);
-        n += launch_matvec_residual_exact(ws.act, rows, d.F, wt(), L.w_down, d.H, ws.h, s);
+        const double wb = wt() == W_BF16 ? 2.0 : 4.0, R = rows;
+        const int qkv = d.qd + 2 * d.kvd;
+        {
+            ProfScope p(K_NORM, s, R * d.H * 8.0 + d.H * 4.0, 0);
+            n += launch_rmsnorm_exact(ws.h, L.attn_norm, ws.xn, rows, d.H, d.eps, s);
+        }
+        {
+            ProfScope p(K_QKV, s, wb * d.H * qkv + 4.0 * R * (d.H + qkv), 2.0 * R * d.H * qkv);
+            n += launch_qkv_exact(ws.xn, rows, d, wt(), L.wq, L.wk, L.wv, ws.pos, rope_cos_, rope_sin_, ws.q, kc,
+                                  vc, prior, s);
+        }
+        {
+            const double kvb = 2.0 * 4.0 * d.kvd * (prior + rows);
+            ProfScope p(K_ATTN, s, kvb + 8.0 * R * d.qd, 4.0 * R * d.qd * (prior + rows));
+            n += launch_attention_exact(ws.q, kc, vc, ws.row_off, ws.runs, rows, prior + rows, d, ws.att,
+                                        ws.status, s);
+        }
+        {
+            ProfScope p(K_OPROJ, s, wb * d.qd * d.H + 4.0 * R * (d.qd + 2.0 * d.H), 2.0 * R * d.qd * d.H);
+            n += launch_matvec_residual_exact(ws.att, rows, d.qd, wt(), L.wo, d.H, ws.h, s);
+        }
+        {
+            ProfScope p(K_NORM, s, R * d.H * 8.0 + d.H * 4.0, 0);
+            n += launch_rmsnorm_exact(ws.h, L.ffn_norm, ws.xn, rows, d.H, d.eps, s);
+        }
+        {
+            ProfScope p(K_GATEUP, s, 2.0 * wb * d.H * d.F + 4.0 * R * (d.H + d.F), 4.0 * R * d.H * d.F);
+            n += launch_gateup_exact(ws.xn, rows, d.H, d.F, wt(), L.w_gate, L.w_up, ws.act, s);
+        }
+        {
+            ProfScope p(K_DOWN, s, wb * d.F * d.H + 4.0 * R * (d.F + 2.0 * d.H), 2.0 * R * d.F * d.H);
+            n += launch_matvec_residual_exact(ws.act, rows, d.F, wt(), L.w_down, d.H, ws.h, s);
+        }
     }
     return n;
 }
@@ -475,8 +509,12 @@ int Engine::head_device(int rows, Workspace& ws, bool want_logits, bool want_arg
     if (!final_norm_ || !lm_head_) throw Error(Kind::internal, "engine does not host the LM head");
     const Dims d = dims();
     int n = 0;
+    const double wb = wt() == W_BF16 ? 2.0 : 4.0, R = rows;
     n += launch_rmsnorm_exact(ws.h, final_norm_, ws.xn, rows, d.H, d.eps, s);
-    n += launch_matvec_store_exact(ws.xn, rows, d.H, wt(), lm_head_, d.V, ws.logits, s);
+    {
+        ProfScope p(K_HEAD, s, wb * d.H * d.V + 4.0 * R * (d.H + d.V), 2.0 * R * d.H * d.V);
+        n += launch_matvec_store_exact(ws.xn, rows, d.H, wt(), lm_head_, d.V, ws.logits, s);
+    }
     if (want_argmax) n += launch_argmax(ws.logits, rows, d.V, ws.argmax, s);
     (void)want_logits;
     return n;

@@ -107,7 +107,7 @@ public:
     void mark_committed(int c) { committed_ = c; }
     void set_len(int l) { len_ = l; }
     void reset() { len_ = 0; committed_ = 0; }
-    void resolve(const int32_t* keep, int n);  // tinyformer.cpp:282-308
+    void resolve(const int32_t* keep, int n, cudaStream_t s = nullptr);  // tinyformer.cpp:282-308
     void crop(int pos);                        // tinyformer.cpp:310-316
     float* kslab(int layer) const;
     float* vslab(int layer) const;
@@ -124,6 +124,7 @@ private:
     float* v_ = nullptr;
     size_t slab_elems_ = 0;
     cudaStream_t stream_ = nullptr;
+    int32_t* keep_pin_ = nullptr;
     Workspace ws_;
 };
 

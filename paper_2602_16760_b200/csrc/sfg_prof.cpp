@@ -1,0 +1,83 @@
+#include "sfg_prof.h"
+
+namespace sfg {
+
+KernelProfiler& KernelProfiler::get() {
+    static KernelProfiler p;
+    return p;
+}
+
+void KernelProfiler::enable(bool v) {
+    std::lock_guard<std::mutex> lk(mu_);
+    on_ = v;
+}
+
+int KernelProfiler::begin(int cls, cudaStream_t s) {
+    if (!on_) return -1;
+    std::lock_guard<std::mutex> lk(mu_);
+    int idx = -1;
+    for (size_t i = 0; i < slots_.size(); ++i)
+        if (!slots_[i].used) {
+            idx = static_cast<int>(i);
+            break;
+        }
+    if (idx < 0) {
+        Slot sl{};
+        cudaEventCreate(&sl.a);
+        cudaEventCreate(&sl.b);
+        slots_.push_back(sl);
+        idx = static_cast<int>(slots_.size()) - 1;
+    }
+    Slot& sl = slots_[idx];
+    sl.used = true;
+    sl.cls = cls;
+    cudaEventRecord(sl.a, s);
+    return idx;
+}
+
+void KernelProfiler::end(int slot, cudaStream_t s, double bytes, double flops) {
+    std::lock_guard<std::mutex> lk(mu_);
+    Slot& sl = slots_[slot];
+    sl.bytes = bytes;
+    sl.flops = flops;
+    cudaEventRecord(sl.b, s);
+    pending_.push_back(slot);
+}
+
+void KernelProfiler::collect() {
+    std::lock_guard<std::mutex> lk(mu_);
+    std::vector<int> keep;
+    for (int i : pending_) {
+        Slot& sl = slots_[i];
+        if (cudaEventQuery(sl.b) != cudaSuccess) {
+            keep.push_back(i);
+            continue;
+        }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, sl.a, sl.b);
+        count_[sl.cls] += 1;
+        ms_[sl.cls] += ms;
+        bytes_[sl.cls] += sl.bytes;
+        flops_[sl.cls] += sl.flops;
+        sl.used = false;
+    }
+    pending_.swap(keep);
+}
+
+void KernelProfiler::reset() {
+    collect();
+    std::lock_guard<std::mutex> lk(mu_);
+    for (int c = 0; c < K_NCLASS; ++c) count_[c] = 0, ms_[c] = bytes_[c] = flops_[c] = 0;
+}
+
+void KernelProfiler::stats(int cls, int64_t* count, double* ms, double* bytes, double* flops) {
+    collect();
+    std::lock_guard<std::mutex> lk(mu_);
+    if (cls < 0 || cls >= K_NCLASS) return;
+    *count = count_[cls];
+    *ms = ms_[cls];
+    *bytes = bytes_[cls];
+    *flops = flops_[cls];
+}
+
+}  // namespace sfg

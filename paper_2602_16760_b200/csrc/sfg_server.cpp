@@ -266,7 +266,8 @@ void Server::handle_frame(const wire::FrameView& f, std::vector<uint8_t>& resp) 
             keep.reserve(f.h.keep->size());
             for (int64_t k : *f.h.keep) keep.push_back(static_cast<int32_t>(k));
         }
-        if (!keep.empty() || bank.provisional() > 0) bank.resolve(keep.data(), static_cast<int>(keep.size()));
+        if (!keep.empty() || bank.provisional() > 0)
+            bank.resolve(keep.data(), static_cast<int>(keep.size()), bank.stream());
         if (f.h.crop) {
             const int64_t p = *f.h.crop;
             if (p < 0 || p > bank.len()) throw Error(Kind::protocol, "crop position exceeds session length");
@@ -338,7 +339,8 @@ int Server::linked_step(const LinkedStep& st) {
         std::vector<int32_t> keep;
         if (st.keep)
             for (int64_t k : *st.keep) keep.push_back(static_cast<int32_t>(k));
-        if (!keep.empty() || bank.provisional() > 0) bank.resolve(keep.data(), static_cast<int>(keep.size()));
+        if (!keep.empty() || bank.provisional() > 0)
+            bank.resolve(keep.data(), static_cast<int>(keep.size()), st.stream);
         if (st.crop) {
             if (*st.crop < 0 || *st.crop > bank.len()) throw Error(Kind::protocol, "crop position exceeds session length");
             bank.crop(static_cast<int>(*st.crop));
