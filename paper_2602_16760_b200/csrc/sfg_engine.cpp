@@ -448,9 +448,40 @@ void Engine::load(const float* params) {
     SFG_CUDA(cudaMemcpy(rope_sin_, sn.data(), sn.size() * sizeof(float), cudaMemcpyHostToDevice));
 }
 
+// FAST math streams weights from a tiled, pre-swizzled W^T image (see
+// sfg_fast.cu); the reference-layout copies are released afterwards.
 void Engine::build_fast_layouts() {
-    for (int l = 0; l < cfg_.n_layers; ++l)
-        if (layers_[l].hosted) fast_build_layer(*this, layers_[l], stream_);
+    auto release = [&](void*& p) {
+        if (!p) return;
+        for (auto it = allocs_.begin(); it != allocs_.end(); ++it)
+            if (*it == p) {
+                allocs_.erase(it);
+                break;
+            }
+        cudaFree(p);
+        p = nullptr;
+    };
+    for (int l = 0; l < cfg_.n_layers; ++l) {
+        LayerWeights& L = layers_[l];
+        if (!L.hosted) continue;
+        fast_build_layer(*this, L, stream_);
+        SFG_CUDA(cudaStreamSynchronize(stream_));
+        const size_t H = cfg_.hidden_dim, qd = cfg_.q_dim(), kvd = cfg_.kv_dim(), F = cfg_.ffn_dim;
+        weight_bytes_ -= static_cast<int64_t>(2 * (H * qd + 2 * H * kvd + qd * H + 3 * H * F));
+        release(L.wq);
+        release(L.wk);
+        release(L.wv);
+        release(L.wo);
+        release(L.w_gate);
+        release(L.w_up);
+        release(L.w_down);
+    }
+    if (lm_head_) {
+        f_lm_head_ = fast_build_head(*this, lm_head_, stream_);
+        SFG_CUDA(cudaStreamSynchronize(stream_));
+        weight_bytes_ -= static_cast<int64_t>(2 * static_cast<size_t>(cfg_.hidden_dim) * cfg_.vocab_size);
+        release(lm_head_);
+    }
     SFG_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -506,7 +537,11 @@ int Engine::forward_device(Bank& b, int lb, int le, int rows, Workspace& ws, cud
 }
 
 int Engine::head_device(int rows, Workspace& ws, bool want_logits, bool want_argmax, cudaStream_t s) {
-    if (!final_norm_ || !lm_head_) throw Error(Kind::internal, "engine does not host the LM head");
+    if (!final_norm_ || (!lm_head_ && !f_lm_head_)) throw Error(Kind::internal, "engine does not host the LM head");
+    if (fast()) {
+        (void)want_argmax;  // the FAST head always produces the argmax
+        return fast_head(*this, f_lm_head_, final_norm_, rows, ws, want_logits, s);
+    }
     const Dims d = dims();
     int n = 0;
     const double wb = wt() == W_BF16 ? 2.0 : 4.0, R = rows;

@@ -176,6 +176,11 @@ public:
     std::mutex& mutex() { return mu_; }
     Workspace& ws() { return ws_; }
     cudaStream_t stream() const { return stream_; }
+    // take ownership of a device allocation holding weights
+    void adopt(void* p, size_t bytes) {
+        allocs_.push_back(p);
+        weight_bytes_ += static_cast<int64_t>(bytes);
+    }
 
 private:
     void load(const float* params);
@@ -210,7 +215,10 @@ struct DeviceGuard {
 // FAST-mode layer executor (sfg_fast.cu).
 int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, int prior,
                        cudaStream_t s);
+int fast_head(Engine& e, const void* f_lm_head, const float* final_norm, int rows, Workspace& ws,
+              bool want_logits, cudaStream_t s);
 size_t fast_workspace_bytes(const ModelCfg& c, int rows);
 void fast_build_layer(Engine& e, LayerWeights& L, cudaStream_t s);
+void* fast_build_head(Engine& e, const void* lm_head, cudaStream_t s);
 
 }  // namespace sfg

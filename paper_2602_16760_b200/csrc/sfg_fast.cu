@@ -1,17 +1,799 @@
-// FAST-mode layer executor (tcgen05 weight-streaming GEMMs) — placeholder
-// until the tcgen05 path lands; engines created with SFG_MATH_FAST fail loudly.
+// FAST-mode layer executor: weight-streaming skinny GEMMs on tcgen05 (sm_100a).
+//
+// Every projection of the lookahead step is Y[B x N] = X[B x K] . W[K x N]
+// with B <= 16 token rows and N, K in the thousands — a dense contraction
+// that is HBM-bound at ~16 flop/byte.  It runs "swap-AB" on the 5th-gen
+// tensor core: D[128 features x 48] (TMEM, fp32) += W^T[128 x K] . Xs^T, where
+// Xs stacks the fp32 activations as three bf16 pieces (hi | mid | lo, 16 rows
+// each) so bf16 x bf16 products reconstruct ~fp32 activations exactly and
+// only the weights are bf16 (their storage precision).
+//
+//   * weights are re-laid out once at load into the exact shared-memory image
+//     of each [128 x 64] K-major SWIZZLE_128B stage (16 KB), so a stage is ONE
+//     contiguous cp.async.bulk (TMA engine, UBLKCP) — no tensor maps;
+//   * 8-stage smem ring, warp-specialised: warp 0 = bulk-copy producer, warp 1
+//     = single-thread tcgen05.mma issuer, warps 2-5 = TMEM epilogue (two TMEM
+//     accumulators so the epilogue of one tile overlaps the next);
+//   * stream-K: the (tile, k-block) space is cut into gridDim.x (= #SMs)
+//     contiguous equal ranges; tiles split between CTAs are finished by the
+//     last arriving CTA, which sums the pieces in fixed k order — results are
+//     deterministic and independent of B (batch invariance);
+//   * epilogues fuse RoPE + KV-cache append (QKV), the residual add (O, down),
+//     SiLU(gate)*up, and logits + per-tile argmax partials (LM head).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <initializer_list>
+
 #include "sfg_engine.h"
+#include "sfg_expf.h"
+#include "sfg_prof.h"
 
 namespace sfg {
+namespace fast {
 
-size_t fast_workspace_bytes(const ModelCfg&, int) { return 16; }
+constexpr int kRows = 16;            // token rows per pass
+constexpr int kN = 3 * kRows;        // MMA N: hi | mid | lo
+constexpr int kM = 128;              // output features per tile (MMA M)
+constexpr int kKB = 64;              // K per stage: one 128-byte swizzle row of bf16
+constexpr int kStages = 8;
+constexpr int kABytes = kM * kKB * 2;  // 16 KB
+constexpr int kBBytes = kN * kKB * 2;  // 6 KB
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kThreads = 192;
+constexpr int kAccCols = 64;           // TMEM columns per accumulator (48 used)
+constexpr int kTmemCols = 128;         // two accumulators
+constexpr int kMaxPieces = 16;
 
-void fast_build_layer(Engine&, LayerWeights&, cudaStream_t) {
-    throw Error(Kind::config, "FAST math is not built in this library version");
+enum Epi : int { EPI_RESID = 0, EPI_QKV = 1, EPI_GATEUP = 2, EPI_HEAD = 3 };
+
+struct GemmArgs {
+    const uint8_t* W;   // tiled, swizzled [tiles][KB][kABytes]
+    const uint8_t* X;   // swizzled [KB][kBBytes]
+    int tiles, KB;
+    int n_out;          // real output features (EPI_GATEUP: F, gate/up pairs)
+    float* partials;    // [tiles][kMaxPieces][kRows][kM]
+    int* counters;      // [tiles]
+    int rows, row0;     // valid rows of this pass, global row offset
+    // EPI_RESID: out[(row0+r)*ld + f] += y
+    // EPI_GATEUP: out[(row0+r)*ld + f] = silu(g)*u
+    // EPI_HEAD: out (nullable) logits [(row0+r)*ld + f]
+    float* out;
+    int ld;
+    // EPI_QKV
+    int qd, kvd, hd, max_len, prior;
+    const int32_t* pos;
+    const float* rope_cos;
+    const float* rope_sin;
+    float* kc;
+    float* vc;
+    // EPI_HEAD
+    float* amax_val;    // [rows_total][tiles]
+    int32_t* amax_idx;
+};
+
+// ── PTX wrappers ──────────────────────────────────────────────────────────
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>(1) << 16;            // LBO (unused for swizzled K-major)
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;    // SBO
+    d |= static_cast<uint64_t>(1) << 46;            // descriptor version (sm100)
+    d |= static_cast<uint64_t>(2) << 61;            // SWIZZLE_128B
+    return d;
 }
 
-int fast_forward_layer(Engine&, Bank&, int, int, Workspace&, int, cudaStream_t) {
-    throw Error(Kind::internal, "FAST math is not built in this library version");
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M x N.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kN >> 3) << 17) |
+                            (static_cast<uint32_t>(kM >> 4) << 24);
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(kIdesc), "r"(accum)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// Byte offset of element (row, kk) inside a [rows x 64] K-major SW128 tile.
+__host__ __device__ __forceinline__ uint32_t sw128_off(int row, int kk) {
+    return static_cast<uint32_t>((row >> 3) * 1024 + (row & 7) * 128 + (((kk >> 3) ^ (row & 7)) << 4) + (kk & 7) * 2);
+}
+
+// ── epilogues ─────────────────────────────────────────────────────────────
+// Thread = one output feature m of the tile (TMEM lane); y[r] for r < 16.
+template <int EPI>
+__device__ __forceinline__ void final_epilogue(const GemmArgs& a, int tile, int m, const float (&y)[kRows],
+                                               float* xch) {
+    const int f = tile * kM + m;
+    if constexpr (EPI == EPI_RESID) {
+        if (f < a.n_out)
+#pragma unroll
+            for (int r = 0; r < kRows; ++r)
+                if (r < a.rows) {
+                    float* o = a.out + static_cast<size_t>(a.row0 + r) * a.ld + f;
+                    *o = *o + y[r];
+                }
+    } else if constexpr (EPI == EPI_QKV) {
+        // features: [0,qd) q | [qd, qd+kvd) k | [qd+kvd, qd+2kvd) v; RoPE pairs
+        // (2i, 2i+1) sit on adjacent lanes of the same warp.
+        const bool valid = f < a.qd + 2 * a.kvd;
+        const int seg = f < a.qd ? 0 : (f < a.qd + a.kvd ? 1 : 2);
+        const int fl = seg == 0 ? f : (seg == 1 ? f - a.qd : f - a.qd - a.kvd);
+        const int d = fl % a.hd, half = a.hd >> 1, i = d >> 1;
+        const bool odd = (m & 1) != 0;
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) {
+            const float partner = __shfl_xor_sync(0xffffffffu, y[r], 1);
+            if (!valid || r >= a.rows) continue;
+            float v = y[r];
+            const int row = a.row0 + r;
+            if (seg != 2) {
+                const int p = a.pos[row];
+                const float c = a.rope_cos[static_cast<size_t>(p) * half + i];
+                const float s = a.rope_sin[static_cast<size_t>(p) * half + i];
+                v = odd ? __fadd_rn(__fmul_rn(partner, s), __fmul_rn(v, c))
+                        : __fsub_rn(__fmul_rn(v, c), __fmul_rn(partner, s));
+            }
+            if (seg == 0) {
+                a.out[static_cast<size_t>(row) * a.qd + fl] = v;
+            } else {
+                const int kvh = fl / a.hd;
+                float* dst = (seg == 1 ? a.kc : a.vc) +
+                             (static_cast<size_t>(kvh) * a.max_len + a.prior + row) * a.hd + d;
+                *dst = v;
+            }
+        }
+    } else if constexpr (EPI == EPI_GATEUP) {
+        // tile rows 0-63: gate features, 64-127: the matching up features
+        float* ub = xch;  // [64][kRows]
+        if (m >= 64)
+            for (int r = 0; r < kRows; ++r) ub[(m - 64) * kRows + r] = y[r];
+        named_sync(1, 128);
+        if (m < 64) {
+            const int fg = tile * 64 + m;
+            if (fg < a.n_out)
+#pragma unroll
+                for (int r = 0; r < kRows; ++r)
+                    if (r < a.rows) {
+                        const float g = y[r];
+                        const float silu = __fdiv_rn(g, __fadd_rn(1.0f, sfg_expf(-g)));
+                        a.out[static_cast<size_t>(a.row0 + r) * a.ld + fg] = __fmul_rn(silu, ub[m * kRows + r]);
+                    }
+        }
+        named_sync(1, 128);
+    } else {  // EPI_HEAD: logits + (max, argmax) per row over this tile
+        float* sv = xch;                                    // [4][kRows]
+        int* si = reinterpret_cast<int*>(xch + 4 * kRows);  // [4][kRows]
+        const int wq = (threadIdx.x >> 5) & 3;
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) {
+            float v = f < a.n_out ? y[r] : -INFINITY;
+            int idx = f < a.n_out ? f : 0x7fffffff;
+            if (a.out && f < a.n_out && r < a.rows) a.out[static_cast<size_t>(a.row0 + r) * a.ld + f] = y[r];
+            for (int o = 16; o > 0; o >>= 1) {
+                const float v2 = __shfl_xor_sync(0xffffffffu, v, o);
+                const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+                if (v2 > v || (v2 == v && i2 < idx)) {
+                    v = v2;
+                    idx = i2;
+                }
+            }
+            if ((threadIdx.x & 31) == 0) {
+                sv[wq * kRows + r] = v;
+                si[wq * kRows + r] = idx;
+            }
+        }
+        named_sync(1, 128);
+        if (m < a.rows) {
+            const int r = m;
+            float v = sv[r];
+            int idx = si[r];
+            for (int w = 1; w < 4; ++w) {
+                const float v2 = sv[w * kRows + r];
+                const int i2 = si[w * kRows + r];
+                if (v2 > v || (v2 == v && i2 < idx)) {
+                    v = v2;
+                    idx = i2;
+                }
+            }
+            a.amax_val[static_cast<size_t>(a.row0 + r) * a.tiles + tile] = v;
+            a.amax_idx[static_cast<size_t>(a.row0 + r) * a.tiles + tile] = idx;
+        }
+        named_sync(1, 128);
+    }
+}
+
+// ── the kernel ────────────────────────────────────────────────────────────
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ GemmArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int* flag = reinterpret_cast<int*>(tmem_slot + 4);
+    float* xch = reinterpret_cast<float*>(flag + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const long long U = static_cast<long long>(a.tiles) * a.KB;
+    const int G = gridDim.x, c = blockIdx.x;
+    const long long start = c * U / G, end = (c + 1) * U / G;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ── producer: bulk copies into the smem ring
+            int stage = 0;
+            uint32_t phase = 0;
+            for (long long u = start; u < end;) {
+                const int t = static_cast<int>(u / a.KB);
+                const int lo = static_cast<int>(u - static_cast<long long>(t) * a.KB);
+                const int hi = static_cast<int>(min(end - static_cast<long long>(t) * a.KB, static_cast<long long>(a.KB)));
+                for (int kb = lo; kb < hi; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * kStageBytes;
+                    mbar_expect_tx(&full[stage], kStageBytes);
+                    bulk_g2s(sa, a.W + (static_cast<size_t>(t) * a.KB + kb) * kABytes, kABytes, &full[stage]);
+                    bulk_g2s(sa + kABytes, a.X + static_cast<size_t>(kb) * kBBytes, kBBytes, &full[stage]);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                u = static_cast<long long>(t) * a.KB + hi;
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ── MMA issuer
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            for (long long u = start; u < end;) {
+                const int t = static_cast<int>(u / a.KB);
+                const int lo = static_cast<int>(u - static_cast<long long>(t) * a.KB);
+                const int hi = static_cast<int>(min(end - static_cast<long long>(t) * a.KB, static_cast<long long>(a.KB)));
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc * kAccCols;
+                for (int kb = lo; kb < hi; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + stage * kStageBytes);
+                    const uint64_t da = smem_desc(sa), db = smem_desc(sa + kABytes);
+#pragma unroll
+                    for (int k = 0; k < kKB / 16; ++k)  // +32 bytes per K=16 step inside the swizzle row
+                        mma_bf16(d, da + 2 * k, db + 2 * k, (kb > lo || k > 0) ? 1u : 0u);
+                    mma_commit(&empty[stage]);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit(&tfull[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+                u = static_cast<long long>(t) * a.KB + hi;
+            }
+        }
+    } else {  // ── epilogue warps 2..5 (TMEM lane quadrant = warp % 4)
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const int et = threadIdx.x - 64;  // 0..127
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (long long u = start; u < end;) {
+            const int t = static_cast<int>(u / a.KB);
+            const int lo = static_cast<int>(u - static_cast<long long>(t) * a.KB);
+            const int hi = static_cast<int>(min(end - static_cast<long long>(t) * a.KB, static_cast<long long>(a.KB)));
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            float v[kN];
+            const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * kAccCols;
+            tmem_ld16(ta, v);
+            tmem_ld16(ta + 16, v + 16);
+            tmem_ld16(ta + 32, v + 32);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+            float y[kRows];
+#pragma unroll
+            for (int r = 0; r < kRows; ++r) y[r] = (v[r] + v[kRows + r]) + v[2 * kRows + r];
+
+            if (lo == 0 && hi == a.KB) {
+                final_epilogue<EPI>(a, t, m, y, xch);
+            } else {
+                // split tile: deposit this piece, the last arriver reduces in k order
+                const long long first_u = static_cast<long long>(t) * a.KB;
+                const int c_first = static_cast<int>(((first_u + 1) * G - 1) / U);
+                const int piece = c - c_first;
+                const long long last_u = first_u + a.KB - 1;
+                const int n_pieces = static_cast<int>(((last_u + 1) * G - 1) / U) - c_first + 1;
+                float* slot = a.partials + (static_cast<size_t>(t) * kMaxPieces + piece) * kRows * kM;
+#pragma unroll
+                for (int r = 0; r < kRows; ++r) slot[r * kM + m] = y[r];
+                __threadfence();
+                named_sync(1, 128);
+                if (et == 0) {
+                    const int old = atomicAdd(&a.counters[t], 1);
+                    *flag = (old == n_pieces - 1) ? 1 : 0;
+                    if (old == n_pieces - 1) a.counters[t] = 0;  // reset for the next launch
+                }
+                named_sync(1, 128);
+                if (*flag) {
+                    __threadfence();
+                    float s[kRows];
+                    const float* p0 = a.partials + static_cast<size_t>(t) * kMaxPieces * kRows * kM;
+#pragma unroll
+                    for (int r = 0; r < kRows; ++r) s[r] = __ldcg(p0 + r * kM + m);
+                    for (int p = 1; p < n_pieces; ++p)
+#pragma unroll
+                        for (int r = 0; r < kRows; ++r) s[r] = s[r] + __ldcg(p0 + (static_cast<size_t>(p) * kRows + r) * kM + m);
+                    final_epilogue<EPI>(a, t, m, s, xch);
+                }
+                named_sync(1, 128);
+            }
+            u = static_cast<long long>(t) * a.KB + hi;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+    }
+}
+
+// ── activation prologue: [RMSNorm] + 3-way bf16 split into the swizzled B image
+// One CTA per row of the pass; rows beyond `rows` keep stale values, which
+// only feed their own (ignored) MMA columns.
+constexpr int kPrepThreads = 256;
+__global__ void __launch_bounds__(kPrepThreads) prep_kernel(const float* __restrict__ x, int ldx, int K,
+                                                            const float* __restrict__ gain, float eps,
+                                                            uint8_t* __restrict__ xs) {
+    const int r = blockIdx.x;
+    const float* xr = x + static_cast<size_t>(r) * ldx;
+    float scale = 1.0f;
+    if (gain) {
+        __shared__ float red[kPrepThreads / 32];
+        float ss = 0.0f;
+        for (int i = threadIdx.x; i < K; i += kPrepThreads) ss += xr[i] * xr[i];
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float t = 0.0f;
+            for (int w = 0; w < kPrepThreads / 32; ++w) t += red[w];
+            red[0] = 1.0f / sqrtf(t / static_cast<float>(K) + eps);
+        }
+        __syncthreads();
+        scale = red[0];
+    }
+    // each thread handles 8 consecutive k (one 16-byte chunk per piece)
+    for (int k8 = threadIdx.x * 8; k8 < K; k8 += kPrepThreads * 8) {
+        __align__(16) __nv_bfloat16 hi[8], mid[8], lo[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            float v = xr[k8 + e];
+            if (gain) v = (v * scale) * gain[k8 + e];
+            const __nv_bfloat16 h = __float2bfloat16_rn(v);
+            const float r1 = v - __bfloat162float(h);
+            const __nv_bfloat16 mm = __float2bfloat16_rn(r1);
+            hi[e] = h;
+            mid[e] = mm;
+            lo[e] = __float2bfloat16_rn(r1 - __bfloat162float(mm));
+        }
+        const int kb = k8 / kKB, kk = k8 % kKB;
+        uint8_t* base = xs + static_cast<size_t>(kb) * kBBytes;
+        *reinterpret_cast<uint4*>(base + sw128_off(r, kk)) = *reinterpret_cast<uint4*>(hi);
+        *reinterpret_cast<uint4*>(base + sw128_off(kRows + r, kk)) = *reinterpret_cast<uint4*>(mid);
+        *reinterpret_cast<uint4*>(base + sw128_off(2 * kRows + r, kk)) = *reinterpret_cast<uint4*>(lo);
+    }
+}
+
+// argmax over the per-tile partials (first maximum wins)
+__global__ void head_argmax_kernel(const float* __restrict__ val, const int32_t* __restrict__ idx, int tiles,
+                                   int32_t* __restrict__ out) {
+    const int r = blockIdx.x;
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+        const float v = val[static_cast<size_t>(r) * tiles + t];
+        const int i = idx[static_cast<size_t>(r) * tiles + t];
+        if (v > bv || (v == bv && i < bi)) {
+            bv = v;
+            bi = i;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (v2 > bv || (v2 == bv && i2 < bi)) {
+            bv = v2;
+            bi = i2;
+        }
+    }
+    __shared__ float sv[32];
+    __shared__ int si[32];
+    if ((threadIdx.x & 31) == 0) {
+        sv[threadIdx.x >> 5] = bv;
+        si[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+            if (sv[w] > bv || (sv[w] == bv && si[w] < bi)) {
+                bv = sv[w];
+                bi = si[w];
+            }
+        out[r] = bi == 0x7fffffff ? 0 : bi;
+    }
+}
+
+// ── weight re-layout: reference [K x N] (row-major, in x out) -> tiled SW128 W^T
+// kind 0: plain (feature f = tile*128 + m from src0 with ld n0)
+// kind 1: q|k|v concat   kind 2: gate/up interleave (64 + 64 per tile)
+__global__ void relayout_kernel(const __nv_bfloat16* __restrict__ s0, const __nv_bfloat16* __restrict__ s1,
+                                const __nv_bfloat16* __restrict__ s2, int n0, int n1, int n2, int kind, int K,
+                                int tiles, uint8_t* __restrict__ dst) {
+    const int KB = K / kKB;
+    const size_t total = static_cast<size_t>(tiles) * KB * kM * kKB;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        // e enumerates (tile, kb, kk, m) with m fastest so reads of a weight row coalesce
+        const int m = static_cast<int>(e % kM);
+        size_t rest = e / kM;
+        const int kk = static_cast<int>(rest % kKB);
+        rest /= kKB;
+        const int kb = static_cast<int>(rest % KB);
+        const int t = static_cast<int>(rest / KB);
+        const int k = kb * kKB + kk;
+        __nv_bfloat16 v = __float2bfloat16_rn(0.0f);
+        if (kind == 0) {
+            const int f = t * kM + m;
+            if (f < n0) v = s0[static_cast<size_t>(k) * n0 + f];
+        } else if (kind == 1) {
+            const int f = t * kM + m;
+            if (f < n0) v = s0[static_cast<size_t>(k) * n0 + f];
+            else if (f < n0 + n1) v = s1[static_cast<size_t>(k) * n1 + (f - n0)];
+            else if (f < n0 + n1 + n2) v = s2[static_cast<size_t>(k) * n2 + (f - n0 - n1)];
+        } else {
+            const int f = t * 64 + (m & 63);
+            if (f < n0) v = (m < 64 ? s0 : s1)[static_cast<size_t>(k) * n0 + f];
+        }
+        uint8_t* tileb = dst + (static_cast<size_t>(t) * KB + kb) * kABytes;
+        *reinterpret_cast<__nv_bfloat16*>(tileb + sw128_off(m, kk)) = v;
+    }
+}
+
+constexpr size_t smem_bytes() {
+    return 1024 + static_cast<size_t>(kStages) * kStageBytes + 2 * kStages * 8 + 4 * 8 + 16 + 16 +
+           (64 * kRows + 8 * kRows) * 4;
+}
+
+template <int EPI>
+void launch_gemm(const GemmArgs& a, int grid, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        SFG_CUDA(cudaFuncSetAttribute(gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem_bytes())));
+        configured = true;
+    }
+    gemm_kernel<EPI><<<grid, kThreads, smem_bytes(), s>>>(a);
+}
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
+int tiles_for(int n) { return (n + kM - 1) / kM; }
+
+}  // namespace fast
+
+using namespace fast;
+
+// ── workspace layout inside Workspace::fast ───────────────────────────────
+namespace {
+struct FastWs {
+    uint8_t* xs;       // [KBmax][kBBytes]
+    float* partials;   // [tiles_max][kMaxPieces][kRows][kM]
+    int* counters;     // [tiles_max]
+    float* amax_val;   // [rows][tiles_head]
+    int32_t* amax_idx;
+};
+size_t max_tiles(const ModelCfg& c) {
+    const int qkv = tiles_for(c.q_dim() + 2 * c.kv_dim());
+    const int gu = (c.ffn_dim + 63) / 64;
+    const int hv = tiles_for(c.vocab_size);
+    return static_cast<size_t>(std::max({qkv, gu, hv, tiles_for(c.hidden_dim)}));
+}
+size_t max_kb(const ModelCfg& c) {
+    return static_cast<size_t>(std::max({c.hidden_dim, c.q_dim(), c.ffn_dim}) / kKB);
+}
+FastWs carve(const ModelCfg& c, Workspace& ws, int rows) {
+    FastWs f;
+    uint8_t* p = static_cast<uint8_t*>(ws.fast);
+    auto take = [&](size_t bytes) {
+        uint8_t* r = p;
+        p += (bytes + 1023) & ~size_t(1023);
+        return r;
+    };
+    f.xs = take(max_kb(c) * kBBytes);
+    f.partials = reinterpret_cast<float*>(take(max_tiles(c) * kMaxPieces * kRows * kM * sizeof(float)));
+    f.counters = reinterpret_cast<int*>(take(max_tiles(c) * sizeof(int)));
+    f.amax_val = reinterpret_cast<float*>(take(static_cast<size_t>(rows) * tiles_for(c.vocab_size) * sizeof(float)));
+    f.amax_idx = reinterpret_cast<int32_t*>(take(static_cast<size_t>(rows) * tiles_for(c.vocab_size) * sizeof(int32_t)));
+    return f;
+}
+}  // namespace
+
+size_t fast_workspace_bytes(const ModelCfg& c, int rows) {
+    return max_kb(c) * kBBytes + max_tiles(c) * kMaxPieces * kRows * kM * sizeof(float) + max_tiles(c) * sizeof(int) +
+           2 * static_cast<size_t>(rows) * tiles_for(c.vocab_size) * sizeof(float) + 8 * 1024;
+}
+
+static void check_fast_shape(const ModelCfg& c) {
+    if (c.hidden_dim % kKB || c.q_dim() % kKB || c.ffn_dim % kKB)
+        throw Error(Kind::config, "FAST math needs hidden_dim, q_dim and ffn_dim to be multiples of 64");
+}
+
+static void* relayout(Engine& e, const void* s0, const void* s1, const void* s2, int n0, int n1, int n2, int kind,
+                      int K, int tiles, cudaStream_t s) {
+    void* dst = nullptr;
+    const size_t bytes = static_cast<size_t>(tiles) * (K / kKB) * kABytes;
+    SFG_CUDA(cudaMalloc(&dst, bytes));
+    relayout_kernel<<<2048, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(s0), static_cast<const __nv_bfloat16*>(s1),
+                                         static_cast<const __nv_bfloat16*>(s2), n0, n1, n2, kind, K, tiles,
+                                         static_cast<uint8_t*>(dst));
+    SFG_CUDA(cudaGetLastError());
+    e.adopt(dst, bytes);
+    return dst;
+}
+
+void fast_build_layer(Engine& e, LayerWeights& L, cudaStream_t s) {
+    const ModelCfg& c = e.cfg();
+    check_fast_shape(c);
+    const int H = c.hidden_dim, qd = c.q_dim(), kvd = c.kv_dim(), F = c.ffn_dim;
+    L.f_qkv = relayout(e, L.wq, L.wk, L.wv, qd, kvd, kvd, 1, H, tiles_for(qd + 2 * kvd), s);
+    L.f_o = relayout(e, L.wo, nullptr, nullptr, H, 0, 0, 0, qd, tiles_for(H), s);
+    L.f_gu = relayout(e, L.w_gate, L.w_up, nullptr, F, 0, 0, 2, H, (F + 63) / 64, s);
+    L.f_down = relayout(e, L.w_down, nullptr, nullptr, H, 0, 0, 0, F, tiles_for(H), s);
+}
+
+void* fast_build_head(Engine& e, const void* lm_head, cudaStream_t s) {
+    const ModelCfg& c = e.cfg();
+    check_fast_shape(c);
+    return relayout(e, lm_head, nullptr, nullptr, c.vocab_size, 0, 0, 0, c.hidden_dim, tiles_for(c.vocab_size), s);
+}
+
+static int grid_for(int tiles, int KB) {
+    const long long U = static_cast<long long>(tiles) * KB;
+    return static_cast<int>(std::min<long long>(U, num_sms()));
+}
+
+// One layer of forward_layers (tinyformer.cpp:412-504) in FAST math.
+int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, int prior, cudaStream_t s) {
+    const ModelCfg& c = e.cfg();
+    const Dims d = e.dims();
+    const LayerWeights& L = e.layer(layer);
+    FastWs f = carve(c, ws, ws.cap_rows);
+    float* kc = b.kslab(layer);
+    float* vc = b.vslab(layer);
+    int n = 0;
+    const double R = rows;
+    for (int p0 = 0; p0 < rows; p0 += kRows) {
+        const int pr = std::min(kRows, rows - p0);
+        GemmArgs a{};
+        a.X = f.xs;
+        a.partials = f.partials;
+        a.counters = f.counters;
+        a.rows = pr;
+        a.row0 = p0;
+        // attention-input RMSNorm + split, fused QKV + RoPE + KV append
+        prep_kernel<<<pr, kPrepThreads, 0, s>>>(ws.h + static_cast<size_t>(p0) * d.H, d.H, d.H, L.attn_norm, d.eps, f.xs);
+        ++n;
+        a.W = static_cast<const uint8_t*>(L.f_qkv);
+        a.tiles = tiles_for(d.qd + 2 * d.kvd);
+        a.KB = d.H / kKB;
+        a.n_out = d.qd + 2 * d.kvd;
+        a.out = ws.q;
+        a.qd = d.qd;
+        a.kvd = d.kvd;
+        a.hd = d.hd;
+        a.max_len = d.max_len;
+        a.prior = prior;
+        a.pos = ws.pos;
+        a.rope_cos = e.rope_cos();
+        a.rope_sin = e.rope_sin();
+        a.kc = kc;
+        a.vc = vc;
+        {
+            ProfScope ps(K_QKV, s, 2.0 * d.H * a.n_out + 4.0 * pr * (d.H + a.n_out), 2.0 * pr * d.H * a.n_out);
+            launch_gemm<EPI_QKV>(a, grid_for(a.tiles, a.KB), s);
+        }
+        ++n;
+    }
+    {
+        const double kvb = 2.0 * 4.0 * d.kvd * (prior + rows);
+        ProfScope ps(K_ATTN, s, kvb + 8.0 * R * d.qd, 4.0 * R * d.qd * (prior + rows));
+        n += launch_attention_exact(ws.q, kc, vc, ws.row_off, ws.runs, rows, prior + rows, d, ws.att, ws.status, s);
+    }
+    for (int p0 = 0; p0 < rows; p0 += kRows) {
+        const int pr = std::min(kRows, rows - p0);
+        GemmArgs a{};
+        a.X = f.xs;
+        a.partials = f.partials;
+        a.counters = f.counters;
+        a.rows = pr;
+        a.row0 = p0;
+        // O-proj + residual
+        prep_kernel<<<pr, kPrepThreads, 0, s>>>(ws.att + static_cast<size_t>(p0) * d.qd, d.qd, d.qd, nullptr, 0.f, f.xs);
+        a.W = static_cast<const uint8_t*>(L.f_o);
+        a.tiles = tiles_for(d.H);
+        a.KB = d.qd / kKB;
+        a.n_out = d.H;
+        a.out = ws.h;
+        a.ld = d.H;
+        {
+            ProfScope ps(K_OPROJ, s, 2.0 * d.qd * d.H + 4.0 * pr * (d.qd + 2.0 * d.H), 2.0 * pr * d.qd * d.H);
+            launch_gemm<EPI_RESID>(a, grid_for(a.tiles, a.KB), s);
+        }
+        // FFN RMSNorm + split, gate|up + SiLU*up
+        prep_kernel<<<pr, kPrepThreads, 0, s>>>(ws.h + static_cast<size_t>(p0) * d.H, d.H, d.H, L.ffn_norm, d.eps, f.xs);
+        a.W = static_cast<const uint8_t*>(L.f_gu);
+        a.tiles = (d.F + 63) / 64;
+        a.KB = d.H / kKB;
+        a.n_out = d.F;
+        a.out = ws.act;
+        a.ld = d.F;
+        {
+            ProfScope ps(K_GATEUP, s, 4.0 * d.H * d.F + 4.0 * pr * (d.H + d.F), 4.0 * pr * d.H * d.F);
+            launch_gemm<EPI_GATEUP>(a, grid_for(a.tiles, a.KB), s);
+        }
+        // down + residual
+        prep_kernel<<<pr, kPrepThreads, 0, s>>>(ws.act + static_cast<size_t>(p0) * d.F, d.F, d.F, nullptr, 0.f, f.xs);
+        a.W = static_cast<const uint8_t*>(L.f_down);
+        a.tiles = tiles_for(d.H);
+        a.KB = d.F / kKB;
+        a.n_out = d.H;
+        a.out = ws.h;
+        a.ld = d.H;
+        {
+            ProfScope ps(K_DOWN, s, 2.0 * d.F * d.H + 4.0 * pr * (d.F + 2.0 * d.H), 2.0 * pr * d.F * d.H);
+            launch_gemm<EPI_RESID>(a, grid_for(a.tiles, a.KB), s);
+        }
+        n += 6;
+    }
+    SFG_CUDA(cudaGetLastError());
+    return n;
+}
+
+// finalize (tinyformer.cpp:510-526) + argmax_row in FAST math: final RMSNorm
+// + split, LM-head GEMM with logits/argmax-partial epilogue, partial reduce.
+int fast_head(Engine& e, const void* f_lm_head, const float* final_norm, int rows, Workspace& ws, bool want_logits,
+              cudaStream_t s) {
+    const ModelCfg& c = e.cfg();
+    FastWs f = carve(c, ws, ws.cap_rows);
+    const int tiles = tiles_for(c.vocab_size);
+    int n = 0;
+    for (int p0 = 0; p0 < rows; p0 += kRows) {
+        const int pr = std::min(kRows, rows - p0);
+        prep_kernel<<<pr, kPrepThreads, 0, s>>>(ws.h + static_cast<size_t>(p0) * c.hidden_dim, c.hidden_dim,
+                                                c.hidden_dim, final_norm, c.rms_eps, f.xs);
+        GemmArgs a{};
+        a.W = static_cast<const uint8_t*>(f_lm_head);
+        a.X = f.xs;
+        a.tiles = tiles;
+        a.KB = c.hidden_dim / kKB;
+        a.n_out = c.vocab_size;
+        a.partials = f.partials;
+        a.counters = f.counters;
+        a.rows = pr;
+        a.row0 = p0;
+        a.out = want_logits ? ws.logits : nullptr;
+        a.ld = c.vocab_size;
+        a.amax_val = f.amax_val;
+        a.amax_idx = f.amax_idx;
+        {
+            ProfScope ps(K_HEAD, s, 2.0 * c.hidden_dim * c.vocab_size + 4.0 * pr * (c.hidden_dim + c.vocab_size),
+                         2.0 * pr * c.hidden_dim * c.vocab_size);
+            launch_gemm<EPI_HEAD>(a, grid_for(a.tiles, a.KB), s);
+        }
+        n += 2;
+    }
+    head_argmax_kernel<<<rows, 256, 0, s>>>(f.amax_val, f.amax_idx, tiles, ws.argmax);
+    SFG_CUDA(cudaGetLastError());
+    return n + 1;
 }
 
 }  // namespace sfg
