@@ -298,8 +298,7 @@ int32_t sfg_client_last_profile(sfg_client* c, sfg_step_profile* out) {
     return SFG_OK;
 }
 
-static int g_graphs = 1;
-void sfg_set_graphs(int32_t enabled) { g_graphs = enabled; }
+void sfg_set_graphs(int32_t enabled) { graphs_enabled() = enabled != 0; }
 
 void sfg_profiler_enable(int32_t on) { KernelProfiler::get().enable(on != 0); }
 void sfg_profiler_reset(void) { KernelProfiler::get().reset(); }

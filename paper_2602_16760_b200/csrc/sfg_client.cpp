@@ -1,9 +1,16 @@
 // Trusted-side runtime: SplitClient::prefill/decode_step (client.cpp:120-228)
 // and decode_sequential / decode_lookahead_with_pool (decoding.cpp:111-355)
-// on the B200.  Per step the device runs [KV compaction] -> embed -> prefix
-// layers -> [wire] -> suffix layers -> final norm + LM head -> argmax ->
-// verify/branch selection, enqueued without host synchronisation; only the
-// committed-token summary (VerifyOut) returns to the host.
+// on the B200.
+//
+// A decode step splits into host work (protocol checks and cache
+// bookkeeping, exactly as the reference orders them) and one device
+// sequence: [inputs H2D] -> in-place KV compaction (prefix, suffix and, when
+// device-linked, the server's bank) -> embed -> prefix layers -> wire round
+// trip -> server layers -> wire round trip -> suffix layers -> final norm +
+// LM head -> argmax -> verify/branch selection -> [summary D2H].  Every
+// per-step scalar lives in device memory (Workspace::meta), so the device
+// sequence of a device-linked step is captured once per batch size as a
+// CUDA graph and replayed.
 #include "sfg_client.h"
 
 #include <algorithm>
@@ -11,6 +18,8 @@
 #include <cstring>
 #include <random>
 #include <thread>
+
+#include "sfg_prof.h"
 
 namespace sfg {
 
@@ -111,8 +120,19 @@ Client::Client(Engine& local, const ClientCfg& cfg, sfg_frame_handler handler, v
     if (cfg_.prefix_layers + cfg_.suffix_layers >= c.n_layers)
         throw Error(Kind::config, "prefix + suffix must leave a non-empty middle range");
     if (!handler_ && !linked_) throw Error(Kind::config, "client needs a frame handler or a linked server");
-    if (linked_ && linked_->engine().device() != local.device())
-        throw Error(Kind::config, "a linked server must live on the client's device");
+    if (linked_) {
+        const Engine& se = linked_->engine();
+        const ModelCfg& sc = se.cfg();
+        if (se.device() != local.device()) throw Error(Kind::config, "a linked server must live on the client's device");
+        if (se.fast() != local.fast()) throw Error(Kind::config, "a linked server must use the client's math mode");
+        if (sc.hidden_dim != c.hidden_dim || sc.ffn_dim != c.ffn_dim || sc.n_heads != c.n_heads ||
+            sc.n_kv_heads != c.n_kv_heads || sc.head_dim != c.head_dim || sc.vocab_size != c.vocab_size ||
+            sc.max_seq_len != c.max_seq_len || sc.n_layers != c.n_layers)
+            throw Error(Kind::config, "a linked server must serve the client's model shape");
+        if (linked_->config().layer_begin != cfg_.prefix_layers ||
+            linked_->config().layer_end != c.n_layers - cfg_.suffix_layers)
+            throw Error(Kind::config, "server layer range does not match the client split");
+    }
     if (sid_.empty()) {  // random_session_id (client.cpp:16-23)
         static const char* hex = "0123456789abcdef";
         std::random_device rd;
@@ -128,16 +148,23 @@ Client::Client(Engine& local, const ClientCfg& cfg, sfg_frame_handler handler, v
     SFG_CUDA(cudaMalloc(&d_vout_, sizeof(VerifyOut)));
     SFG_CUDA(cudaMallocHost(&h_vin_, sizeof(VerifyIn)));
     SFG_CUDA(cudaMallocHost(&h_vout_, sizeof(VerifyOut)));
+    std::memset(h_vin_, 0, sizeof(VerifyIn));
 }
 
 Client::~Client() {
     DeviceGuard g(eng_.device());
     cudaStreamSynchronize(prefix_->stream());
+    for (auto& gr : graphs_) {
+        if (gr.exec) cudaGraphExecDestroy(gr.exec);
+        KernelProfiler::get().release_graph(gr.prof_slots);
+    }
     for (auto& e : ev_) cudaEventDestroy(e);
     cudaFree(d_vin_);
     cudaFree(d_vout_);
     cudaFreeHost(h_vin_);
     cudaFreeHost(h_vout_);
+    if (h_argmax_) cudaFreeHost(h_argmax_);
+    if (h_logits_) cudaFreeHost(h_logits_);
 }
 
 uint64_t Client::clamped() {
@@ -160,39 +187,98 @@ void Client::sleep_one_way() const {
     }
 }
 
-// One request/response exchange of the hidden rows currently in ws.h.
-void Client::exchange(bool prompt, int seq, const int32_t* pos, const MaskRuns* runs, int mask_kv,
-                      const int32_t* keep, int n_keep, bool send_keep, std::optional<int> crop) {
+void Client::ensure_out(int rows) {
+    if (rows <= out_rows_) return;
+    SFG_CUDA(cudaDeviceSynchronize());
+    if (h_argmax_) cudaFreeHost(h_argmax_);
+    if (h_logits_) cudaFreeHost(h_logits_);
+    const int r = std::max(rows, 16);
+    SFG_CUDA(cudaMallocHost(&h_argmax_, sizeof(int32_t) * r));
+    SFG_CUDA(cudaMallocHost(&h_logits_, sizeof(float) * static_cast<size_t>(r) * eng_.cfg().vocab_size));
+    out_rows_ = r;
+    for (auto& gr : graphs_) gr.generation = ~0ull;  // outputs moved: recapture
+}
+
+// Host staging of the step inputs at cap-derived offsets (fixed addresses,
+// so a captured graph's copy nodes stay valid).
+void Client::stage_inputs(int seq, const int32_t* ids, const int32_t* pos, const MaskRuns& mr) {
+    Workspace& ws = prefix_->ws();
+    const StageLayout L = stage_layout(ws.cap_rows, ws.cap_runs);
+    char* p = static_cast<char*>(ws.stage_pin);
+    std::memcpy(p + L.ids, ids, sizeof(int32_t) * seq);
+    std::memcpy(p + L.pos, pos, sizeof(int32_t) * seq);
+    std::memcpy(p + L.roff, mr.row_off.data(), sizeof(int32_t) * mr.row_off.size());
+    std::memcpy(p + L.runs, mr.runs.data(), sizeof(MaskRun) * mr.runs.size());
+}
+
+// [inputs H2D] -> compaction -> embed -> prefix layers
+int Client::dev_pre(int rows, Bank* server_bank, bool verify, cudaStream_t s) {
+    const ModelCfg& c = eng_.cfg();
+    Workspace& ws = prefix_->ws();
+    const StageLayout L = stage_layout(ws.cap_rows, ws.cap_runs);
+    const char* p = static_cast<const char*>(ws.stage_pin);
+    int n = 0;
+    SFG_CUDA(cudaMemcpyAsync(ws.meta, ws.meta_pin, sizeof(int32_t) * (4 + kMetaKeep), cudaMemcpyHostToDevice, s));
+    SFG_CUDA(cudaMemcpyAsync(ws.ids, p + L.ids, sizeof(int32_t) * ws.cap_rows, cudaMemcpyHostToDevice, s));
+    SFG_CUDA(cudaMemcpyAsync(ws.pos, p + L.pos, sizeof(int32_t) * ws.cap_rows, cudaMemcpyHostToDevice, s));
+    SFG_CUDA(cudaMemcpyAsync(ws.row_off, p + L.roff, sizeof(int32_t) * (ws.cap_rows + 1), cudaMemcpyHostToDevice, s));
+    SFG_CUDA(cudaMemcpyAsync(ws.runs, p + L.runs, sizeof(MaskRun) * ws.cap_runs, cudaMemcpyHostToDevice, s));
+    if (verify) SFG_CUDA(cudaMemcpyAsync(d_vin_, h_vin_, sizeof(VerifyIn), cudaMemcpyHostToDevice, s));
+    SFG_CUDA(cudaMemsetAsync(ws.status, 0, sizeof(uint32_t), s));
+    const int mk = std::min(kMetaKeep, ws.cap_rows);
+    for (Bank* b : {prefix_.get(), suffix_.get(), server_bank}) {
+        if (!b || b->layer_end() == b->layer_begin()) continue;
+        n += launch_kv_compact_meta(b->kslab(b->layer_begin()), b->vslab(b->layer_begin()),
+                                    b->layer_end() - b->layer_begin(), c.n_kv_heads, c.max_seq_len, c.head_dim,
+                                    ws.meta, mk, s);
+    }
+    n += eng_.embed_device(rows, ws, s);
+    n += eng_.forward_device(*prefix_, 0, cfg_.prefix_layers, rows, ws, s);
+    return n;
+}
+
+// wire round trip -> server layers (device-linked) -> wire round trip
+int Client::dev_server(int rows, Bank* server_bank, cudaStream_t s) {
+    const ModelCfg& c = eng_.cfg();
+    Workspace& ws = prefix_->ws();
+    const int n = rows * c.hidden_dim;
+    const int f32 = cfg_.wire_dtype == SFG_WIRE_F32;
+    int k = launch_wire_roundtrip(ws.h, f32, n, ws.clamped, s);  // encode/decode_values
+    k += launch_link_delay(cfg_.one_way_delay_ms, s);             // request leg
+    SFG_CUDA(cudaEventRecord(ev_[1], s));
+    k += linked_->engine().forward_device(*server_bank, linked_->config().layer_begin, linked_->config().layer_end,
+                                          rows, ws, s);
+    SFG_CUDA(cudaEventRecord(ev_[2], s));
+    const int rd = linked_->config().response_dtype;
+    k += launch_wire_roundtrip(ws.h, rd < 0 ? f32 : rd == SFG_WIRE_F32, n, nullptr, s);
+    k += launch_link_delay(cfg_.one_way_delay_ms, s);             // response leg
+    return k;
+}
+
+// suffix layers -> head -> argmax -> verify -> [summary D2H]
+int Client::dev_post(int rows, bool want_logits, bool verify, cudaStream_t s) {
+    const ModelCfg& c = eng_.cfg();
+    Workspace& ws = prefix_->ws();
+    int n = eng_.forward_device(*suffix_, c.n_layers - cfg_.suffix_layers, c.n_layers, rows, ws, s);
+    n += eng_.head_device(rows, ws, want_logits, true, s);
+    if (verify) {
+        n += launch_verify(ws.argmax, d_vin_, d_vout_, s);
+        SFG_CUDA(cudaMemcpyAsync(h_vout_, d_vout_, sizeof(VerifyOut), cudaMemcpyDeviceToHost, s));
+    }
+    SFG_CUDA(cudaMemcpyAsync(h_argmax_, ws.argmax, sizeof(int32_t) * rows, cudaMemcpyDeviceToHost, s));
+    if (want_logits)
+        SFG_CUDA(cudaMemcpyAsync(h_logits_, ws.logits, sizeof(float) * rows * c.vocab_size, cudaMemcpyDeviceToHost, s));
+    return n;
+}
+
+// Frame path: device pack -> host frame -> handler -> host frame -> device unpack
+void Client::exchange_frames(bool prompt, int seq, const int32_t* pos, const MaskRuns* runs, int mask_kv,
+                             const int32_t* keep, int n_keep, bool send_keep, std::optional<int> crop) {
     const ModelCfg& c = eng_.cfg();
     Workspace& ws = prefix_->ws();
     cudaStream_t s = prefix_->stream();
     const int n = seq * c.hidden_dim;
     const int f32 = cfg_.wire_dtype == SFG_WIRE_F32;
-    if (linked_) {
-        // encode_values/decode_values round trip on device (the values the
-        // frame would carry), then the server's middle layers in place.
-        prof_.launches += launch_wire_roundtrip(ws.h, f32, n, ws.clamped, s);
-        sleep_one_way();
-        std::vector<int64_t> kv;
-        if (send_keep) kv.assign(keep, keep + n_keep);
-        Server::LinkedStep st{&sid_, prompt, seq, pos, send_keep ? &kv : nullptr,
-                              crop ? std::optional<int64_t>(*crop) : std::nullopt,
-                              runs, seq, mask_kv, ws.h, s};
-        SFG_CUDA(cudaEventRecord(ev_[1], s));
-        try {
-            prof_.launches += linked_->linked_step(st);
-        } catch (const Error& e) {  // exchange_hidden marks the client dead
-            dead_ = true;
-            throw Error(e.kind(), std::string("server: ") + e.what());
-        }
-        SFG_CUDA(cudaEventRecord(ev_[2], s));
-        const int rd = linked_->config().response_dtype;
-        const int rf = rd < 0 ? f32 : rd == SFG_WIRE_F32;
-        prof_.launches += launch_wire_roundtrip(ws.h, rf, n, nullptr, s);
-        sleep_one_way();
-        return;
-    }
-    // frame path: device pack -> host frame -> handler -> host frame -> device unpack
     const size_t wbytes = static_cast<size_t>(n) * (f32 ? 4 : 2);
     prof_.launches += launch_pack_rows(ws.h, f32, n, ws.wire, ws.clamped, s);
     payload_.resize(wbytes);
@@ -254,31 +340,6 @@ void Client::exchange(bool prompt, int seq, const int32_t* pos, const MaskRuns* 
     SFG_CUDA(cudaStreamSynchronize(s));  // rcopy must outlive the copy
 }
 
-static void upload_local_meta(Engine& e, Workspace& ws, int seq, const int32_t* ids, const int32_t* pos,
-                              const MaskRuns& mr, cudaStream_t s) {
-    e.ensure_ws(ws, seq, static_cast<int>(mr.runs.size()), seq);
-    char* pin = static_cast<char*>(ws.pinned);
-    const size_t ib = sizeof(int32_t) * seq, rb = sizeof(int32_t) * mr.row_off.size(),
-                 ub = sizeof(MaskRun) * mr.runs.size();
-    if (2 * ib + rb + ub > ws.pinned_bytes / 2) {
-        SFG_CUDA(cudaMemcpyAsync(ws.ids, ids, ib, cudaMemcpyHostToDevice, s));
-        SFG_CUDA(cudaMemcpyAsync(ws.pos, pos, ib, cudaMemcpyHostToDevice, s));
-        SFG_CUDA(cudaMemcpyAsync(ws.row_off, mr.row_off.data(), rb, cudaMemcpyHostToDevice, s));
-        SFG_CUDA(cudaMemcpyAsync(ws.runs, mr.runs.data(), ub, cudaMemcpyHostToDevice, s));
-        SFG_CUDA(cudaStreamSynchronize(s));
-        return;
-    }
-    // staging is free: the previous step ended with a stream sync
-    std::memcpy(pin, ids, ib);
-    std::memcpy(pin + ib, pos, ib);
-    std::memcpy(pin + 2 * ib, mr.row_off.data(), rb);
-    std::memcpy(pin + 2 * ib + rb, mr.runs.data(), ub);
-    SFG_CUDA(cudaMemcpyAsync(ws.ids, pin, ib, cudaMemcpyHostToDevice, s));
-    SFG_CUDA(cudaMemcpyAsync(ws.pos, pin + ib, ib, cudaMemcpyHostToDevice, s));
-    SFG_CUDA(cudaMemcpyAsync(ws.row_off, pin + 2 * ib, rb, cudaMemcpyHostToDevice, s));
-    SFG_CUDA(cudaMemcpyAsync(ws.runs, pin + 2 * ib + rb, ub, cudaMemcpyHostToDevice, s));
-}
-
 // SplitClient::prefill (client.cpp:120-167)
 int Client::prefill(const int32_t* prompt, int n, float* logits_row) {
     const ModelCfg& c = eng_.cfg();
@@ -299,12 +360,27 @@ int Client::prefill(const int32_t* prompt, int n, float* logits_row) {
     const MaskRuns mr = causal_runs(n, 0);
     prof_ = StepProfile{};
     prof_.batch = n;
-    upload_local_meta(eng_, ws, n, prompt, pos.data(), mr, s);
-    prof_.launches += eng_.embed_device(n, ws, s);
-    prof_.launches += eng_.forward_device(*prefix_, 0, cfg_.prefix_layers, n, ws, s);
+    eng_.ensure_ws(ws, n, static_cast<int>(mr.runs.size()), 1);
+    ensure_out(1);
+    stage_inputs(n, prompt, pos.data(), mr);
+    std::memset(ws.meta_pin, 0, sizeof(int32_t) * 4);  // prior 0, no relocation
+    prof_.launches += dev_pre(n, nullptr, false, s);
     prefix_->set_len(n);
     prefix_->mark_committed(n);
-    exchange(true, n, pos.data(), nullptr, n, nullptr, 0, false, std::nullopt);
+    if (linked_) {
+        Server::LinkedStep st{&sid_, true, n, pos.data(), nullptr, std::nullopt, nullptr, n, n};
+        Server::Lease lease;
+        try {
+            lease = linked_->linked_begin(st);
+        } catch (const Error& e) {
+            dead_ = true;
+            throw Error(e.kind(), std::string("server: ") + e.what());
+        }
+        prof_.launches += dev_server(n, lease.bank, s);  // link delays run on the device timeline
+        linked_->linked_end(lease, n);
+    } else {
+        exchange_frames(true, n, pos.data(), nullptr, n, nullptr, 0, false, std::nullopt);
+    }
     prof_.launches += eng_.forward_device(*suffix_, c.n_layers - cfg_.suffix_layers, c.n_layers, n, ws, s);
     suffix_->set_len(n);
     suffix_->mark_committed(n);
@@ -313,15 +389,41 @@ int Client::prefill(const int32_t* prompt, int n, float* logits_row) {
         SFG_CUDA(cudaMemcpyAsync(ws.h, ws.h + static_cast<size_t>(n - 1) * c.hidden_dim,
                                  sizeof(float) * c.hidden_dim, cudaMemcpyDeviceToDevice, s));
     prof_.launches += eng_.head_device(1, ws, logits_row != nullptr, true, s);
-    int32_t first = 0;
-    SFG_CUDA(cudaMemcpyAsync(&first, ws.argmax, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SFG_CUDA(cudaMemcpyAsync(h_argmax_, ws.argmax, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     if (logits_row)
-        SFG_CUDA(cudaMemcpyAsync(logits_row, ws.logits, sizeof(float) * c.vocab_size, cudaMemcpyDeviceToHost, s));
+        SFG_CUDA(cudaMemcpyAsync(h_logits_, ws.logits, sizeof(float) * c.vocab_size, cudaMemcpyDeviceToHost, s));
     SFG_CUDA(cudaStreamSynchronize(s));
     SFG_CUDA(cudaGetLastError());
+    if (logits_row) std::memcpy(logits_row, h_logits_, sizeof(float) * c.vocab_size);
     prompt_len_ = n;
     prefilled_ = true;
-    return first;
+    return h_argmax_[0];
+}
+
+Client::Graph* Client::find_graph(int rows, bool logits, bool verify, Bank* server_bank) {
+    const uint64_t gen = prefix_->ws().generation;
+    for (auto& g : graphs_)
+        if (g.rows == rows && g.logits == logits && g.verify == verify && g.server_bank == server_bank &&
+            g.generation == gen)
+            return &g;
+    // drop stale entries (workspace reallocated or server session replaced)
+    for (auto it = graphs_.begin(); it != graphs_.end();) {
+        if (it->generation != gen || graphs_.size() > 16) {
+            if (it->exec) cudaGraphExecDestroy(it->exec);
+            KernelProfiler::get().release_graph(it->prof_slots);
+            it = graphs_.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    Graph g;
+    g.rows = rows;
+    g.logits = logits;
+    g.verify = verify;
+    g.server_bank = server_bank;
+    g.generation = gen;
+    graphs_.push_back(g);
+    return &graphs_.back();
 }
 
 // SplitClient::decode_step (client.cpp:169-228)
@@ -340,11 +442,14 @@ void Client::decode_step(int seq, const int32_t* tokens, const int32_t* position
     int kv = 0;
     MaskRuns causal;
     const MaskRuns* mr = runs;
-    SFG_CUDA(cudaEventRecord(ev_[0], s));
+    const int committed_before = prefix_->committed_len();
+    bool relocate = false;
     try {
         if (n_keep > 0 || prefix_->provisional() > 0) {
-            prefix_->resolve(keep, n_keep, s);
-            suffix_->resolve(keep, n_keep, s);
+            if (n_keep > kMetaKeep) throw Error(Kind::input, "keep list longer than 256 entries");
+            prefix_->resolve_meta(keep, n_keep);
+            suffix_->resolve_meta(keep, n_keep);
+            relocate = n_keep > 0;
         }
         if (crop) {
             prefix_->crop(*crop);
@@ -364,37 +469,99 @@ void Client::decode_step(int seq, const int32_t* tokens, const int32_t* position
             mr = &causal;
         }
         if (mr->any_empty_row) throw Error(Kind::protocol, "mask row admits no attendable position");
-        upload_local_meta(eng_, ws, seq, tokens, positions, *mr, s);
-        prof_.launches += eng_.embed_device(seq, ws, s);
-        prof_.launches += eng_.forward_device(*prefix_, 0, cfg_.prefix_layers, seq, ws, s);
-        prefix_->set_len(kv);
     } catch (...) {
         dead_ = true;
         throw;
     }
-    // decode loops always send their mask; a null runs pointer means "no
-    // mask" on the wire and the causal law on both sides.
-    exchange(false, seq, positions, runs, kv, keep, n_keep, first_step_done_, crop);
-    prof_.launches += eng_.forward_device(*suffix_, c.n_layers - cfg_.suffix_layers, c.n_layers, seq, ws, s);
-    suffix_->set_len(kv);
-    prof_.launches += eng_.head_device(seq, ws, logits_out != nullptr, true, s);
-    if (vin) {  // fused verify tail: argmax rows -> branch selection on device
-        std::memcpy(h_vin_, vin, sizeof(VerifyIn));
-        SFG_CUDA(cudaMemcpyAsync(d_vin_, h_vin_, sizeof(VerifyIn), cudaMemcpyHostToDevice, s));
-        prof_.launches += launch_verify(ws.argmax, d_vin_, d_vout_, s);
-        SFG_CUDA(cudaMemcpyAsync(h_vout_, d_vout_, sizeof(VerifyOut), cudaMemcpyDeviceToHost, s));
+    const bool want_logits = logits_out != nullptr;
+    eng_.ensure_ws(ws, seq, static_cast<int>(mr->runs.size()), seq);
+    ensure_out(seq);
+    stage_inputs(seq, tokens, positions, *mr);
+    ws.meta_pin[0] = prefix_->len();
+    ws.meta_pin[1] = committed_before;
+    ws.meta_pin[2] = relocate ? n_keep : 0;
+    if (relocate) std::memcpy(ws.meta_pin + 3, keep, sizeof(int32_t) * n_keep);
+    if (vin) std::memcpy(h_vin_, vin, sizeof(VerifyIn));
+    const bool send_keep = first_step_done_;
+
+    if (linked_) {
+        std::vector<int64_t> kv64;
+        if (send_keep) kv64.assign(keep, keep + n_keep);
+        Server::LinkedStep st{&sid_, false, seq, positions, send_keep ? &kv64 : nullptr,
+                              crop ? std::optional<int64_t>(*crop) : std::nullopt, runs, seq, kv};
+        Server::Lease lease;
+        try {
+            lease = linked_->linked_begin(st);
+        } catch (const Error& e) {
+            dead_ = true;
+            throw Error(e.kind(), std::string("server: ") + e.what());
+        }
+        if (lease.committed_before != committed_before || lease.prior != prefix_->len() ||
+            lease.n_keep != (relocate ? n_keep : lease.n_keep)) {
+            dead_ = true;
+            throw Error(Kind::internal, "client and server caches out of lockstep");
+        }
+        SFG_CUDA(cudaEventRecord(ev_[0], s));
+        Graph* gr = nullptr;
+        if (graphs_enabled()) {
+            gr = find_graph(seq, want_logits, vin != nullptr, lease.bank);
+            ++gr->seen;
+        }
+        if (gr && gr->exec) {
+            SFG_CUDA(cudaGraphLaunch(gr->exec, s));
+            prof_.launches = gr->launches;
+            prof_.graph = true;
+        } else if (gr && gr->seen >= 2) {  // first replay-eligible occurrence: capture
+            KernelProfiler::get().begin_capture(&gr->prof_slots);
+            SFG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            int k = 0;
+            try {
+                k += dev_pre(seq, lease.bank, vin != nullptr, s);
+                k += dev_server(seq, lease.bank, s);
+                k += dev_post(seq, want_logits, vin != nullptr, s);
+            } catch (...) {
+                cudaGraph_t dead = nullptr;
+                cudaStreamEndCapture(s, &dead);
+                if (dead) cudaGraphDestroy(dead);
+                KernelProfiler::get().end_capture();
+                throw;
+            }
+            cudaGraph_t graph = nullptr;
+            SFG_CUDA(cudaStreamEndCapture(s, &graph));
+            KernelProfiler::get().end_capture();
+            SFG_CUDA(cudaGraphInstantiate(&gr->exec, graph, 0));
+            cudaGraphDestroy(graph);
+            gr->launches = k;
+            SFG_CUDA(cudaGraphLaunch(gr->exec, s));
+            prof_.launches = k;
+            prof_.graph = true;
+        } else {
+            prof_.launches += dev_pre(seq, lease.bank, vin != nullptr, s);
+            prof_.launches += dev_server(seq, lease.bank, s);
+            prof_.launches += dev_post(seq, want_logits, vin != nullptr, s);
+        }
+        SFG_CUDA(cudaEventRecord(ev_[3], s));
+        linked_->linked_end(lease, seq);
+        SFG_CUDA(cudaEventSynchronize(ev_[3]));
+        if (gr && gr->exec && KernelProfiler::get().on()) KernelProfiler::get().collect_graph(gr->prof_slots);
+    } else {
+        SFG_CUDA(cudaEventRecord(ev_[0], s));
+        prof_.launches += dev_pre(seq, nullptr, vin != nullptr, s);
+        exchange_frames(false, seq, positions, runs, kv, keep, n_keep, send_keep, crop);
+        prof_.launches += dev_post(seq, want_logits, vin != nullptr, s);
+        SFG_CUDA(cudaEventRecord(ev_[3], s));
+        SFG_CUDA(cudaEventSynchronize(ev_[3]));
     }
-    if (argmax_out) SFG_CUDA(cudaMemcpyAsync(argmax_out, ws.argmax, sizeof(int32_t) * seq, cudaMemcpyDeviceToHost, s));
-    if (logits_out)
-        SFG_CUDA(cudaMemcpyAsync(logits_out, ws.logits, sizeof(float) * seq * c.vocab_size, cudaMemcpyDeviceToHost, s));
-    SFG_CUDA(cudaEventRecord(ev_[3], s));
-    first_step_done_ = true;
-    SFG_CUDA(cudaEventSynchronize(ev_[3]));
     SFG_CUDA(cudaGetLastError());
+    prefix_->set_len(kv);
+    suffix_->set_len(kv);
+    first_step_done_ = true;
     if (vout) std::memcpy(vout, h_vout_, sizeof(VerifyOut));
+    if (argmax_out) std::memcpy(argmax_out, h_argmax_, sizeof(int32_t) * seq);
+    if (logits_out) std::memcpy(logits_out, h_logits_, sizeof(float) * seq * c.vocab_size);
     float a = 0, b = 0;
     cudaEventElapsedTime(&a, ev_[0], ev_[3]);
-    cudaEventElapsedTime(&b, ev_[1], ev_[2]);
+    if (linked_ && !prof_.graph) cudaEventElapsedTime(&b, ev_[1], ev_[2]);
     prof_.step_ms = a;
     if (linked_) prof_.server_ms = b;
     prof_.local_ms = a - b;

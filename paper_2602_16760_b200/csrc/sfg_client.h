@@ -2,7 +2,8 @@
 // decode loops of decoding.cpp with a host NGramPool.  The exchange is either
 // frame-level through a FrameHandler-like C callback (drop-in against any
 // splitf server) or device-linked to an in-process sfg::Server on the same
-// device (no host copies; wire quantisation applied on device).
+// device (no host copies; wire quantisation applied on device).  Linked
+// steps are captured once per batch size as a CUDA graph and replayed.
 #pragma once
 #include <chrono>
 #include <optional>
@@ -61,6 +62,7 @@ struct ClientCfg {
 struct StepProfile {
     double step_ms = 0, server_ms = 0, local_ms = 0;
     int launches = 0, batch = 0;
+    bool graph = false;
 };
 
 class Client {
@@ -70,8 +72,8 @@ public:
     ~Client();
 
     int prefill(const int32_t* prompt, int n, float* logits_row);
-    // One exchange (client.cpp:169-228).  Results stay on device unless
-    // requested: logits rows -> logits_out (host), verify tail -> vout.
+    // One exchange (client.cpp:169-228).  Outputs: logits rows (host), row
+    // argmaxes (host), verify tail (VerifyOut) when vin is given.
     void decode_step(int seq, const int32_t* tokens, const int32_t* positions, const MaskRuns* runs,
                      const int32_t* keep, int n_keep, std::optional<int> crop, float* logits_out,
                      int32_t* argmax_out, const VerifyIn* vin, VerifyOut* vout);
@@ -83,9 +85,26 @@ public:
     Engine& engine() { return eng_; }
 
 private:
-    void exchange(bool prompt, int seq, const int32_t* pos, const MaskRuns* runs, int mask_kv,
-                  const int32_t* keep, int n_keep, bool send_keep, std::optional<int> crop);
+    struct Graph {
+        int rows;
+        bool logits, verify;
+        Bank* server_bank;
+        uint64_t generation;
+        cudaGraphExec_t exec = nullptr;
+        std::vector<int> prof_slots;
+        int launches = 0;
+        int seen = 0;
+    };
+    // device step pieces (graph-capturable: no host syncs, fixed sizes)
+    int dev_pre(int rows, Bank* server_bank, bool verify, cudaStream_t s);
+    int dev_server(int rows, Bank* server_bank, cudaStream_t s);
+    int dev_post(int rows, bool want_logits, bool verify, cudaStream_t s);
+    void exchange_frames(bool prompt, int seq, const int32_t* pos, const MaskRuns* runs, int mask_kv,
+                         const int32_t* keep, int n_keep, bool send_keep, std::optional<int> crop);
     void sleep_one_way() const;
+    void stage_inputs(int seq, const int32_t* ids, const int32_t* pos, const MaskRuns& mr);
+    void ensure_out(int rows);
+    Graph* find_graph(int rows, bool logits, bool verify, Bank* server_bank);
 
     Engine& eng_;
     ClientCfg cfg_;
@@ -102,6 +121,10 @@ private:
     VerifyOut* d_vout_ = nullptr;
     VerifyIn* h_vin_ = nullptr;
     VerifyOut* h_vout_ = nullptr;
+    int32_t* h_argmax_ = nullptr;   // pinned [out_rows_]
+    float* h_logits_ = nullptr;     // pinned [out_rows_ x vocab]
+    int out_rows_ = 0;
+    std::vector<Graph> graphs_;
     std::vector<uint8_t> req_, payload_;
 };
 

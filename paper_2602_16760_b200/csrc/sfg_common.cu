@@ -94,6 +94,18 @@ __global__ void roundtrip_kernel(float* __restrict__ x, int f32, int n, unsigned
     if (c && clamped) atomicAdd(clamped, (unsigned long long)c);
 }
 
+// Simulated one-way link delay on the device timeline (SimChannel's sleep,
+// transport.cpp:235-243): one thread spins on %globaltimer, so the delay
+// sits between the producing and consuming kernels of a captured graph.
+__global__ void link_delay_kernel(unsigned long long ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        __nanosleep(2000);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+}
+
 // embed_at (tinyformer.cpp:348-373): row gather, bf16/f32 -> f32 exact.
 __global__ void embed_kernel(const void* __restrict__ table, int wt, const int32_t* __restrict__ ids,
                              int H, float* __restrict__ out) {
@@ -114,6 +126,27 @@ __global__ void kv_compact_kernel(float* __restrict__ kc, float* __restrict__ vc
                                   int n_keep) {
     extern __shared__ float buf[];  // [n_keep][hd]
     const int slab = blockIdx.x;     // (layer * n_kv + head) * 2 + {0:K,1:V}
+    float* base = ((slab & 1) ? vc : kc) + (size_t)(slab >> 1) * max_len * hd;
+    for (int t = threadIdx.x; t < n_keep * hd; t += blockDim.x) {
+        const int i = t / hd, dd = t - i * hd;
+        buf[t] = base[(size_t)(committed + keep[i]) * hd + dd];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_keep * hd; t += blockDim.x) {
+        const int i = t / hd, dd = t - i * hd;
+        base[(size_t)(committed + i) * hd + dd] = buf[t];
+    }
+}
+
+// Same compaction, parameters from the step meta block (meta[1] committed,
+// meta[2] n_keep, meta[3..] keep) so a captured graph replays it every step.
+__global__ void kv_compact_meta_kernel(float* __restrict__ kc, float* __restrict__ vc, int max_len, int hd,
+                                       const int32_t* __restrict__ meta) {
+    extern __shared__ float buf[];
+    const int committed = meta[1], n_keep = meta[2];
+    if (n_keep <= 0) return;
+    const int32_t* keep = meta + 3;
+    const int slab = blockIdx.x;
     float* base = ((slab & 1) ? vc : kc) + (size_t)(slab >> 1) * max_len * hd;
     for (int t = threadIdx.x; t < n_keep * hd; t += blockDim.x) {
         const int i = t / hd, dd = t - i * hd;
@@ -192,6 +225,12 @@ int launch_wire_roundtrip(float* x, int f32, int n, unsigned long long* clamped,
     return 1;
 }
 
+int launch_link_delay(double ms, cudaStream_t s) {
+    if (ms <= 0.0) return 0;
+    link_delay_kernel<<<1, 1, 0, s>>>(static_cast<unsigned long long>(ms * 1e6));
+    return 1;
+}
+
 int launch_embed(const void* table, int wt, const int32_t* ids, int rows, int H, float* out,
                  cudaStream_t s) {
     embed_kernel<<<rows, 256, 0, s>>>(table, wt, ids, H, out);
@@ -203,6 +242,19 @@ int launch_kv_compact(float* kcache, float* vcache, int layers, int n_kv, int ma
     if (n_keep <= 0 || layers <= 0) return 0;
     kv_compact_kernel<<<layers * n_kv * 2, 256, sizeof(float) * n_keep * hd, s>>>(
         kcache, vcache, n_kv, max_len, hd, committed, keep, n_keep);
+    return 1;
+}
+
+int launch_kv_compact_meta(float* kcache, float* vcache, int layers, int n_kv, int max_len, int hd,
+                           const int32_t* meta, int max_keep, cudaStream_t s) {
+    if (layers <= 0) return 0;
+    const size_t smem = sizeof(float) * (size_t)max_keep * hd;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaFuncSetAttribute(kv_compact_meta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = smem;
+    }
+    kv_compact_meta_kernel<<<layers * n_kv * 2, 256, smem, s>>>(kcache, vcache, max_len, hd, meta);
     return 1;
 }
 

@@ -31,6 +31,11 @@ void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
                                     " (" + file + ":" + std::to_string(line) + ")");
 }
 
+bool& graphs_enabled() {
+    static bool on = true;
+    return on;
+}
+
 DeviceGuard::DeviceGuard(int dev) {
     cudaGetDevice(&prev);
     if (prev != dev) SFG_CUDA(cudaSetDevice(dev));
@@ -110,9 +115,11 @@ MaskRuns runs_from_dense(const float* mask, int rows, int kv) {
 void Workspace::release() {
     for (void* p : {(void*)h, (void*)xn, (void*)q, (void*)att, (void*)act, (void*)logits, (void*)pos,
                     (void*)ids, (void*)argmax, (void*)keep, (void*)row_off, (void*)runs, (void*)status,
-                    (void*)clamped, wire, fast})
+                    (void*)clamped, wire, fast, (void*)meta})
         if (p) cudaFree(p);
     if (pinned) cudaFreeHost(pinned);
+    if (meta_pin) cudaFreeHost(meta_pin);
+    if (stage_pin) cudaFreeHost(stage_pin);
     *this = Workspace{};
 }
 
@@ -171,7 +178,25 @@ void Engine::ensure_ws(Workspace& ws, int rows, int runs, int logit_rows) {
         grow((void**)&ws.logits, sizeof(float) * r * c.vocab_size);
         ws.cap_logit_rows = r;
     }
+    if (!ws.meta) {
+        grow((void**)&ws.meta, sizeof(int32_t) * (4 + kMetaKeep));
+        SFG_CUDA(cudaMallocHost(&ws.meta_pin, sizeof(int32_t) * (4 + kMetaKeep)));
+        std::memset(ws.meta_pin, 0, sizeof(int32_t) * (4 + kMetaKeep));
+    }
+    const StageLayout L = stage_layout(ws.cap_rows, ws.cap_runs);
+    if (L.total > ws.stage_bytes) {
+        if (ws.stage_pin) cudaFreeHost(ws.stage_pin);
+        SFG_CUDA(cudaMallocHost(&ws.stage_pin, L.total));
+        ws.stage_bytes = L.total;
+    }
+    ++ws.generation;
     SFG_CUDA(cudaDeviceSynchronize());
+}
+
+void Engine::set_prior(Workspace& ws, int prior, cudaStream_t s) {
+    // eager paths sync at the end of every call, so the pinned slot is free
+    ws.meta_pin[0] = prior;
+    SFG_CUDA(cudaMemcpyAsync(ws.meta, ws.meta_pin, sizeof(int32_t), cudaMemcpyHostToDevice, s));
 }
 
 // ── banks ─────────────────────────────────────────────────────────────────
@@ -232,6 +257,19 @@ void Bank::resolve(const int32_t* keep, int n, cudaStream_t s) {
                           n, st);
         SFG_CUDA(cudaGetLastError());
         if (own) SFG_CUDA(cudaStreamSynchronize(st));
+    }
+    committed_ += n;
+    len_ = committed_;
+}
+
+void Bank::resolve_meta(const int32_t* keep, int n) {
+    const int tail = provisional();
+    int prev = -1;
+    for (int i = 0; i < n; ++i) {
+        if (keep[i] <= prev || keep[i] >= tail)
+            throw Error(Kind::protocol,
+                        "keep indices must be strictly increasing and within the provisional tail");
+        prev = keep[i];
     }
     committed_ += n;
     len_ = committed_;
@@ -508,7 +546,7 @@ int Engine::forward_device(Bank& b, int lb, int le, int rows, Workspace& ws, cud
         {
             ProfScope p(K_QKV, s, wb * d.H * qkv + 4.0 * R * (d.H + qkv), 2.0 * R * d.H * qkv);
             n += launch_qkv_exact(ws.xn, rows, d, wt(), L.wq, L.wk, L.wv, ws.pos, rope_cos_, rope_sin_, ws.q, kc,
-                                  vc, prior, s);
+                                  vc, ws.meta, s);
         }
         {
             const double kvb = 2.0 * 4.0 * d.kvd * (prior + rows);
@@ -595,6 +633,7 @@ void Engine::forward_host(Bank& b, int lb, int le, int seq, const float* h, cons
     SFG_CUDA(cudaMemcpyAsync(ws.row_off, mr.row_off.data(), sizeof(int32_t) * (seq + 1), cudaMemcpyHostToDevice, s));
     SFG_CUDA(cudaMemcpyAsync(ws.runs, mr.runs.data(), sizeof(MaskRun) * mr.runs.size(), cudaMemcpyHostToDevice, s));
     SFG_CUDA(cudaMemsetAsync(ws.status, 0, sizeof(uint32_t), s));
+    set_prior(ws, prior, s);
     forward_device(b, lb, le, seq, ws, s);
     SFG_CUDA(cudaGetLastError());
     uint32_t st = 0;

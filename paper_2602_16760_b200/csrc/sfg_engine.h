@@ -85,8 +85,38 @@ struct Workspace {
     size_t fast_bytes = 0;
     void* pinned = nullptr;        // host staging
     size_t pinned_bytes = 0;
+    // Per-step scalars read by kernels from device memory, so one captured
+    // CUDA graph serves every step of a given batch size:
+    //   meta[0] = cache length before the batch (QKV epilogue KV slot base)
+    //   meta[1] = committed length before resolve, meta[2] = #kept rows,
+    //   meta[3 .. 3+kMetaKeep) = keep list (in-place compaction).
+    int32_t* meta = nullptr;       // device
+    int32_t* meta_pin = nullptr;   // pinned mirror
+    void* stage_pin = nullptr;     // pinned [ids | pos | row_off | runs] at cap-derived offsets
+    size_t stage_bytes = 0;
+    uint64_t generation = 0;       // bumped whenever a buffer is reallocated
     void release();
 };
+
+constexpr int kMetaKeep = 256;
+struct StageLayout {
+    size_t ids, pos, roff, runs, total;
+};
+inline StageLayout stage_layout(int cap_rows, int cap_runs) {
+    StageLayout L{};
+    size_t o = 0;
+    L.ids = o;
+    o += 4 * static_cast<size_t>(cap_rows);
+    L.pos = o;
+    o += 4 * static_cast<size_t>(cap_rows);
+    L.roff = o;
+    o += 4 * static_cast<size_t>(cap_rows + 1);
+    o = (o + 15) & ~size_t(15);
+    L.runs = o;
+    o += sizeof(MaskRun) * static_cast<size_t>(cap_runs);
+    L.total = o;
+    return L;
+}
 
 class Engine;
 
@@ -108,6 +138,9 @@ public:
     void set_len(int l) { len_ = l; }
     void reset() { len_ = 0; committed_ = 0; }
     void resolve(const int32_t* keep, int n, cudaStream_t s = nullptr);  // tinyformer.cpp:282-308
+    // resolve() bookkeeping only (validation + committed/len); the caller
+    // enqueues the meta-driven compaction itself (graph-captured steps).
+    void resolve_meta(const int32_t* keep, int n);
     void crop(int pos);                        // tinyformer.cpp:310-316
     float* kslab(int layer) const;
     float* vslab(int layer) const;
@@ -155,6 +188,8 @@ public:
 
     // Ensure ws holds `rows` rows / `runs` runs / `logit_rows` logit rows.
     void ensure_ws(Workspace& ws, int rows, int runs, int logit_rows);
+    // Eager paths: ws.meta[0] = prior (cache length) on stream s.
+    void set_prior(Workspace& ws, int prior, cudaStream_t s);
 
     // Layer executor over device-resident rows (ws.h holds the input and
     // receives the output).  ws.pos / ws.row_off / ws.runs must be loaded.
@@ -204,6 +239,10 @@ private:
     Workspace ws_;
     std::mutex mu_;
 };
+
+// Process-wide switch: capture/replay the device part of decode steps as
+// CUDA graphs (sfg_set_graphs).
+bool& graphs_enabled();
 
 // Scoped device selection.
 struct DeviceGuard {

@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kThreads) qkv_exact_kernel(
     const float* __restrict__ xn, int rows, Dims d, const void* wq, const void* wk, const void* wv,
     const int32_t* __restrict__ pos, const float* __restrict__ rope_cos,
     const float* __restrict__ rope_sin, float* __restrict__ q, float* __restrict__ kc,
-    float* __restrict__ vc, int prior) {
+    float* __restrict__ vc, const int32_t* __restrict__ prior_ptr) {
     __shared__ __align__(16) float xs[kKC * RB];
     const int pairs_q = d.qd / 2, pairs_kv = d.kvd / 2;
     const int pair = blockIdx.x * kThreads + threadIdx.x;
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kThreads) qkv_exact_kernel(
             q[(size_t)row * d.qd + col + 1] = b;
         } else {
             const int kvh = col / d.hd, dd = col % d.hd;
-            float* dst = (seg == 1 ? kc : vc) + ((size_t)kvh * d.max_len + prior + row) * d.hd + dd;
+            float* dst = (seg == 1 ? kc : vc) + ((size_t)kvh * d.max_len + *prior_ptr + row) * d.hd + dd;
             dst[0] = a;
             dst[1] = b;
         }
@@ -356,7 +356,7 @@ int launch_rmsnorm_exact(const float* h, const float* g, float* y, int rows, int
 
 int launch_qkv_exact(const float* xn, int rows, const Dims& d, int wt, const void* wq,
                      const void* wk, const void* wv, const int32_t* pos, const float* rope_cos,
-                     const float* rope_sin, float* q, float* kcache, float* vcache, int prior,
+                     const float* rope_sin, float* q, float* kcache, float* vcache, const int32_t* prior,
                      cudaStream_t s) {
     const int pairs = (d.qd + 2 * d.kvd) / 2;
     dim3 grid((pairs + kThreads - 1) / kThreads, (rows + kRB - 1) / kRB);

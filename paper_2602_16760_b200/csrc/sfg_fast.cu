@@ -62,7 +62,8 @@ struct GemmArgs {
     float* out;
     int ld;
     // EPI_QKV
-    int qd, kvd, hd, max_len, prior;
+    int qd, kvd, hd, max_len;
+    const int32_t* prior;  // device: cache length before this batch
     const int32_t* pos;
     const float* rope_cos;
     const float* rope_sin;
@@ -195,7 +196,7 @@ __device__ __forceinline__ void final_epilogue(const GemmArgs& a, int tile, int 
             } else {
                 const int kvh = fl / a.hd;
                 float* dst = (seg == 1 ? a.kc : a.vc) +
-                             (static_cast<size_t>(kvh) * a.max_len + a.prior + row) * a.hd + d;
+                             (static_cast<size_t>(kvh) * a.max_len + *a.prior + row) * a.hd + d;
                 *dst = v;
             }
         }
@@ -691,7 +692,7 @@ int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, i
         a.kvd = d.kvd;
         a.hd = d.hd;
         a.max_len = d.max_len;
-        a.prior = prior;
+        a.prior = ws.meta;
         a.pos = ws.pos;
         a.rope_cos = e.rope_cos();
         a.rope_sin = e.rope_sin();
@@ -706,7 +707,7 @@ int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, i
     {
         const double kvb = 2.0 * 4.0 * d.kvd * (prior + rows);
         ProfScope ps(K_ATTN, s, kvb + 8.0 * R * d.qd, 4.0 * R * d.qd * (prior + rows));
-        n += launch_attention_exact(ws.q, kc, vc, ws.row_off, ws.runs, rows, prior + rows, d, ws.att, ws.status, s);
+        n += launch_attention_fast(ws.q, kc, vc, ws.row_off, ws.runs, rows, d, ws.att, ws.status, s);
     }
     for (int p0 = 0; p0 < rows; p0 += kRows) {
         const int pr = std::min(kRows, rows - p0);

@@ -49,7 +49,7 @@ int launch_rmsnorm_exact(const float* h, const float* g, float* y, int rows, int
                          cudaStream_t s);
 int launch_qkv_exact(const float* xn, int rows, const Dims& d, int wt, const void* wq,
                      const void* wk, const void* wv, const int32_t* pos, const float* rope_cos,
-                     const float* rope_sin, float* q, float* kcache, float* vcache, int prior,
+                     const float* rope_sin, float* q, float* kcache, float* vcache, const int32_t* prior,
                      cudaStream_t s);
 int launch_attention_exact(const float* q, const float* kcache, const float* vcache,
                            const int32_t* row_off, const MaskRun* runs, int rows, int kv_len,
@@ -61,6 +61,11 @@ int launch_gateup_exact(const float* xn, int rows, int H, int F, int wt, const v
 int launch_matvec_store_exact(const float* x, int rows, int K, int wt, const void* w, int N,
                               float* out, cudaStream_t s);
 
+// ── FAST-mode attention (sfg_attn.cu) ─────────────────────────────────────
+int launch_attention_fast(const float* q, const float* kcache, const float* vcache,
+                          const int32_t* row_off, const MaskRun* runs, int rows, const Dims& d,
+                          float* att, uint32_t* status, cudaStream_t s);
+
 // ── shared kernels (sfg_common.cu) ────────────────────────────────────────
 int launch_embed(const void* table, int wt, const int32_t* ids, int rows, int H, float* out,
                  cudaStream_t s);
@@ -70,7 +75,10 @@ int launch_pack_rows(const float* in, int f32, int n, void* wire, unsigned long 
 int launch_wire_roundtrip(float* x, int f32, int n, unsigned long long* clamped, cudaStream_t s);
 int launch_kv_compact(float* kcache, float* vcache, int layers, int n_kv, int max_len, int hd,
                       int committed, const int32_t* keep, int n_keep, cudaStream_t s);
+int launch_kv_compact_meta(float* kcache, float* vcache, int layers, int n_kv, int max_len, int hd,
+                           const int32_t* meta, int max_keep, cudaStream_t s);
 int launch_argmax(const float* logits, int rows, int V, int32_t* out, cudaStream_t s);
+int launch_link_delay(double ms, cudaStream_t s);
 int launch_convert_weights(const float* src, void* dst, int wt, size_t n, cudaStream_t s);
 
 }  // namespace sfg

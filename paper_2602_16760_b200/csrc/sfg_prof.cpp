@@ -13,7 +13,9 @@ void KernelProfiler::enable(bool v) {
 }
 
 int KernelProfiler::begin(int cls, cudaStream_t s) {
-    if (!on_) return -1;
+    // while capturing, always record: the graph's event nodes must exist for
+    // later replays that run with the profiler on
+    if (!on_ && !capture_) return -1;
     std::lock_guard<std::mutex> lk(mu_);
     int idx = -1;
     for (size_t i = 0; i < slots_.size(); ++i)
@@ -41,7 +43,38 @@ void KernelProfiler::end(int slot, cudaStream_t s, double bytes, double flops) {
     sl.bytes = bytes;
     sl.flops = flops;
     cudaEventRecord(sl.b, s);
-    pending_.push_back(slot);
+    if (capture_)
+        capture_->push_back(slot);
+    else
+        pending_.push_back(slot);
+}
+
+void KernelProfiler::begin_capture(std::vector<int>* list) {
+    std::lock_guard<std::mutex> lk(mu_);
+    capture_ = list;
+}
+
+void KernelProfiler::end_capture() {
+    std::lock_guard<std::mutex> lk(mu_);
+    capture_ = nullptr;
+}
+
+void KernelProfiler::collect_graph(const std::vector<int>& list) {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (int i : list) {
+        Slot& sl = slots_[i];
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, sl.a, sl.b) != cudaSuccess) continue;
+        count_[sl.cls] += 1;
+        ms_[sl.cls] += ms;
+        bytes_[sl.cls] += sl.bytes;
+        flops_[sl.cls] += sl.flops;
+    }
+}
+
+void KernelProfiler::release_graph(const std::vector<int>& list) {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (int i : list) slots_[i].used = false;
 }
 
 void KernelProfiler::collect() {

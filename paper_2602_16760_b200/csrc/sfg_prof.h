@@ -27,6 +27,14 @@ public:
     void reset();
     void stats(int cls, int64_t* count, double* ms, double* bytes, double* flops);
 
+    // Graph capture: slots recorded while capturing belong to the graph (its
+    // event-record nodes fire on every replay); collect_graph() accumulates
+    // them after each replay, release_graph() frees them with the graph.
+    void begin_capture(std::vector<int>* list);
+    void end_capture();
+    void collect_graph(const std::vector<int>& list);
+    void release_graph(const std::vector<int>& list);
+
 private:
     struct Slot {
         int cls;
@@ -35,6 +43,7 @@ private:
         bool used;
     };
     bool on_ = false;
+    std::vector<int>* capture_ = nullptr;
     std::mutex mu_;
     std::vector<Slot> slots_;
     std::vector<int> pending_;

@@ -291,6 +291,7 @@ void Server::handle_frame(const wire::FrameView& f, std::vector<uint8_t>& resp) 
     SFG_CUDA(cudaMemcpyAsync(ws.wire, f.tensor, f.tensor_len, cudaMemcpyHostToDevice, s));
     launch_unpack_rows(ws.wire, in_f32, n, ws.h, s);
     SFG_CUDA(cudaMemsetAsync(ws.status, 0, sizeof(uint32_t), s));
+    eng_.set_prior(ws, bank.len(), s);
     eng_.forward_device(bank, cfg_.layer_begin, cfg_.layer_end, seq, ws, s);
     launch_pack_rows(ws.h, out_dt == wire::Dtype::f32, n, ws.wire, nullptr, s);
     SFG_CUDA(cudaGetLastError());
@@ -316,31 +317,39 @@ void Server::handle_frame(const wire::FrameView& f, std::vector<uint8_t>& resp) 
     wire::encode(h, payload.data(), out_bytes, nullptr, 0, resp);
 }
 
-int Server::linked_step(const LinkedStep& st) {
+// handle_prompt / handle_step (server.cpp:203-265) for a device-linked
+// client: identical checks and state transitions, no device work.
+Server::Lease Server::linked_begin(const LinkedStep& st) {
     const ModelCfg& c = eng_.cfg();
-    std::shared_ptr<Session> sess;
+    Lease l;
+    l.is_prompt = st.is_prompt;
     if (st.is_prompt) {
         if (st.session_id->empty()) throw Error(Kind::protocol, "prompt frame requires a session_id");
         for (int i = 0; i < st.seq; ++i)
             if (st.pos[i] < 0 || st.pos[i] >= c.max_seq_len) throw Error(Kind::capacity, "position exceeds max_seq_len");
         if (st.seq > c.max_seq_len) throw Error(Kind::capacity, "prompt exceeds max_seq_len");
-        sess = create_or_reset_session(*st.session_id);
+        l.sess = create_or_reset_session(*st.session_id);
     } else {
-        sess = find_session(*st.session_id);
-        if (!sess) throw Error(Kind::session, "unknown or expired session: " + *st.session_id);
+        l.sess = find_session(*st.session_id);
+        if (!l.sess) throw Error(Kind::session, "unknown or expired session: " + *st.session_id);
     }
-    std::lock_guard<std::mutex> lk(sess->mutex);
-    Bank& bank = *sess->bank;
+    l.lock = std::unique_lock<std::mutex>(l.sess->mutex);
+    Bank& bank = *l.sess->bank;
+    l.bank = &bank;
+    l.committed_before = bank.committed_len();
     if (st.is_prompt) {
         bank.reset();
+        l.committed_before = 0;
     } else {
         for (int i = 0; i < st.seq; ++i)
             if (st.pos[i] < 0 || st.pos[i] >= c.max_seq_len) throw Error(Kind::capacity, "position exceeds max_seq_len");
         std::vector<int32_t> keep;
         if (st.keep)
             for (int64_t k : *st.keep) keep.push_back(static_cast<int32_t>(k));
-        if (!keep.empty() || bank.provisional() > 0)
-            bank.resolve(keep.data(), static_cast<int>(keep.size()), st.stream);
+        if (!keep.empty() || bank.provisional() > 0) {
+            bank.resolve_meta(keep.data(), static_cast<int>(keep.size()));
+            l.n_keep = static_cast<int>(keep.size());
+        }
         if (st.crop) {
             if (*st.crop < 0 || *st.crop > bank.len()) throw Error(Kind::protocol, "crop position exceeds session length");
             bank.crop(static_cast<int>(*st.crop));
@@ -355,20 +364,15 @@ int Server::linked_step(const LinkedStep& st) {
         throw Error(Kind::protocol, "mask shape does not match cache length plus batch");
     }
     forward_checks(bank, st.seq, *mr, c.max_seq_len);
-    DeviceGuard g(eng_.device());
-    Workspace& ws = bank.ws();
-    std::vector<int32_t> pos(st.pos, st.pos + st.seq);
-    upload_meta(eng_, ws, pos, *mr, st.stream);
-    const size_t bytes = sizeof(float) * st.seq * c.hidden_dim;
-    SFG_CUDA(cudaMemcpyAsync(ws.h, st.rows, bytes, cudaMemcpyDeviceToDevice, st.stream));
-    SFG_CUDA(cudaMemsetAsync(ws.status, 0, sizeof(uint32_t), st.stream));
-    int n = eng_.forward_device(bank, cfg_.layer_begin, cfg_.layer_end, st.seq, ws, st.stream);
-    SFG_CUDA(cudaMemcpyAsync(st.rows, ws.h, bytes, cudaMemcpyDeviceToDevice, st.stream));
-    SFG_CUDA(cudaGetLastError());
-    bank.set_len(bank.len() + st.seq);
-    if (st.is_prompt) bank.mark_committed(bank.len());
-    sess->last_active = now_s_();
-    return n;
+    l.prior = bank.len();
+    return l;
+}
+
+void Server::linked_end(Lease& l, int seq) {
+    l.bank->set_len(l.bank->len() + seq);
+    if (l.is_prompt) l.bank->mark_committed(l.bank->len());
+    l.sess->last_active = now_s_();
+    l.lock.unlock();
 }
 
 }  // namespace sfg

@@ -43,10 +43,13 @@ public:
         std::mutex mutex;
     };
 
-    // Device-linked step for an in-process client on the same device: rows
-    // are device fp32 already carrying the wire quantisation; they are
-    // transformed in place on stream s.  Same state machine and checks as
-    // handle_step; returns kernels launched.
+    // Device-linked steps for an in-process client on the same device.
+    // linked_begin runs the handle_prompt / handle_step state machine and all
+    // host-side checks (session, positions, keep, crop, mask shape, capacity)
+    // and applies the bookkeeping; it does NOT touch the device.  The client
+    // then runs the server's layers over its own device rows against
+    // lease.bank (KV compaction driven by the client's step meta), and calls
+    // linked_end once the step's work is enqueued.
     struct LinkedStep {
         const std::string* session_id;
         bool is_prompt;
@@ -56,10 +59,18 @@ public:
         std::optional<int64_t> crop;
         const MaskRuns* runs;             // nullptr = causal
         int mask_q, mask_kv;              // declared mask shape (when runs != nullptr)
-        float* rows;                      // device [seq x H], in/out
-        cudaStream_t stream;
     };
-    int linked_step(const LinkedStep& st);
+    struct Lease {
+        std::shared_ptr<Session> sess;
+        std::unique_lock<std::mutex> lock;
+        Bank* bank = nullptr;
+        int prior = 0;                    // cache length the forward appends at
+        int committed_before = 0;         // committed length before resolve
+        int n_keep = 0;                   // rows relocated by resolve (0: none)
+        bool is_prompt = false;
+    };
+    Lease linked_begin(const LinkedStep& st);
+    void linked_end(Lease& l, int seq);
 
 private:
     std::shared_ptr<Session> find_session(const std::string& id);
