@@ -40,7 +40,7 @@ H_7B = dict(vocab_size=32768, n_layers=32, hidden_dim=4096, n_heads=32, n_kv_hea
 SPLIT = 2
 W, NG, G = 5, 3, 5
 PROMPT_LEN = 24
-KCLASS = ["qkv", "attention", "o_proj", "gate_up", "down", "rmsnorm", "lm_head", "other"]
+KCLASS = ["qkv", "attention", "o_proj", "gate_up", "down", "rmsnorm", "lm_head", "other", "layer_stack"]
 
 
 def peaks():

@@ -251,6 +251,14 @@ void sfg_set_graphs(int32_t enabled);
  * 5 RMSNorm, 6 LM head, 7 other.  bytes/flops are ALGORITHMIC per launch,
  * summed.                                                                 */
 void sfg_profiler_enable(int32_t on);
+/* debugging hooks: FAST megakernel on/off; copy a bank workspace buffer
+ * (0 hidden rows, 1 q, 2 attention output, 3 SwiGLU activation) to host.  */
+void sfg_debug_set_mega(int32_t on);
+/* megakernel phase timeline: per CTA x barrier id, globaltimer stamps of
+ * {input-barrier passed, activation image done, phase done, -}           */
+void sfg_debug_mega_trace(int32_t on);
+int32_t sfg_debug_mega_trace_read(sfg_bank* b, uint64_t* out, size_t n);
+int32_t sfg_debug_bank_buffer(sfg_bank* b, int32_t which, float* out, int32_t n);
 void sfg_profiler_reset(void);
 int32_t sfg_profiler_stats(int32_t cls, int64_t* count, double* ms, double* bytes, double* flops);
 

@@ -143,6 +143,10 @@ def lib() -> C.CDLL:
         "sfg_client_last_profile": (i32, [vp, C.POINTER(StepProfile)]),
         "sfg_set_graphs": (None, [i32]),
         "sfg_profiler_enable": (None, [i32]),
+        "sfg_debug_set_mega": (None, [i32]),
+        "sfg_debug_mega_trace": (None, [i32]),
+        "sfg_debug_mega_trace_read": (i32, [vp, C.POINTER(C.c_uint64), C.c_size_t]),
+        "sfg_debug_bank_buffer": (i32, [vp, i32, f32p, i32]),
         "sfg_profiler_reset": (None, []),
         "sfg_profiler_stats": (i32, [i32, C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double),
                                      C.POINTER(C.c_double)]),

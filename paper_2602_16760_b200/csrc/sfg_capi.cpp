@@ -300,6 +300,24 @@ int32_t sfg_client_last_profile(sfg_client* c, sfg_step_profile* out) {
 
 void sfg_set_graphs(int32_t enabled) { graphs_enabled() = enabled != 0; }
 
+void sfg_debug_set_mega(int32_t on) { mega_mode() = on ? 1 : 0; }
+void sfg_debug_mega_trace(int32_t on) { mega_trace_enabled() = on != 0; }
+int32_t sfg_debug_mega_trace_read(sfg_bank* b, uint64_t* out, size_t n) {
+    return mega_trace_read(*b->b, reinterpret_cast<unsigned long long*>(out), n);
+}
+
+int32_t sfg_debug_bank_buffer(sfg_bank* b, int32_t which, float* out, int32_t n) {
+    SFG_GUARD({
+        Workspace& ws = b->b->ws();
+        const int tilesH = (b->eng->e->cfg().hidden_dim + 127) / 128;
+        const float* src = which == 0 ? ws.h : which == 1 ? ws.q : which == 2 ? ws.att : which == 3 ? ws.act
+                                                                                    : mega_ss(*b->b, which - 4, tilesH);
+        if (!src) throw Error(Kind::input, "buffer not allocated");
+        SFG_CUDA(cudaDeviceSynchronize());
+        SFG_CUDA(cudaMemcpy(out, src, sizeof(float) * n, cudaMemcpyDeviceToHost));
+    })
+}
+
 void sfg_profiler_enable(int32_t on) { KernelProfiler::get().enable(on != 0); }
 void sfg_profiler_reset(void) { KernelProfiler::get().reset(); }
 int32_t sfg_profiler_stats(int32_t cls, int64_t* count, double* ms, double* bytes, double* flops) {

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstring>
 #include <random>
+#include <cstdlib>
 #include <thread>
 
 #include "sfg_prof.h"
@@ -503,7 +504,8 @@ void Client::decode_step(int seq, const int32_t* tokens, const int32_t* position
         }
         SFG_CUDA(cudaEventRecord(ev_[0], s));
         Graph* gr = nullptr;
-        if (graphs_enabled()) {
+        static const bool debug_eager = std::getenv("SFG_DEBUG") != nullptr;
+        if (graphs_enabled() && !debug_eager) {
             gr = find_graph(seq, want_logits, vin != nullptr, lease.bank);
             ++gr->seen;
         }
@@ -536,9 +538,22 @@ void Client::decode_step(int seq, const int32_t* tokens, const int32_t* position
             prof_.launches = k;
             prof_.graph = true;
         } else {
+            static const bool dbg = std::getenv("SFG_DEBUG") != nullptr;
+            auto check = [&](const char* where) {
+                if (!dbg) return;
+                const cudaError_t e1 = cudaStreamSynchronize(s);
+                const cudaError_t e2 = cudaGetLastError();
+                if (e1 != cudaSuccess || e2 != cudaSuccess)
+                    throw Error(Kind::internal, std::string("debug: CUDA error after ") + where + ": " +
+                                                    cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+            };
+            check("entry");
             prof_.launches += dev_pre(seq, lease.bank, vin != nullptr, s);
+            check("dev_pre");
             prof_.launches += dev_server(seq, lease.bank, s);
+            check("dev_server");
             prof_.launches += dev_post(seq, want_logits, vin != nullptr, s);
+            check("dev_post");
         }
         SFG_CUDA(cudaEventRecord(ev_[3], s));
         linked_->linked_end(lease, seq);

@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <random>
 
 namespace sfg {
@@ -524,10 +525,26 @@ void Engine::build_fast_layouts() {
 }
 
 // ── engine: execution ─────────────────────────────────────────────────────
+int& mega_mode() {
+    static int on = -1;
+    if (on < 0) {
+        const char* v = std::getenv("SFG_MEGA");
+        on = (v && v[0] == '0') ? 0 : 1;
+    }
+    return on;
+}
+static bool mega_env_enabled() { return mega_mode() == 1; }
+
 int Engine::forward_device(Bank& b, int lb, int le, int rows, Workspace& ws, cudaStream_t s) {
     const Dims d = dims();
     const int prior = b.len();
     int n = 0;
+    if (lb >= le) return 0;
+    if (fast() && mega_env_enabled() && le - lb <= 50 && mega_supported(*this, rows, ws.additive_mask)) {
+        for (int layer = lb; layer < le; ++layer)
+            if (!layers_[layer].hosted) throw Error(Kind::internal, "layer not hosted by this engine");
+        return mega_forward(*this, b, lb, le, rows, ws, s);
+    }
     for (int layer = lb; layer < le; ++layer) {
         const LayerWeights& L = layers_[layer];
         if (!L.hosted) throw Error(Kind::internal, "layer not hosted by this engine");
@@ -628,6 +645,8 @@ void Engine::forward_host(Bank& b, int lb, int le, int seq, const float* h, cons
     Workspace& ws = b.ws();
     cudaStream_t s = b.stream();
     ensure_ws(ws, seq, static_cast<int>(mr.runs.size()), 0);
+    ws.additive_mask = false;
+    for (const MaskRun& r : mr.runs) ws.additive_mask = ws.additive_mask || r.mval != 0.0f;
     SFG_CUDA(cudaMemcpyAsync(ws.h, h, sizeof(float) * seq * H, cudaMemcpyHostToDevice, s));
     SFG_CUDA(cudaMemcpyAsync(ws.pos, pos, sizeof(int32_t) * seq, cudaMemcpyHostToDevice, s));
     SFG_CUDA(cudaMemcpyAsync(ws.row_off, mr.row_off.data(), sizeof(int32_t) * (seq + 1), cudaMemcpyHostToDevice, s));

@@ -95,6 +95,7 @@ struct Workspace {
     void* stage_pin = nullptr;     // pinned [ids | pos | row_off | runs] at cap-derived offsets
     size_t stage_bytes = 0;
     uint64_t generation = 0;       // bumped whenever a buffer is reallocated
+    bool additive_mask = false;    // some visible column carries a non-zero mask value
     void release();
 };
 
@@ -148,6 +149,8 @@ public:
     cudaStream_t stream() const { return stream_; }
     Workspace& ws() { return ws_; }
     Engine& engine() { return eng_; }
+    // per-bank state of the FAST megakernel (layer table, grid barrier)
+    std::shared_ptr<void> mega;
 
 private:
     Engine& eng_;
@@ -243,6 +246,9 @@ private:
 // Process-wide switch: capture/replay the device part of decode steps as
 // CUDA graphs (sfg_set_graphs).
 bool& graphs_enabled();
+// 1: FAST forward uses the layer-stack megakernel when it applies (default;
+// env SFG_MEGA=0 or sfg_debug_set_mega(0) selects the per-GEMM kernels).
+int& mega_mode();
 
 // Scoped device selection.
 struct DeviceGuard {
@@ -259,5 +265,13 @@ int fast_head(Engine& e, const void* f_lm_head, const float* final_norm, int row
 size_t fast_workspace_bytes(const ModelCfg& c, int rows);
 void fast_build_layer(Engine& e, LayerWeights& L, cudaStream_t s);
 void* fast_build_head(Engine& e, const void* lm_head, cudaStream_t s);
+float* fast_partials(const ModelCfg& c, Workspace& ws);
+int* fast_counters(const ModelCfg& c, Workspace& ws);
+// FAST layer-stack megakernel (sfg_mega.cu)
+bool mega_supported(const Engine& e, int rows, bool additive_mask);
+int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cudaStream_t s);
+float* mega_ss(Bank& b, int which, int tilesH);
+bool& mega_trace_enabled();
+int mega_trace_read(Bank& b, unsigned long long* out, size_t n);
 
 }  // namespace sfg

@@ -618,6 +618,9 @@ FastWs carve(const ModelCfg& c, Workspace& ws, int rows) {
 }
 }  // namespace
 
+float* fast_partials(const ModelCfg& c, Workspace& ws) { return carve(c, ws, ws.cap_rows).partials; }
+int* fast_counters(const ModelCfg& c, Workspace& ws) { return carve(c, ws, ws.cap_rows).counters; }
+
 size_t fast_workspace_bytes(const ModelCfg& c, int rows) {
     return max_kb(c) * kBBytes + max_tiles(c) * kMaxPieces * kRows * kM * sizeof(float) + max_tiles(c) * sizeof(int) +
            2 * static_cast<size_t>(rows) * tiles_for(c.vocab_size) * sizeof(float) + 8 * 1024;
@@ -657,9 +660,14 @@ void* fast_build_head(Engine& e, const void* lm_head, cudaStream_t s) {
     return relayout(e, lm_head, nullptr, nullptr, c.vocab_size, 0, 0, 0, c.hidden_dim, tiles_for(c.vocab_size), s);
 }
 
+// Stream-K grid: every CTA gets >= ceil((KB-1)/(kMaxPieces-1)) k-blocks so
+// no tile is split into more than kMaxPieces pieces.
 static int grid_for(int tiles, int KB) {
     const long long U = static_cast<long long>(tiles) * KB;
-    return static_cast<int>(std::min<long long>(U, num_sms()));
+    const int min_units = (KB - 1 + kMaxPieces - 2) / (kMaxPieces - 1);
+    long long g = min_units > 0 ? U / min_units : U;
+    g = std::min<long long>(g, num_sms());
+    return static_cast<int>(std::max<long long>(g, 1));
 }
 
 // One layer of forward_layers (tinyformer.cpp:412-504) in FAST math.

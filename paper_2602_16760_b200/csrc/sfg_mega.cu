@@ -1,0 +1,944 @@
+// FAST-mode layer-stack megakernel (sm_100a): forward_layers over a whole
+// layer range in ONE cooperative launch.
+//
+// Why: a lookahead step streams 12 GB of weights through 28 x 4 dependent
+// skinny GEMMs.  With one kernel per GEMM every boundary costs a launch, a
+// TMEM/barrier prologue and a DRAM-latency ramp, and HBM idles meanwhile.
+// Here one CTA per SM (320 threads) runs the whole stack:
+//
+//   warp 0      weight producer: walks the CTA's stream-K share of every GEMM
+//               of every layer and keeps the 8-stage smem ring full with
+//               cp.async.bulk weight tiles — never waits on activations, so
+//               the next GEMM's weights arrive while the current one drains
+//               and while attention / grid barriers are in flight;
+//   warp 1      tcgen05.mma issuer (one thread), TMEM double accumulator;
+//   warps 2-5   TMEM epilogue: RoPE + KV append (QKV), residual add + per-tile
+//               sum-of-squares partials (O, down), SiLU*up (gate|up), stream-K
+//               fixup (last arriver sums the pieces in fixed k order); each
+//               output is also stored as the NEXT GEMM's input image (3-way
+//               bf16 split, times the RMSNorm gain, in the MMA's swizzled
+//               layout), and the 1/rms row scale is applied to the consuming
+//               GEMM's accumulator;
+//   warp 6      activation loader (one thread): after the phase's grid
+//               barrier, one 6 KB bulk copy of the image per stage;
+//   warps 2-9   attention phase between QKV and O (flash-decode style, fixed
+//               key partition -> deterministic, batch invariant).
+//
+// Dependent phases are separated by a monotonic grid barrier (all CTAs are
+// co-resident: cooperative launch, one CTA per SM); the last CTA to exit
+// resets it for the next launch.  Arithmetic matches sfg_fast.cu (same
+// split, same stream-K fixup order) within the stated tolerance; results
+// are deterministic and independent of the batch composition.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "sfg_engine.h"
+#include "sfg_prof.h"
+#include "sfg_tc.cuh"
+
+namespace sfg {
+namespace mega {
+
+using namespace tc;
+
+constexpr int kMaxStages = 8;
+constexpr int kThreads = 320;
+constexpr int kAccCols = 64;
+constexpr int kTmemCols = 128;
+constexpr int kMaxPieces = 16;
+constexpr int kMaxGroup = 8;
+enum Phase : int { P_QKV = 0, P_O = 1, P_GU = 2, P_DOWN = 3 };
+
+struct LayerDesc {
+    const uint8_t* w[4];     // tiled W^T images: qkv, o, gate|up, down
+    const float* attn_norm;
+    const float* ffn_norm;
+    const float* next_attn_norm;  // the following layer's attn_norm (nullptr for the last)
+    float* kc;               // this layer's K slab [n_kv][max_len][hd]
+    float* vc;
+};
+
+struct MegaArgs {
+    const LayerDesc* layers;
+    int nlayers, rows, stages;
+    int H, qd, kvd, F, hd, n_heads, n_kv, max_len;
+    float eps;
+    float* h;        // [16][H] residual stream, in/out
+    float* q;        // [16][qd]
+    float* att;      // [16][qd]
+    float* act;      // [16][F]
+    float* ss_d;     // [tilesH][16] sum-of-squares partials of h (input / after down)
+    float* ss_o;     // [tilesH][16] after O-proj
+    const int32_t* pos;
+    const float* rope_cos;
+    const float* rope_sin;
+    const int32_t* prior;
+    const int32_t* row_off;
+    const MaskRun* runs;
+    float* partials;   // [tiles_max][kMaxPieces][16][128]
+    int* counters;     // [tiles_max]
+    unsigned* bar;     // per-barrier arrival counters + exit counter
+    uint32_t* status;
+    uint8_t* xim[4];   // per phase: the GEMM's input as [KB][48 x 64] split bf16 images (put_split)
+    // optional [G][kBarSlots][8]: 0 X start, 1 X done, 2 arrive (globaltimer);
+    // 3/4/5 ns waited by X-writer (empty), MMA (full), producer (empty)
+    unsigned long long* trace;
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+struct Geo {
+    int tiles, KB, G;  // G: CTAs sharing this GEMM's stream-K split (see split_ctas)
+};
+// Stream-K split width: at most gridDim.x CTAs, each with at least
+// ceil((KB-1)/(kMaxPieces-1)) k-blocks so a tile never has more than
+// kMaxPieces pieces; CTAs >= G get no units in this phase.
+__host__ __device__ __forceinline__ int split_ctas(int tiles, int KB, int grid) {
+    const long long U = static_cast<long long>(tiles) * KB;
+    const int min_units = (KB - 1 + kMaxPieces - 2) / (kMaxPieces - 1);
+    long long g = min_units > 0 ? U / min_units : U;
+    if (g > grid) g = grid;
+    if (g < 1) g = 1;
+    return static_cast<int>(g);
+}
+__device__ __forceinline__ Geo geom(const MegaArgs& a, int p) {
+    int t, kb;
+    switch (p) {
+        case P_QKV: t = (a.qd + 2 * a.kvd + kM - 1) / kM; kb = a.H / kKB; break;
+        case P_O: t = (a.H + kM - 1) / kM; kb = a.qd / kKB; break;
+        case P_GU: t = a.F / 64; kb = a.H / kKB; break;
+        default: t = (a.H + kM - 1) / kM; kb = a.F / kKB; break;
+    }
+    return {t, kb, split_ctas(t, kb, gridDim.x)};
+}
+// this CTA's unit range [st, en) of a phase (empty when c >= g.G)
+__device__ __forceinline__ void unit_range(const Geo& g, int c, long long& st, long long& en) {
+    const long long U = static_cast<long long>(g.tiles) * g.KB;
+    if (c >= g.G) {
+        st = en = 0;
+        return;
+    }
+    st = c * U / g.G;
+    en = (c + 1) * U / g.G;
+}
+
+// ── grid barrier ──────────────────────────────────────────────────────────
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void grid_arrive(unsigned* bar) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+}
+__device__ __forceinline__ void grid_wait(const unsigned* bar, unsigned target) {
+    unsigned long long spins = 0;
+    while (ld_acquire(bar) < target) {
+        __nanosleep(64);
+        if (++spins > (1ull << 27)) asm volatile("trap;");  // never hang the GPU
+    }
+    __threadfence();
+}
+// barrier ids: 0 = input stats; layer i: 1+5i QKV, 2+5i attention, 3+5i O, 4+5i gate|up, 5+5i down.
+// One counter per id (a single monotonic counter is wrong: CTAs with no
+// work in a phase may arrive for later barriers before others arrive for
+// the current one); bar[kBarSlots] counts exits, the last CTA out zeroes all.
+constexpr int kBarSlots = 256;
+__device__ __forceinline__ void arrive_id(unsigned* bar, int id) { grid_arrive(bar + id); }
+__device__ __forceinline__ void wait_id(unsigned* bar, int id, int G) { grid_wait(bar + id, static_cast<unsigned>(G)); }
+__device__ __forceinline__ int input_barrier(int layer, int p) {
+    switch (p) {
+        case P_QKV: return layer == 0 ? 0 : 5 * (layer - 1) + 5;
+        case P_O: return 5 * layer + 2;
+        case P_GU: return 5 * layer + 3;
+        default: return 5 * layer + 4;
+    }
+}
+
+// bounded mbarrier wait (traps instead of hanging on a protocol bug)
+__device__ __forceinline__ void mwait(uint64_t* b, uint32_t parity) {
+    uint32_t done = 0;
+    unsigned long long spins = 0;
+    while (true) {
+        asm volatile(
+            "{\n.reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (++spins > (1ull << 26)) asm volatile("trap;");
+    }
+}
+
+// mwait that also accumulates the time spent waiting when tracing
+__device__ __forceinline__ void mwait_acc(uint64_t* b, uint32_t parity, bool tr, unsigned long long& acc) {
+    if (!tr) {
+        mwait(b, parity);
+        return;
+    }
+    const unsigned long long t0 = gtimer();
+    mwait(b, parity);
+    acc += gtimer() - t0;
+}
+
+// Deterministic sum over the 128 epilogue threads (feature m = 32*quad + lane)
+// of v[r]^2 for 16 rows -> out[r]: warp butterfly, then a fixed 4-way combine.
+__device__ __forceinline__ void tile_sumsq(const float (&v)[kRows], float* red, float* out, int et) {
+    const int quad = et >> 5, lane = et & 31;
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+        float s = v[r] * v[r];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) red[quad * kRows + r] = s;
+    }
+    named_sync(1, 128);
+    if (et < kRows) out[et] = (red[et] + red[kRows + et]) + (red[2 * kRows + et] + red[3 * kRows + et]);
+    named_sync(1, 128);
+}
+
+// generic-proxy global writes <-> cp.async.bulk reads of the same bytes
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// Store x as its 3-way bf16 split (hi | mid | lo rows of the B operand) at
+// feature k, row r of a phase's global activation image: [KB][48 x 64] bf16
+// K-major SW128 blocks, the exact smem layout the MMA reads, so a stage's
+// activations arrive with one 6 KB bulk copy.
+__device__ __forceinline__ void put_split(uint8_t* img, int k, int r, float x) {
+    uint8_t* blk = img + static_cast<size_t>(k >> 6) * kBBytes;
+    const int kk = k & 63;
+    const __nv_bfloat16 hb = __float2bfloat16_rn(x);
+    const float r1 = x - __bfloat162float(hb);
+    const __nv_bfloat16 mb = __float2bfloat16_rn(r1);
+    const __nv_bfloat16 lb = __float2bfloat16_rn(r1 - __bfloat162float(mb));
+    *reinterpret_cast<__nv_bfloat16*>(blk + sw128_off(r, kk)) = hb;
+    *reinterpret_cast<__nv_bfloat16*>(blk + sw128_off(kRows + r, kk)) = mb;
+    *reinterpret_cast<__nv_bfloat16*>(blk + sw128_off(2 * kRows + r, kk)) = lb;
+}
+
+// ── epilogues (thread = feature m of the tile; y[r] for 16 rows) ─────────
+// RMSNorm is split across the two sides of the GEMM: the producing epilogue
+// stores split(h * gain) (gain is per input feature), and the consuming
+// epilogue scales its accumulator by the per-row 1/rms (rs[r]), which needs
+// the whole row's sum of squares and so is only known after the barrier.
+__device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int p, int tile, int m, int et,
+                          const float (&yin)[kRows], float* xch, const float* rs) {
+    float y[kRows];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) y[r] = (p == P_QKV || p == P_GU) ? yin[r] * rs[r] : yin[r];
+    if (p == P_QKV) {
+        const int f = tile * kM + m;
+        const bool valid = f < a.qd + 2 * a.kvd;
+        const int seg = f < a.qd ? 0 : (f < a.qd + a.kvd ? 1 : 2);
+        const int fl = seg == 0 ? f : (seg == 1 ? f - a.qd : f - a.qd - a.kvd);
+        const int d = fl % a.hd, half = a.hd >> 1, i = d >> 1;
+        const bool odd = (m & 1) != 0;
+        const int prior = *a.prior;
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) {
+            const float partner = __shfl_xor_sync(0xffffffffu, y[r], 1);
+            if (!valid || r >= a.rows) continue;
+            float v = y[r];
+            if (seg != 2) {
+                const int ps = a.pos[r];
+                const float c = a.rope_cos[static_cast<size_t>(ps) * half + i];
+                const float s = a.rope_sin[static_cast<size_t>(ps) * half + i];
+                v = odd ? __fadd_rn(__fmul_rn(partner, s), __fmul_rn(v, c))
+                        : __fsub_rn(__fmul_rn(v, c), __fmul_rn(partner, s));
+            }
+            if (seg == 0) {
+                a.q[static_cast<size_t>(r) * a.qd + fl] = v;
+            } else {
+                float* dst = (seg == 1 ? L.kc : L.vc) +
+                             (static_cast<size_t>(fl / a.hd) * a.max_len + prior + r) * a.hd + d;
+                *dst = v;
+            }
+        }
+    } else if (p == P_GU) {
+        float* ub = xch;  // [64][16]
+        if (m >= 64)
+#pragma unroll
+            for (int r = 0; r < kRows; ++r) ub[(m - 64) * kRows + r] = y[r];
+        named_sync(1, 128);
+        if (m < 64) {
+            const int fg = tile * 64 + m;
+            if (fg < a.F)
+#pragma unroll
+                for (int r = 0; r < kRows; ++r)
+                    if (r < a.rows) {
+                        const float g = y[r];
+                        const float silu = g / (1.0f + expf(-g));
+                        const float v = silu * ub[m * kRows + r];
+                        a.act[static_cast<size_t>(r) * a.F + fg] = v;
+                        put_split(a.xim[P_DOWN], fg, r, v);
+                    }
+        }
+        named_sync(1, 128);
+    } else {  // residual add + sum-of-squares partials for the next RMSNorm
+        const int f = tile * kM + m;
+        // the next GEMM's input image: split(h * gain) of ffn_norm (after O)
+        // or of the next layer's attn_norm (after down; none after the last)
+        const float* gn = p == P_O ? L.ffn_norm : L.next_attn_norm;
+        uint8_t* img = p == P_O ? a.xim[P_GU] : a.xim[P_QKV];
+        const float gf = (gn && f < a.H) ? __ldg(gn + f) : 0.0f;
+        float hn[kRows];
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) {
+            hn[r] = 0.0f;
+            if (f < a.H && r < a.rows) {
+                float* o = a.h + static_cast<size_t>(r) * a.H + f;
+                hn[r] = __ldcg(o) + y[r];
+                *o = hn[r];
+                if (gn) put_split(img, f, r, hn[r] * gf);
+            }
+        }
+        float* ss = (p == P_O ? a.ss_o : a.ss_d) + static_cast<size_t>(tile) * kRows;
+        tile_sumsq(hn, xch + 64 * kRows, ss, et);
+    }
+}
+
+// ── attention for one (row, kv head): flash-decode over the row's visible
+// keys with a fixed key partition (chunk i of 32 keys -> warp i % 8).
+template <int HD, int GR>  // GR: compile-time bound on the GQA group (register arrays)
+__device__ void attention_item(const MegaArgs& a, const LayerDesc& L, int row, int kvh, int at, float* qs,
+                               float* wst, float* ocomb, int* cols) {
+    const int group = a.n_heads / a.n_kv;
+    const int warp = at >> 5, lane = at & 31;
+    for (int t = at; t < group * HD; t += 256)
+        qs[t] = __ldcg(a.q + static_cast<size_t>(row) * a.qd + static_cast<size_t>(kvh * group) * HD + t);
+    // expand visibility runs into compacted columns
+    __shared__ int n_s, roff_s[65];
+    const int r0 = a.row_off[row], r1 = a.row_off[row + 1];
+    int total = 0;
+    for (int base = r0; base < r1; base += 64) {
+        const int nr = min(64, r1 - base);
+        if (at == 0) {
+            int off = total;
+            for (int r = 0; r < nr; ++r) {
+                roff_s[r] = off;
+                off += a.runs[base + r].end - a.runs[base + r].start;
+            }
+            roff_s[64] = off;
+        }
+        named_sync(3, 256);
+        for (int r = 0; r < nr; ++r) {
+            const MaskRun rr = a.runs[base + r];
+            for (int j = rr.start + at; j < rr.end; j += 256) cols[roff_s[r] + j - rr.start] = j;
+        }
+        total = roff_s[64];
+        named_sync(3, 256);
+    }
+    if (at == 0) n_s = total;
+    named_sync(3, 256);
+    const int n = n_s;
+    // NOTE: frame masks carry mval == 0 for every visible column; additive
+    // masks (seam 2) take the per-GEMM path (see mega_supported()).
+    const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(HD));
+    const float* kb = L.kc + static_cast<size_t>(kvh) * a.max_len * HD;
+    const float* vb = L.vc + static_cast<size_t>(kvh) * a.max_len * HD;
+    // A warp takes 8 keys per iteration: 4 lanes per key split the score dot
+    // (HD/4 dims each, one batch of loads), then all 32 lanes sweep head
+    // dims for the value sum with the 8 value rows loaded up front.
+    constexpr int DPL = HD / 32;
+    constexpr int Q4 = HD / 16;  // float4 loads per lane per key
+    float mrun[GR], lrun[GR], o[GR][DPL];
+#pragma unroll
+    for (int g = 0; g < GR; ++g) {
+        mrun[g] = -INFINITY;
+        lrun[g] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) o[g][i] = 0.0f;
+    }
+    const int kk = lane >> 2, sub = lane & 3;
+    const int nchunks = (n + 7) / 8;
+    for (int ch = warp; ch < nchunks; ch += 8) {
+        const int c = ch * 8 + kk;
+        const bool live = c < n;
+        const int col = live ? cols[c] : 0;
+        const float4* kr = reinterpret_cast<const float4*>(kb + static_cast<size_t>(col) * HD + sub * (HD / 4));
+        float4 k4[Q4];
+#pragma unroll
+        for (int t = 0; t < Q4; ++t) k4[t] = __ldcg(kr + t);
+        float s[GR];
+#pragma unroll
+        for (int g = 0; g < GR; ++g) {
+            s[g] = 0.0f;
+            if (g >= group) continue;
+            const float4* q4 = reinterpret_cast<const float4*>(qs + g * HD + sub * (HD / 4));
+#pragma unroll
+            for (int t = 0; t < Q4; ++t) {
+                const float4 qq = q4[t];
+                s[g] += qq.x * k4[t].x + qq.y * k4[t].y + qq.z * k4[t].z + qq.w * k4[t].w;
+            }
+            s[g] += __shfl_xor_sync(0xffffffffu, s[g], 1);
+            s[g] += __shfl_xor_sync(0xffffffffu, s[g], 2);
+        }
+        // value rows of the chunk's 8 keys (coalesced over lanes, one batch)
+        float v[8][DPL];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int cj = __shfl_sync(0xffffffffu, col, 4 * j);
+            const bool lj = ch * 8 + j < n;
+#pragma unroll
+            for (int i = 0; i < DPL; ++i) v[j][i] = lj ? __ldcg(vb + static_cast<size_t>(cj) * HD + lane + 32 * i) : 0.0f;
+        }
+#pragma unroll
+        for (int g = 0; g < GR; ++g) {
+            if (g >= group) break;
+            const float sv = live ? s[g] * inv_sqrt_hd : -INFINITY;
+            float cm = sv;
+            for (int off = 16; off > 2; off >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, off));
+            const float mn = fmaxf(mrun[g], cm);
+            const float scale_old = mrun[g] == -INFINITY ? 0.0f : expf(mrun[g] - mn);
+            const float pr = live ? expf(sv - mn) : 0.0f;
+            float ps = sub == 0 ? pr : 0.0f;
+            for (int off = 16; off > 0; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+            lrun[g] = lrun[g] * scale_old + ps;
+            mrun[g] = mn;
+#pragma unroll
+            for (int i = 0; i < DPL; ++i) o[g][i] *= scale_old;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float pj = __shfl_sync(0xffffffffu, pr, 4 * j);
+#pragma unroll
+                for (int i = 0; i < DPL; ++i) o[g][i] += pj * v[j][i];
+            }
+        }
+    }
+    // combine the 8 warps in fixed order
+#pragma unroll
+    for (int g = 0; g < GR; ++g) {
+        if (g >= group) break;
+        if (lane == 0) {
+            wst[(warp * kMaxGroup + g) * 2] = mrun[g];
+            wst[(warp * kMaxGroup + g) * 2 + 1] = lrun[g];
+        }
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) ocomb[(warp * group + g) * HD + lane + 32 * i] = o[g][i];
+    }
+    named_sync(3, 256);
+    for (int t = at; t < group * HD; t += 256) {
+        const int g = t / HD, dd = t % HD;
+        float mx = -INFINITY;
+        for (int w = 0; w < 8; ++w) mx = fmaxf(mx, wst[(w * kMaxGroup + g) * 2]);
+        float l = 0.0f, acc = 0.0f;
+        for (int w = 0; w < 8; ++w) {
+            const float mw = wst[(w * kMaxGroup + g) * 2];
+            const float sc = mw == -INFINITY ? 0.0f : expf(mw - mx);
+            l += wst[(w * kMaxGroup + g) * 2 + 1] * sc;
+            acc += ocomb[(w * group + g) * HD + dd] * sc;
+        }
+        if (mx == -INFINITY) atomicOr(a.status, ST_EMPTY_ROW);
+        const int f = (kvh * group + g) * HD + dd;
+        const float o = acc / l;
+        a.att[static_cast<size_t>(row) * a.qd + f] = o;
+        put_split(a.xim[P_O], f, row, o);
+    }
+    fence_proxy_async_global();
+    named_sync(3, 256);
+}
+
+__device__ __forceinline__ void attention_dispatch(const MegaArgs& a, const LayerDesc& L, int row, int kvh, int at,
+                                                   float* qs, float* wst, float* ocomb, int* cols) {
+    const int group = a.n_heads / a.n_kv;
+    if (group <= 4) {
+        switch (a.hd) {
+            case 64: attention_item<64, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
+            case 128: attention_item<128, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
+            case 160: attention_item<160, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
+            default: attention_item<32, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
+        }
+    } else {
+        switch (a.hd) {
+            case 64: attention_item<64, 8>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
+            default: attention_item<32, 8>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
+        }
+    }
+}
+
+// ── the kernel ────────────────────────────────────────────────────────────
+// 10 warps, one CTA per SM: 3 warps share an SM sub-partition's 16K
+// registers, so 168 registers per thread is the ceiling
+__global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant__ MegaArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = a.stages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * kStageBytes);
+    uint64_t* empty = full + kMaxStages;
+    uint64_t* tfull = empty + kMaxStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int* flag = reinterpret_cast<int*>(tmem_slot + 4);
+    float* xch = reinterpret_cast<float*>(flag + 4);          // 64*16 gate|up + 4*16 sumsq
+    float* rs = xch + 64 * kRows + 4 * kRows;                  // [16] per-row 1/rms of the phase
+    float* qs = rs + kRows;                                    // [group][hd]
+    float* wst = qs + kMaxGroup * a.hd;                        // [8][kMaxGroup][2]
+    float* ocomb = wst + 8 * kMaxGroup * 2;                    // [8][group][hd]
+    int* cols = reinterpret_cast<int*>(ocomb + 8 * (a.n_heads / a.n_kv) * a.hd);  // [max_len]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int G = gridDim.x, c = blockIdx.x;
+    if (threadIdx.x == 0 && a.trace) a.trace[(static_cast<size_t>(c) * kBarSlots + kBarSlots - 1) * 8] = gtimer();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 2);   // weight bytes + activation bytes (two expect_tx arrivals)
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int tilesH = (a.H + kM - 1) / kM;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ── weight producer
+            int stage = 0;
+            uint32_t ph = 0;
+            for (int l = 0; l < a.nlayers; ++l)
+                for (int p = 0; p < 4; ++p) {
+                    const Geo g = geom(a, p);
+                    const uint8_t* W = a.layers[l].w[p];
+                    const long long U = static_cast<long long>(g.tiles) * g.KB;
+                    long long st, en;
+                (void)U;
+                unit_range(g, c, st, en);
+                    unsigned long long wacc = 0;
+                    for (long long u = st; u < en; ++u) {
+                        mwait_acc(&empty[stage], ph ^ 1, a.trace != nullptr, wacc);
+                        mbar_expect_tx(&full[stage], kABytes);
+                        bulk_g2s(smem + stage * kStageBytes, W + static_cast<size_t>(u) * kABytes, kABytes, &full[stage]);
+                        if (++stage == S) {
+                            stage = 0;
+                            ph ^= 1;
+                        }
+                    }
+                    if (a.trace) a.trace[(static_cast<size_t>(c) * kBarSlots + input_barrier(l, p)) * 8 + 5] = wacc;
+                }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ── MMA issuer
+            int stage = 0, acc = 0;
+            uint32_t ph = 0, acc_ph = 0;
+            for (int l = 0; l < a.nlayers; ++l)
+                for (int p = 0; p < 4; ++p) {
+                    const Geo g = geom(a, p);
+                    const long long U = static_cast<long long>(g.tiles) * g.KB;
+                    long long st, en;
+                (void)U;
+                unit_range(g, c, st, en);
+                    unsigned long long wacc = 0;
+                    for (long long u = st; u < en;) {
+                        const int t = static_cast<int>(u / g.KB);
+                        const int lo = static_cast<int>(u - static_cast<long long>(t) * g.KB);
+                        const int hi = static_cast<int>(min(en - static_cast<long long>(t) * g.KB, static_cast<long long>(g.KB)));
+                        mwait(&tempty[acc], acc_ph ^ 1);
+                        tc_fence_after();
+                        const uint32_t d = tmem + acc * kAccCols;
+                        for (int kb = lo; kb < hi; ++kb) {
+                            mwait_acc(&full[stage], ph, a.trace != nullptr, wacc);
+                            tc_fence_after();
+                            const uint32_t sa = smem_u32(smem + stage * kStageBytes);
+                            const uint64_t da = smem_desc(sa), db = smem_desc(sa + kABytes);
+#pragma unroll
+                            for (int k = 0; k < kKB / 16; ++k) mma_bf16(d, da + 2 * k, db + 2 * k, (kb > lo || k > 0) ? 1u : 0u);
+                            mma_commit(&empty[stage]);
+                            if (++stage == S) {
+                                stage = 0;
+                                ph ^= 1;
+                            }
+                        }
+                        mma_commit(&tfull[acc]);
+                        if (++acc == 2) {
+                            acc = 0;
+                            acc_ph ^= 1;
+                        }
+                        u = static_cast<long long>(t) * g.KB + hi;
+                    }
+                    if (a.trace) a.trace[(static_cast<size_t>(c) * kBarSlots + input_barrier(l, p)) * 8 + 4] = wacc;
+                }
+        }
+    } else if (warp < 6) {  // ── epilogue warps 2..5 (+ attention)
+        const int q = warp & 3, m = q * 32 + lane, et = threadIdx.x - 64;
+        // input statistics: sum-of-squares partials of h for the first RMSNorm,
+        // and the first QKV GEMM's input image split(h * attn_norm)
+        for (int t = c; t < tilesH; t += G) {
+            const int f = t * kM + m;
+            const float gf = f < a.H ? __ldg(a.layers[0].attn_norm + f) : 0.0f;
+            float hv[kRows];
+#pragma unroll
+            for (int r = 0; r < kRows; ++r) {
+                hv[r] = (f < a.H && r < a.rows) ? __ldcg(a.h + static_cast<size_t>(r) * a.H + f) : 0.0f;
+                if (f < a.H && r < a.rows) put_split(a.xim[P_QKV], f, r, hv[r] * gf);
+            }
+            tile_sumsq(hv, xch + 64 * kRows, a.ss_d + static_cast<size_t>(t) * kRows, et);
+        }
+        fence_proxy_async_global();
+        named_sync(1, 128);
+        if (et == 0) arrive_id(a.bar, 0);
+        int acc = 0;
+        uint32_t acc_ph = 0;
+        for (int l = 0; l < a.nlayers; ++l) {
+            const LayerDesc& L = a.layers[l];
+            for (int p = 0; p < 4; ++p) {
+                const Geo g = geom(a, p);
+                const long long U = static_cast<long long>(g.tiles) * g.KB;
+                long long st, en;
+                unit_range(g, c, st, en);
+                if ((p == P_QKV || p == P_GU) && st < en) {  // per-row 1/rms from the ss partials
+                    if (et == 0) wait_id(a.bar, input_barrier(l, p), G);
+                    named_sync(1, 128);
+                    if (et < kRows) {
+                        const float* ssb = p == P_QKV ? a.ss_d : a.ss_o;
+                        float ss = 0.0f;
+                        for (int t = 0; t < tilesH; ++t) ss += __ldcg(ssb + t * kRows + et);
+                        rs[et] = 1.0f / sqrtf(ss / static_cast<float>(a.H) + a.eps);
+                    }
+                    named_sync(1, 128);
+                }
+                unsigned long long t_acc = 0;
+                for (long long u = st; u < en;) {
+                    const int t = static_cast<int>(u / g.KB);
+                    const int lo = static_cast<int>(u - static_cast<long long>(t) * g.KB);
+                    const int hi = static_cast<int>(min(en - static_cast<long long>(t) * g.KB, static_cast<long long>(g.KB)));
+                    mwait(&tfull[acc], acc_ph);
+                    if (a.trace && et == 0) t_acc = gtimer();
+                    tc_fence_after();
+                    float v[kN];
+                    const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * kAccCols;
+                    tmem_ld16(ta, v);
+                    tmem_ld16(ta + 16, v + 16);
+                    tmem_ld16(ta + 32, v + 32);
+                    tmem_wait_ld();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                    if (++acc == 2) {
+                        acc = 0;
+                        acc_ph ^= 1;
+                    }
+                    float y[kRows];
+#pragma unroll
+                    for (int r = 0; r < kRows; ++r) y[r] = (v[r] + v[kRows + r]) + v[2 * kRows + r];
+                    if (lo == 0 && hi == g.KB) {
+                        epi_final(a, L, p, t, m, et, y, xch, rs);
+                    } else {  // stream-K fixup: last arriver sums the pieces in k order
+                        const long long first_u = static_cast<long long>(t) * g.KB;
+                        const int c_first = static_cast<int>(((first_u + 1) * g.G - 1) / U);
+                        const int piece = c - c_first;
+                        const int n_pieces = static_cast<int>(((first_u + g.KB) * g.G - 1) / U) - c_first + 1;
+                        float* slot = a.partials + (static_cast<size_t>(t) * kMaxPieces + piece) * kRows * kM;
+#pragma unroll
+                        for (int r = 0; r < kRows; ++r) slot[r * kM + m] = y[r];
+                        __threadfence();
+                        named_sync(1, 128);
+                        if (et == 0) {
+                            const int old = atomicAdd(&a.counters[t], 1);
+                            *flag = (old == n_pieces - 1) ? 1 : 0;
+                            if (old == n_pieces - 1) a.counters[t] = 0;
+                        }
+                        named_sync(1, 128);
+                        if (*flag) {
+                            __threadfence();
+                            float s[kRows];
+                            const float* p0 = a.partials + static_cast<size_t>(t) * kMaxPieces * kRows * kM;
+#pragma unroll
+                            for (int r = 0; r < kRows; ++r) s[r] = __ldcg(p0 + r * kM + m);
+                            for (int pc = 1; pc < n_pieces; ++pc)
+#pragma unroll
+                                for (int r = 0; r < kRows; ++r)
+                                    s[r] = s[r] + __ldcg(p0 + (static_cast<size_t>(pc) * kRows + r) * kM + m);
+                            epi_final(a, L, p, t, m, et, s, xch, rs);
+                        }
+                        named_sync(1, 128);
+                    }
+                    u = static_cast<long long>(t) * g.KB + hi;
+                }
+                fence_proxy_async_global();
+                named_sync(1, 128);
+                if (et == 0) {
+                    const int id = 5 * l + (p == P_QKV ? 1 : p + 2);
+                    if (a.trace) {
+                        a.trace[(static_cast<size_t>(c) * kBarSlots + id) * 8 + 2] = gtimer();
+                        a.trace[(static_cast<size_t>(c) * kBarSlots + input_barrier(l, p)) * 8 + 6] = t_acc;
+                    }
+                    arrive_id(a.bar, id);
+                }
+                if (p == P_QKV) {  // attention phase, shared with the activation warps
+                    if (et == 0) wait_id(a.bar, 5 * l + 1, G);
+                    named_sync(1, 128);
+                    __threadfence();
+                    for (int it = c; it < a.rows * a.n_kv; it += G)
+                        attention_dispatch(a, L, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst, ocomb, cols);
+                    named_sync(3, 256);
+                    if (et == 0) {
+                        if (a.trace) a.trace[(static_cast<size_t>(c) * kBarSlots + 5 * l + 2) * 8 + 2] = gtimer();
+                        arrive_id(a.bar, 5 * l + 2);
+                    }
+                }
+            }
+        }
+    } else {  // ── activation loader (warp 6 lane 0) + attention (warps 6..9)
+        const int xt = threadIdx.x - 192;
+        int stage = 0;
+        uint32_t ph = 0;
+        for (int l = 0; l < a.nlayers; ++l) {
+            const LayerDesc& L = a.layers[l];
+            for (int p = 0; p < 4; ++p) {
+                if (xt == 0) {
+                    // after the phase's input barrier, one bulk copy per stage
+                    // brings the unit's k-block of the prebuilt input image
+                    wait_id(a.bar, input_barrier(l, p), G);
+                    fence_proxy_async_global();
+                    if (a.trace) a.trace[(static_cast<size_t>(c) * kBarSlots + input_barrier(l, p)) * 8] = gtimer();
+                    const Geo g = geom(a, p);
+                    long long st, en;
+                    unit_range(g, c, st, en);
+                    const uint8_t* X = a.xim[p];
+                    unsigned long long xwacc = 0;
+                    for (long long u = st; u < en; ++u) {
+                        mwait_acc(&empty[stage], ph ^ 1, a.trace != nullptr, xwacc);
+                        mbar_expect_tx(&full[stage], kBBytes);
+                        bulk_g2s(smem + stage * kStageBytes + kABytes, X + static_cast<size_t>(u % g.KB) * kBBytes,
+                                 kBBytes, &full[stage]);
+                        if (++stage == S) {
+                            stage = 0;
+                            ph ^= 1;
+                        }
+                    }
+                    if (a.trace) {
+                        a.trace[(static_cast<size_t>(c) * kBarSlots + input_barrier(l, p)) * 8 + 1] = gtimer();
+                        a.trace[(static_cast<size_t>(c) * kBarSlots + input_barrier(l, p)) * 8 + 3] = xwacc;
+                    }
+                }
+                __syncwarp();
+                if (p == P_QKV) {  // join the attention phase
+                    if (xt == 0) wait_id(a.bar, 5 * l + 1, G);
+                    named_sync(2, 128);
+                    __threadfence();
+                    for (int it = c; it < a.rows * a.n_kv; it += G)
+                        attention_dispatch(a, L, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst, ocomb, cols);
+                    named_sync(3, 256);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_free(tmem, kTmemCols);
+    }
+    if (threadIdx.x == 0) {  // last CTA out resets the barrier for the next launch
+        __threadfence();
+        const unsigned prev = atomicAdd(a.bar + kBarSlots, 1u);
+        if (prev == static_cast<unsigned>(G) - 1) {
+            const int nbar = 1 + 5 * a.nlayers;
+            for (int i = 0; i < nbar; ++i) atomicExch(a.bar + i, 0u);
+            atomicExch(a.bar + kBarSlots, 0u);
+        }
+    }
+}
+
+size_t smem_bytes(int stages, int hd, int group, int max_len) {
+    return 1024 + static_cast<size_t>(stages) * kStageBytes + (2 * kMaxStages + 4) * 8 + 32 +
+           sizeof(float) * (64 * kRows + 5 * kRows + kMaxGroup * hd + 8 * kMaxGroup * 2 + 8 * group * hd) +
+           sizeof(int) * static_cast<size_t>(max_len);
+}
+
+}  // namespace mega
+
+using namespace mega;
+
+// The megakernel covers decode batches (<= 16 rows) with frame-style masks
+// (visible mask value 0); seam-2 additive masks and long prompts take the
+// per-GEMM path.
+bool mega_supported(const Engine& e, int rows, bool additive_mask) {
+    if (rows < 1 || rows > tc::kRows || additive_mask) return false;
+    const ModelCfg& c = e.cfg();
+    const int group = c.n_heads / c.n_kv_heads;
+    if (group > kMaxGroup || c.head_dim % 32 != 0 || c.head_dim > 160) return false;
+    if (group > 4 && c.head_dim > 64) return false;  // register budget of the attention phase
+    if (c.hidden_dim % tc::kKB || c.q_dim() % tc::kKB || c.ffn_dim % tc::kKB) return false;
+    const size_t sm = smem_bytes(4, c.head_dim, c.n_heads / c.n_kv_heads, c.max_seq_len);
+    return sm <= 227 * 1024;
+}
+
+namespace {
+struct MegaState {
+    LayerDesc* d_layers = nullptr;
+    int lb = -1, le = -1;
+    unsigned* bar = nullptr;
+    float* ss = nullptr;
+    unsigned long long* trace = nullptr;
+    uint8_t* xim = nullptr;  // the four phases' input images, back to back
+    ~MegaState() {
+        if (d_layers) cudaFree(d_layers);
+        if (bar) cudaFree(bar);
+        if (ss) cudaFree(ss);
+        if (trace) cudaFree(trace);
+        if (xim) cudaFree(xim);
+    }
+};
+}  // namespace
+
+bool& mega_trace_enabled() {
+    static bool on = false;
+    return on;
+}
+
+// debugging: copy the bank's phase timeline ([G][256][8] globaltimer stamps)
+int mega_trace_read(Bank& b, unsigned long long* out, size_t n) {
+    MegaState* st = static_cast<MegaState*>(b.mega.get());
+    if (!st || !st->trace) return 0;
+    SFG_CUDA(cudaDeviceSynchronize());
+    SFG_CUDA(cudaMemcpy(out, st->trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost));
+    return 1;
+}
+
+// debugging: the bank's sum-of-squares partial buffers (0: ss_d, 1: ss_o)
+float* mega_ss(Bank& b, int which, int tilesH) {
+    MegaState* st = static_cast<MegaState*>(b.mega.get());
+    if (!st) return nullptr;
+    return st->ss + (which ? tilesH * tc::kRows : 0);
+}
+
+int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cudaStream_t s) {
+    const ModelCfg& c = e.cfg();
+    // per-bank layer table (weights + this bank's KV slabs), grid barrier and
+    // sum-of-squares buffers, owned by the bank
+    MegaState* stp = static_cast<MegaState*>(b.mega.get());
+    if (stp && (stp->lb != lb || stp->le != le)) {
+        SFG_CUDA(cudaDeviceSynchronize());
+        b.mega.reset();
+        stp = nullptr;
+    }
+    if (!stp) {
+        auto holder = std::make_shared<MegaState>();
+        MegaState& st = *holder;
+        st.lb = lb;
+        st.le = le;
+        std::vector<LayerDesc> host(le - lb);
+        for (int l = lb; l < le; ++l) {
+            const LayerWeights& L = e.layer(l);
+            LayerDesc& d = host[l - lb];
+            d.w[0] = static_cast<const uint8_t*>(L.f_qkv);
+            d.w[1] = static_cast<const uint8_t*>(L.f_o);
+            d.w[2] = static_cast<const uint8_t*>(L.f_gu);
+            d.w[3] = static_cast<const uint8_t*>(L.f_down);
+            d.attn_norm = L.attn_norm;
+            d.ffn_norm = L.ffn_norm;
+            d.next_attn_norm = l + 1 < le ? e.layer(l + 1).attn_norm : nullptr;
+            d.kc = b.kslab(l);
+            d.vc = b.vslab(l);
+        }
+        SFG_CUDA(cudaMalloc(&st.d_layers, sizeof(LayerDesc) * host.size()));
+        SFG_CUDA(cudaMemcpy(st.d_layers, host.data(), sizeof(LayerDesc) * host.size(), cudaMemcpyHostToDevice));
+        SFG_CUDA(cudaMalloc(&st.bar, sizeof(unsigned) * (kBarSlots + 1)));
+        SFG_CUDA(cudaMemset(st.bar, 0, sizeof(unsigned) * (kBarSlots + 1)));
+        const int tilesH = (c.hidden_dim + tc::kM - 1) / tc::kM;
+        SFG_CUDA(cudaMalloc(&st.ss, sizeof(float) * 2 * tilesH * tc::kRows));
+        const size_t xblocks = static_cast<size_t>(2 * c.hidden_dim + c.q_dim() + c.ffn_dim) / tc::kKB;
+        SFG_CUDA(cudaMalloc(&st.xim, xblocks * tc::kBBytes));
+        SFG_CUDA(cudaMemset(st.xim, 0, xblocks * tc::kBBytes));
+        SFG_CUDA(cudaDeviceSynchronize());
+        b.mega = holder;
+        stp = holder.get();
+    }
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int group = c.n_heads / c.n_kv_heads;
+    int stages = kMaxStages;
+    while (stages > 4 && smem_bytes(stages, c.head_dim, group, c.max_seq_len) > 227 * 1024) --stages;
+    const size_t smem = smem_bytes(stages, c.head_dim, group, c.max_seq_len);
+    static size_t configured = 0;
+    if (smem > configured) {
+        SFG_CUDA(cudaFuncSetAttribute(mega_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured = smem;
+        int nb = 0;
+        SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, mega_kernel, kThreads, smem));
+        if (nb < 1) {
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, mega_kernel);
+            throw Error(Kind::internal, "megakernel does not fit an SM: regs " + std::to_string(fa.numRegs) +
+                                            " static smem " + std::to_string(fa.sharedSizeBytes) + " dyn smem " +
+                                            std::to_string(smem) + " max threads " + std::to_string(fa.maxThreadsPerBlock));
+        }
+    }
+    const int tilesH = (c.hidden_dim + tc::kM - 1) / tc::kM;
+    MegaArgs a{};
+    a.layers = stp->d_layers;
+    a.nlayers = le - lb;
+    a.rows = rows;
+    a.stages = stages;
+    a.H = c.hidden_dim;
+    a.qd = c.q_dim();
+    a.kvd = c.kv_dim();
+    a.F = c.ffn_dim;
+    a.hd = c.head_dim;
+    a.n_heads = c.n_heads;
+    a.n_kv = c.n_kv_heads;
+    a.max_len = c.max_seq_len;
+    a.eps = c.rms_eps;
+    a.h = ws.h;
+    a.q = ws.q;
+    a.att = ws.att;
+    a.act = ws.act;
+    a.ss_d = stp->ss;
+    a.ss_o = stp->ss + tilesH * tc::kRows;
+    a.pos = ws.pos;
+    a.rope_cos = e.rope_cos();
+    a.rope_sin = e.rope_sin();
+    a.prior = ws.meta;
+    a.row_off = ws.row_off;
+    a.runs = ws.runs;
+    a.partials = fast_partials(c, ws);
+    a.counters = fast_counters(c, ws);
+    a.bar = stp->bar;
+    a.status = ws.status;
+    {
+        const size_t kbH = c.hidden_dim / tc::kKB, kbQ = c.q_dim() / tc::kKB;
+        a.xim[P_QKV] = stp->xim;
+        a.xim[P_O] = a.xim[P_QKV] + kbH * tc::kBBytes;
+        a.xim[P_GU] = a.xim[P_O] + kbQ * tc::kBBytes;
+        a.xim[P_DOWN] = a.xim[P_GU] + kbH * tc::kBBytes;
+    }
+    if (mega_trace_enabled() && !stp->trace) {
+        const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(nsm) * kBarSlots * 8;
+        SFG_CUDA(cudaMalloc(&stp->trace, bytes));
+        SFG_CUDA(cudaMemset(stp->trace, 0, bytes));
+        SFG_CUDA(cudaDeviceSynchronize());
+    }
+    a.trace = mega_trace_enabled() ? stp->trace : nullptr;
+    void* args[] = {&a};
+    {
+        const double H = c.hidden_dim, qd = c.q_dim(), kvd = c.kv_dim(), F = c.ffn_dim, L = le - lb, R = rows;
+        const double bytes = L * 2.0 * (H * (qd + 2 * kvd) + qd * H + 2 * H * F + F * H) +
+                             L * 2.0 * 4.0 * kvd * (b.len() + rows) + 4.0 * R * H * 2;
+        const double flops = L * 2.0 * R * (H * (qd + 2 * kvd) + qd * H + 3 * H * F);
+        ProfScope ps(K_LAYERS, s, bytes, flops);
+        SFG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mega_kernel), dim3(nsm), dim3(kThreads), args, smem, s));
+    }
+    return 1;
+}
+
+}  // namespace sfg

@@ -12,7 +12,7 @@
 namespace sfg {
 
 enum KClass : int {
-    K_QKV = 0, K_ATTN, K_OPROJ, K_GATEUP, K_DOWN, K_NORM, K_HEAD, K_OTHER, K_NCLASS
+    K_QKV = 0, K_ATTN, K_OPROJ, K_GATEUP, K_DOWN, K_NORM, K_HEAD, K_OTHER, K_LAYERS, K_NCLASS
 };
 
 class KernelProfiler {

@@ -1,0 +1,70 @@
+"""Phase timeline of the FAST megakernel at the 7B shape (B200 dev tool).
+
+Per barrier id: when the CTAs passed the phase's input barrier (X start),
+finished building activation images (X done) and finished the phase
+(arrive), relative to the earliest CTA entry; median / max over CTAs."""
+import ctypes as C
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.getcwd())
+sys.path.insert(0, os.path.join(os.getcwd(), "oracle"))
+import paper_2602_16760_b200 as sfg
+import pyoracle as po
+from paper_2602_16760_b200 import _lib
+
+L = _lib.lib()
+NL = int(os.environ.get("NL", "6"))
+cfg = po.mistral7b_cfg()
+eng = sfg.Engine(sfg.ModelConfig(**{k: getattr(cfg, k) for k in po.ModelCfg.__dataclass_fields__}), math=sfg.FAST,
+                 layers=(2, 2 + NL), with_embedding=False, with_head=False)
+bank = eng.bank(2, 2 + NL)
+rng = np.random.default_rng(0)
+h = (rng.standard_normal((24, 4096)) * 0.5).astype(np.float32)
+eng.forward_layers(2, 2 + NL, h, list(range(24)), bank)
+bank.mark_committed(24)
+L.sfg_debug_mega_trace(1)
+h16 = (rng.standard_normal((16, 4096)) * 0.5).astype(np.float32)
+times = []
+for it in range(4):
+    bank.crop(24)
+    t0 = time.perf_counter()
+    eng.forward_layers(2, 2 + NL, h16, list(range(24, 40)), bank)
+    times.append(time.perf_counter() - t0)
+print("wall per forward (ms):", [round(t * 1000, 3) for t in times])
+G = 148
+tr = np.zeros(G * 256 * 8, dtype=np.uint64)
+L.sfg_debug_mega_trace_read(bank.h, tr.ctypes.data_as(C.POINTER(C.c_uint64)), tr.size)
+tr = tr.reshape(G, 256, 8).astype(np.int64)
+t0 = tr[:, 255, 0].min()
+names = {1: "QKV", 2: "ATTN", 3: "O", 4: "GU", 5: "DOWN"}
+print("kernel entry spread (us):", (tr[:, 255, 0].max() - t0) / 1000)
+print("stall columns: total wait (us, median/max over CTAs) of X-writer on empty, MMA on full, producer on empty")
+print(f"{'id':>4} {'phase':>5} {'xstart med/max':>18} {'xdone med/max':>18} {'arrive med/max':>18}"
+      f" {'xw-empty':>14} {'mma-full':>14} {'prod-empty':>14} {'last acc med/max':>18}")
+for bid in range(0, 1 + 5 * NL):
+    ph = "STAT" if bid == 0 else names[(bid - 1) % 5 + 1]
+    def col(k):
+        v = tr[:, bid, k]
+        v = v[v > 0]
+        if v.size == 0:
+            return "-"
+        return f"{(np.median(v) - t0) / 1000:8.1f}/{(v.max() - t0) / 1000:8.1f}"
+    def dur(k):
+        v = tr[:, bid, k]
+        if not v.any():
+            return "-"
+        return f"{np.median(v) / 1000:6.1f}/{v.max() / 1000:6.1f}"
+    print(f"{bid:4d} {ph:>5} {col(0):>18} {col(1):>18} {col(2):>18} {dur(3):>14} {dur(4):>14} {dur(5):>14}"
+          f" {col(6):>18}")
+# the latest CTAs of each phase of layer 1: last accumulator ready (slot 6 of
+# the phase's input barrier) vs arrival at the phase's output barrier
+phase_in = {1: 5, 3: 7, 4: 8, 5: 9}  # output barrier id -> input barrier id (layer 1)
+for out_id, in_id in ((6, 5), (8, 7), (9, 8), (10, 9)):
+    arr = tr[:, out_id, 2]
+    order = np.argsort(arr)[::-1][:6]
+    print(f"phase out {out_id} ({names[(out_id - 1) % 5 + 1]}): latest CTAs",
+          [(int(c), round((tr[c, in_id, 6] - t0) / 1000, 1), round((arr[c] - t0) / 1000, 1)) for c in order])
