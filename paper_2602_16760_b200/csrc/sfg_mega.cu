@@ -81,9 +81,11 @@ struct MegaArgs {
     int* counters;     // [tiles_max]
     unsigned* bar;     // per-barrier arrival counters + exit counter
     uint32_t* status;
+    int pf;            // L2 prefetch distance in weight units (0: off)
+    int evict_first;   // stream weights with an L2 evict-first policy
     uint8_t* xim[4];   // per phase: the GEMM's input as [KB][48 x 64] split bf16 images (put_split)
-    // optional [G][kBarSlots][8]: 0 X start, 1 X done, 2 arrive (globaltimer);
-    // 3/4/5 ns waited by X-writer (empty), MMA (full), producer (empty)
+    // optional [G][kBarSlots][kTraceW] (tools/trace_mega.py): per CTA and
+    // barrier id, globaltimer stamps and wait totals (see tslot users)
     unsigned long long* trace;
 };
 
@@ -91,6 +93,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+constexpr int kTraceW = 16;
+// slot k of (CTA c, barrier id): 0 X start, 1 X done, 2 arrive, 3/4/5 ns waited by
+// X loader (empty) / MMA (full) / producer (empty), 6 last accumulator ready,
+// 7 epilogue done; last fixup: 8 partials fenced, 9 counter, 10 loads, 11 epi_final
+__device__ __forceinline__ unsigned long long* tslot(const MegaArgs& a, int c, int id, int k) {
+    return a.trace + (static_cast<size_t>(c) * 256 + id) * kTraceW + k;
 }
 
 struct Geo {
@@ -224,6 +233,10 @@ __device__ __forceinline__ void put_split(uint8_t* img, int k, int r, float x) {
     *reinterpret_cast<__nv_bfloat16*>(blk + sw128_off(2 * kRows + r, kk)) = lb;
 }
 
+// per-launch constants staged in shared memory at kernel entry
+__shared__ int sh_pos[kRows];
+__shared__ int sh_prior;
+
 // ── epilogues (thread = feature m of the tile; y[r] for 16 rows) ─────────
 // RMSNorm is split across the two sides of the GEMM: the producing epilogue
 // stores split(h * gain) (gain is per input feature), and the consuming
@@ -241,16 +254,27 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int p, int tile
         const int fl = seg == 0 ? f : (seg == 1 ? f - a.qd : f - a.qd - a.kvd);
         const int d = fl % a.hd, half = a.hd >> 1, i = d >> 1;
         const bool odd = (m & 1) != 0;
-        const int prior = *a.prior;
+        const int prior = sh_prior;
+        // all table loads first (stores below could alias them and would
+        // otherwise serialise one L2 round trip per row)
+        float cs[kRows], sn[kRows];
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) {
+            cs[r] = 1.0f;
+            sn[r] = 0.0f;
+            if (valid && seg != 2 && r < a.rows) {
+                const size_t o = static_cast<size_t>(sh_pos[r]) * half + i;
+                cs[r] = __ldg(a.rope_cos + o);
+                sn[r] = __ldg(a.rope_sin + o);
+            }
+        }
 #pragma unroll
         for (int r = 0; r < kRows; ++r) {
             const float partner = __shfl_xor_sync(0xffffffffu, y[r], 1);
             if (!valid || r >= a.rows) continue;
             float v = y[r];
             if (seg != 2) {
-                const int ps = a.pos[r];
-                const float c = a.rope_cos[static_cast<size_t>(ps) * half + i];
-                const float s = a.rope_sin[static_cast<size_t>(ps) * half + i];
+                const float c = cs[r], s = sn[r];
                 v = odd ? __fadd_rn(__fmul_rn(partner, s), __fmul_rn(v, c))
                         : __fsub_rn(__fmul_rn(v, c), __fmul_rn(partner, s));
             }
@@ -291,12 +315,12 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int p, int tile
         const float gf = (gn && f < a.H) ? __ldg(gn + f) : 0.0f;
         float hn[kRows];
 #pragma unroll
+        for (int r = 0; r < kRows; ++r) hn[r] = (f < a.H && r < a.rows) ? __ldcg(a.h + static_cast<size_t>(r) * a.H + f) : 0.0f;
+#pragma unroll
         for (int r = 0; r < kRows; ++r) {
-            hn[r] = 0.0f;
             if (f < a.H && r < a.rows) {
-                float* o = a.h + static_cast<size_t>(r) * a.H + f;
-                hn[r] = __ldcg(o) + y[r];
-                *o = hn[r];
+                hn[r] += y[r];
+                a.h[static_cast<size_t>(r) * a.H + f] = hn[r];
                 if (gn) put_split(img, f, r, hn[r] * gf);
             }
         }
@@ -464,6 +488,41 @@ __device__ __forceinline__ void attention_dispatch(const MegaArgs& a, const Laye
     }
 }
 
+// A CTA's walk over its weight units: (layer, phase, unit) in stream order.
+struct Cursor {
+    int l, p;
+    long long u, en;
+};
+__device__ __forceinline__ void cursor_norm(const MegaArgs& a, int c, Cursor& k) {
+    while (k.l < a.nlayers && k.u >= k.en) {
+        if (++k.p == 4) {
+            k.p = 0;
+            ++k.l;
+        }
+        if (k.l >= a.nlayers) break;
+        long long st, en;
+        unit_range(geom(a, k.p), c, st, en);
+        k.u = st;
+        k.en = en;
+    }
+}
+__device__ __forceinline__ void cursor_begin(const MegaArgs& a, int c, Cursor& k) {
+    k.l = 0;
+    k.p = 0;
+    unit_range(geom(a, 0), c, k.u, k.en);
+    cursor_norm(a, c, k);
+}
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// prefetch the cursor's unit into L2 and advance
+__device__ __forceinline__ void cursor_prefetch_next(const MegaArgs& a, int c, Cursor& k) {
+    if (k.l >= a.nlayers) return;
+    prefetch_l2(a.layers[k.l].w[k.p] + static_cast<size_t>(k.u) * kABytes, kABytes);
+    ++k.u;
+    cursor_norm(a, c, k);
+}
+
 // ── the kernel ────────────────────────────────────────────────────────────
 // 10 warps, one CTA per SM: 3 warps share an SM sub-partition's 16K
 // registers, so 168 registers per thread is the ceiling
@@ -486,7 +545,9 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = gridDim.x, c = blockIdx.x;
-    if (threadIdx.x == 0 && a.trace) a.trace[(static_cast<size_t>(c) * kBarSlots + kBarSlots - 1) * 8] = gtimer();
+    if (threadIdx.x == 0 && a.trace) *tslot(a, c, kBarSlots - 1, 0) = gtimer();
+    if (threadIdx.x < kRows) sh_pos[threadIdx.x] = static_cast<int>(threadIdx.x) < a.rows ? a.pos[threadIdx.x] : 0;
+    if (threadIdx.x == 0) sh_prior = *a.prior;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 2);   // weight bytes + activation bytes (two expect_tx arrivals)
@@ -510,25 +571,34 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
         if (lane == 0) {  // ── weight producer
             int stage = 0;
             uint32_t ph = 0;
+            // L2 prefetch cursor a.pf units ahead of the copies: while the
+            // ring is full (grid barriers, attention, epilogue tails) HBM keeps
+            // streaming upcoming weights into L2
+            const uint64_t pol = l2_evict_first_policy();
+            Cursor pf{0, 0, 0, 0};
+            cursor_begin(a, c, pf);
+            for (int i = 0; i < a.pf; ++i) cursor_prefetch_next(a, c, pf);
             for (int l = 0; l < a.nlayers; ++l)
                 for (int p = 0; p < 4; ++p) {
                     const Geo g = geom(a, p);
                     const uint8_t* W = a.layers[l].w[p];
-                    const long long U = static_cast<long long>(g.tiles) * g.KB;
                     long long st, en;
-                (void)U;
-                unit_range(g, c, st, en);
+                    unit_range(g, c, st, en);
                     unsigned long long wacc = 0;
                     for (long long u = st; u < en; ++u) {
                         mwait_acc(&empty[stage], ph ^ 1, a.trace != nullptr, wacc);
                         mbar_expect_tx(&full[stage], kABytes);
-                        bulk_g2s(smem + stage * kStageBytes, W + static_cast<size_t>(u) * kABytes, kABytes, &full[stage]);
+                        if (a.evict_first)
+                            bulk_g2s_stream(smem + stage * kStageBytes, W + static_cast<size_t>(u) * kABytes, kABytes, &full[stage], pol);
+                        else
+                            bulk_g2s(smem + stage * kStageBytes, W + static_cast<size_t>(u) * kABytes, kABytes, &full[stage]);
+                        if (a.pf) cursor_prefetch_next(a, c, pf);
                         if (++stage == S) {
                             stage = 0;
                             ph ^= 1;
                         }
                     }
-                    if (a.trace) a.trace[(static_cast<size_t>(c) * kBarSlots + input_barrier(l, p)) * 8 + 5] = wacc;
+                    if (a.trace) *tslot(a, c, input_barrier(l, p), 5) = wacc;
                 }
         }
     } else if (warp == 1) {
@@ -570,7 +640,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         }
                         u = static_cast<long long>(t) * g.KB + hi;
                     }
-                    if (a.trace) a.trace[(static_cast<size_t>(c) * kBarSlots + input_barrier(l, p)) * 8 + 4] = wacc;
+                    if (a.trace) *tslot(a, c, input_barrier(l, p), 4) = wacc;
                 }
         }
     } else if (warp < 6) {  // ── epilogue warps 2..5 (+ attention)
@@ -646,6 +716,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
 #pragma unroll
                         for (int r = 0; r < kRows; ++r) slot[r * kM + m] = y[r];
                         __threadfence();
+                        if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 8) = gtimer();
                         named_sync(1, 128);
                         if (et == 0) {
                             const int old = atomicAdd(&a.counters[t], 1);
@@ -654,28 +725,43 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         }
                         named_sync(1, 128);
                         if (*flag) {
+                            if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 9) = gtimer();
                             __threadfence();
                             float s[kRows];
                             const float* p0 = a.partials + static_cast<size_t>(t) * kMaxPieces * kRows * kM;
+                            // pieces in k order; the loads of 4 pieces are in flight together
+                            for (int pc0 = 0; pc0 < n_pieces; pc0 += 4) {
+                                float t4[4][kRows];
 #pragma unroll
-                            for (int r = 0; r < kRows; ++r) s[r] = __ldcg(p0 + r * kM + m);
-                            for (int pc = 1; pc < n_pieces; ++pc)
+                                for (int j = 0; j < 4; ++j)
 #pragma unroll
-                                for (int r = 0; r < kRows; ++r)
-                                    s[r] = s[r] + __ldcg(p0 + (static_cast<size_t>(pc) * kRows + r) * kM + m);
+                                    for (int r = 0; r < kRows; ++r)
+                                        t4[j][r] = pc0 + j < n_pieces
+                                                       ? __ldcg(p0 + (static_cast<size_t>(pc0 + j) * kRows + r) * kM + m)
+                                                       : 0.0f;
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    if (pc0 + j >= n_pieces) break;
+#pragma unroll
+                                    for (int r = 0; r < kRows; ++r) s[r] = (pc0 + j == 0) ? t4[j][r] : s[r] + t4[j][r];
+                                }
+                            }
+                            if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 10) = gtimer();
                             epi_final(a, L, p, t, m, et, s, xch, rs);
+                            if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 11) = gtimer();
                         }
                         named_sync(1, 128);
                     }
                     u = static_cast<long long>(t) * g.KB + hi;
                 }
+                if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 7) = gtimer();
                 fence_proxy_async_global();
                 named_sync(1, 128);
                 if (et == 0) {
                     const int id = 5 * l + (p == P_QKV ? 1 : p + 2);
                     if (a.trace) {
-                        a.trace[(static_cast<size_t>(c) * kBarSlots + id) * 8 + 2] = gtimer();
-                        a.trace[(static_cast<size_t>(c) * kBarSlots + input_barrier(l, p)) * 8 + 6] = t_acc;
+                        *tslot(a, c, id, 2) = gtimer();
+                        *tslot(a, c, input_barrier(l, p), 6) = t_acc;
                     }
                     arrive_id(a.bar, id);
                 }
@@ -687,7 +773,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         attention_dispatch(a, L, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst, ocomb, cols);
                     named_sync(3, 256);
                     if (et == 0) {
-                        if (a.trace) a.trace[(static_cast<size_t>(c) * kBarSlots + 5 * l + 2) * 8 + 2] = gtimer();
+                        if (a.trace) *tslot(a, c, 5 * l + 2, 2) = gtimer();
                         arrive_id(a.bar, 5 * l + 2);
                     }
                 }
@@ -705,7 +791,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     // brings the unit's k-block of the prebuilt input image
                     wait_id(a.bar, input_barrier(l, p), G);
                     fence_proxy_async_global();
-                    if (a.trace) a.trace[(static_cast<size_t>(c) * kBarSlots + input_barrier(l, p)) * 8] = gtimer();
+                    if (a.trace) *tslot(a, c, input_barrier(l, p), 0) = gtimer();
                     const Geo g = geom(a, p);
                     long long st, en;
                     unit_range(g, c, st, en);
@@ -722,8 +808,8 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         }
                     }
                     if (a.trace) {
-                        a.trace[(static_cast<size_t>(c) * kBarSlots + input_barrier(l, p)) * 8 + 1] = gtimer();
-                        a.trace[(static_cast<size_t>(c) * kBarSlots + input_barrier(l, p)) * 8 + 3] = xwacc;
+                        *tslot(a, c, input_barrier(l, p), 1) = gtimer();
+                        *tslot(a, c, input_barrier(l, p), 3) = xwacc;
                     }
                 }
                 __syncwarp();
@@ -916,6 +1002,18 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     a.bar = stp->bar;
     a.status = ws.status;
     {
+        static const int pf_env = [] {
+            const char* v = getenv("SFG_MEGA_PF");
+            return v ? atoi(v) : 32;
+        }();
+        a.pf = pf_env;
+        static const int ef_env = [] {
+            const char* v = getenv("SFG_MEGA_EVICT_FIRST");
+            return v ? atoi(v) : 1;
+        }();
+        a.evict_first = ef_env;
+    }
+    {
         const size_t kbH = c.hidden_dim / tc::kKB, kbQ = c.q_dim() / tc::kKB;
         a.xim[P_QKV] = stp->xim;
         a.xim[P_O] = a.xim[P_QKV] + kbH * tc::kBBytes;
@@ -923,7 +1021,7 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         a.xim[P_DOWN] = a.xim[P_GU] + kbH * tc::kBBytes;
     }
     if (mega_trace_enabled() && !stp->trace) {
-        const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(nsm) * kBarSlots * 8;
+        const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(nsm) * kBarSlots * kTraceW;
         SFG_CUDA(cudaMalloc(&stp->trace, bytes));
         SFG_CUDA(cudaMemset(stp->trace, 0, bytes));
         SFG_CUDA(cudaDeviceSynchronize());

@@ -36,12 +36,13 @@ for it in range(4):
     times.append(time.perf_counter() - t0)
 print("wall per forward (ms):", [round(t * 1000, 3) for t in times])
 G = 148
-tr = np.zeros(G * 256 * 8, dtype=np.uint64)
+tr = np.zeros(G * 256 * 16, dtype=np.uint64)
 L.sfg_debug_mega_trace_read(bank.h, tr.ctypes.data_as(C.POINTER(C.c_uint64)), tr.size)
-tr = tr.reshape(G, 256, 8).astype(np.int64)
+tr = tr.reshape(G, 256, 16).astype(np.int64)
 t0 = tr[:, 255, 0].min()
 names = {1: "QKV", 2: "ATTN", 3: "O", 4: "GU", 5: "DOWN"}
 print("kernel entry spread (us):", (tr[:, 255, 0].max() - t0) / 1000)
+print(f"TOTAL layers {NL}: {(tr[:, 5 * NL, 2].max() - t0) / 1000:.1f} us")
 print("stall columns: total wait (us, median/max over CTAs) of X-writer on empty, MMA on full, producer on empty")
 print(f"{'id':>4} {'phase':>5} {'xstart med/max':>18} {'xdone med/max':>18} {'arrive med/max':>18}"
       f" {'xw-empty':>14} {'mma-full':>14} {'prod-empty':>14} {'last acc med/max':>18}")
@@ -66,5 +67,10 @@ phase_in = {1: 5, 3: 7, 4: 8, 5: 9}  # output barrier id -> input barrier id (la
 for out_id, in_id in ((6, 5), (8, 7), (9, 8), (10, 9)):
     arr = tr[:, out_id, 2]
     order = np.argsort(arr)[::-1][:6]
-    print(f"phase out {out_id} ({names[(out_id - 1) % 5 + 1]}): latest CTAs",
-          [(int(c), round((tr[c, in_id, 6] - t0) / 1000, 1), round((arr[c] - t0) / 1000, 1)) for c in order])
+    print(f"phase out {out_id} ({names[(out_id - 1) % 5 + 1]}): latest CTAs "
+          "(cta: last acc, fenced, counter, loads, epi_final, epi done, arrive)")
+    for c in order:
+        def ts(k, row=in_id):
+            v = tr[c, row, k]
+            return f"{(v - t0) / 1000:7.1f}" if v > 0 else "      -"
+        print(f"   {int(c):4d}:", " ".join(ts(k) for k in (6, 8, 9, 10, 11, 7)), ts(2, out_id))
