@@ -1,5 +1,7 @@
 #include "sfg_prof.h"
 
+#include <cstdio>
+
 namespace sfg {
 
 KernelProfiler& KernelProfiler::get() {
@@ -33,7 +35,9 @@ int KernelProfiler::begin(int cls, cudaStream_t s) {
     Slot& sl = slots_[idx];
     sl.used = true;
     sl.cls = cls;
-    cudaEventRecord(sl.a, s);
+    // inside stream capture an event record only becomes a graph node (and
+    // so timeable after replay) when recorded as an external event
+    cudaEventRecordWithFlags(sl.a, s, capture_ ? cudaEventRecordExternal : cudaEventRecordDefault);
     return idx;
 }
 
@@ -42,7 +46,7 @@ void KernelProfiler::end(int slot, cudaStream_t s, double bytes, double flops) {
     Slot& sl = slots_[slot];
     sl.bytes = bytes;
     sl.flops = flops;
-    cudaEventRecord(sl.b, s);
+    cudaEventRecordWithFlags(sl.b, s, capture_ ? cudaEventRecordExternal : cudaEventRecordDefault);
     if (capture_)
         capture_->push_back(slot);
     else
@@ -64,7 +68,16 @@ void KernelProfiler::collect_graph(const std::vector<int>& list) {
     for (int i : list) {
         Slot& sl = slots_[i];
         float ms = 0;
-        if (cudaEventElapsedTime(&ms, sl.a, sl.b) != cudaSuccess) continue;
+        const cudaError_t e = cudaEventElapsedTime(&ms, sl.a, sl.b);
+        if (e != cudaSuccess) {
+            // a failed query must not leak into the caller's cudaGetLastError()
+            cudaGetLastError();
+            if (!warned_) {
+                warned_ = true;
+                fprintf(stderr, "sfg profiler: graph event timing unavailable (%s)\n", cudaGetErrorString(e));
+            }
+            continue;
+        }
         count_[sl.cls] += 1;
         ms_[sl.cls] += ms;
         bytes_[sl.cls] += sl.bytes;
@@ -87,7 +100,11 @@ void KernelProfiler::collect() {
             continue;
         }
         float ms = 0;
-        cudaEventElapsedTime(&ms, sl.a, sl.b);
+        if (cudaEventElapsedTime(&ms, sl.a, sl.b) != cudaSuccess) {
+            cudaGetLastError();
+            sl.used = false;
+            continue;
+        }
         count_[sl.cls] += 1;
         ms_[sl.cls] += ms;
         bytes_[sl.cls] += sl.bytes;

@@ -43,6 +43,7 @@ private:
         bool used;
     };
     bool on_ = false;
+    bool warned_ = false;
     std::vector<int>* capture_ = nullptr;
     std::mutex mu_;
     std::vector<Slot> slots_;
