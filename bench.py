@@ -231,11 +231,15 @@ def run_ours(args, ws, rank, local):
     rng = np.random.default_rng(101 + rank)
     prompt = rng.integers(0, cfg.vocab_size, PROMPT_LEN).tolist()
     la = _lib.DecodeConfig(2, W, NG, G, 1 << 20)
-    pool = sfg.NGramPool(NG, 1 << 20)
-    seed_pool(_lib, pool, cfg.vocab_size, G, np.random.default_rng(7))
     total_steps = args.warmup + args.steps
+    pools = []
 
     def make_decoder(client):
+        # every decoder starts from an identically seeded pool, so the linked,
+        # frame (e2e) and RTT runs see the same acceptance sequence
+        pool = sfg.NGramPool(NG, 1 << 20)
+        seed_pool(_lib, pool, cfg.vocab_size, G, np.random.default_rng(7))
+        pools.append(pool)
         d = C.c_void_p()
         p = np.asarray(prompt, dtype=np.int32)
         _lib.check(L.sfg_decoder_create(client.h, C.byref(la), pool.h, p.ctypes.data_as(C.POINTER(C.c_int32)),

@@ -1004,7 +1004,7 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     {
         static const int pf_env = [] {
             const char* v = getenv("SFG_MEGA_PF");
-            return v ? atoi(v) : 32;
+            return v ? atoi(v) : 0;
         }();
         a.pf = pf_env;
         static const int ef_env = [] {
