@@ -94,44 +94,31 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+_GROUP = None
+
+
 def dist_setup():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    return ws, rank, local
+    """One process per GPU (torchrun env); replicas only, no data-path collective
+    (paper_2602_16760_b200/replicas.py)."""
+    global _GROUP
+    from paper_2602_16760_b200 import replicas
+    _GROUP = replicas.setup()
+    return _GROUP.world, _GROUP.rank, _GROUP.local
 
 
 def barrier_max(ws, local, x: float) -> float:
-    if ws == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2602_16760_b200 import replicas
+    return replicas.max_over_ranks(_GROUP, x)
 
 
 def barrier(ws, local):
-    if ws > 1:
-        import torch
-        import torch.distributed as dist
-        dist.barrier(device_ids=[local])
-        torch.cuda.synchronize(local)
+    from paper_2602_16760_b200 import replicas
+    replicas.barrier(_GROUP)
 
 
 def dist_sum(ws, local, x: float) -> float:
-    if ws == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    from paper_2602_16760_b200 import replicas
+    return replicas.sum_over_ranks(_GROUP, x)
 
 
 # ── CPU baseline: the reference's own forward_layers on the host ─────────
@@ -394,9 +381,8 @@ def main():
         run_reference(args, ws, rank)
     else:
         run_ours(args, ws, rank, local)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+    from paper_2602_16760_b200 import replicas
+    replicas.teardown(_GROUP)
 
 
 if __name__ == "__main__":

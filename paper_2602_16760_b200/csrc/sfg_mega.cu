@@ -953,7 +953,11 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
     const int group = c.n_heads / c.n_kv_heads;
-    int stages = kMaxStages;
+    static const int stages_cap = [] {
+        const char* v = getenv("SFG_MEGA_STAGES");  // dev knob: ring depth sensitivity
+        return v ? std::min(std::max(atoi(v), 2), kMaxStages) : kMaxStages;
+    }();
+    int stages = stages_cap;
     while (stages > 4 && smem_bytes(stages, c.head_dim, group, c.max_seq_len) > 227 * 1024) --stages;
     const size_t smem = smem_bytes(stages, c.head_dim, group, c.max_seq_len);
     static size_t configured = 0;
