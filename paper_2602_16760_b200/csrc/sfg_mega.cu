@@ -77,12 +77,17 @@ struct MegaArgs {
     const int32_t* prior;
     const int32_t* row_off;
     const MaskRun* runs;
-    float* partials;   // [tiles_max][kMaxPieces][16][128]
-    int* counters;     // [tiles_max]
+    float* partials;   // 2 x [tiles_max][kMaxPieces][16][128] (by phase parity)
+    int* counters;     // 2 x [tiles_max]
+    size_t part_stride;  // floats between the two partial buffers
+    int cnt_stride;      // ints between the two counter arrays
+    unsigned* flags;   // dataflow completion flags (see fptr), zeroed by the last CTA out
+    int nflags;
     unsigned* bar;     // per-barrier arrival counters + exit counter
     uint32_t* status;
     int pf;            // L2 prefetch distance in weight units (0: off)
     int evict_first;   // stream weights with an L2 evict-first policy
+    int spin_mma;      // dev knob: MMA issuer spins on test_wait instead of try_wait
     uint8_t* xim[4];   // per phase: the GEMM's input as [KB][48 x 64] split bf16 images (put_split)
     // optional [G][kBarSlots][kTraceW] (tools/trace_mega.py): per CTA and
     // barrier id, globaltimer stamps and wait totals (see tslot users)
@@ -168,6 +173,62 @@ __device__ __forceinline__ int input_barrier(int layer, int p) {
         case P_O: return 5 * layer + 2;
         case P_GU: return 5 * layer + 3;
         default: return 5 * layer + 4;
+    }
+}
+
+// ── dataflow completion flags (replace grid barriers between phases) ─────
+// A consumer waits only for the producer tiles its own units need: the
+// activation loader for the k-blocks of its range, attention for the 6 QKV
+// tiles of its kv head, and the RMSNorm scale for "all tiles of the
+// producing phase" (a per-phase tile counter).  Kinds: statistics of the
+// input rows (layer -1), then per layer QKV tiles, attention kv heads, O, gate|up, down.
+enum FlagKind : int { K_STATS = 0, K_QKV, K_ATT, K_O, K_GU, K_DOWN };
+__device__ __forceinline__ int kind_tiles(const MegaArgs& a, int k) {
+    switch (k) {
+        case K_QKV: return (a.qd + 2 * a.kvd + kM - 1) / kM;
+        case K_ATT: return a.n_kv;
+        case K_GU: return a.F / 64;
+        default: return (a.H + kM - 1) / kM;  // stats, O, down: 128-feature tiles of H
+    }
+}
+// flag of tile t (t == kind_tiles: the kind's completed-tile counter)
+__device__ __forceinline__ unsigned* fptr(const MegaArgs& a, int l, int k, int t) {
+    const int tH = kind_tiles(a, K_STATS);
+    if (k == K_STATS) return a.flags + t;
+    int off = tH + 1;
+    int lay = 0;
+    for (int j = K_QKV; j <= K_DOWN; ++j) lay += kind_tiles(a, j) + 1;
+    off += l * lay;
+    for (int j = K_QKV; j < k; ++j) off += kind_tiles(a, j) + 1;
+    return a.flags + off + t;
+}
+__device__ __forceinline__ void red_add(unsigned* f, unsigned v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+__device__ __forceinline__ void signal_add(unsigned* f, unsigned v) {
+    __threadfence();
+    atomicAdd(f, v);
+}
+__device__ __forceinline__ void wait_ge(const unsigned* f, unsigned v) {
+    unsigned long long spins = 0;
+    while (ld_acquire(f) < v) {
+        __nanosleep(32);
+        if (++spins > (1ull << 27)) asm volatile("trap;");  // never hang the GPU
+    }
+}
+// is the input k-block kb of phase p (layer l) produced?  (acquire load)
+__device__ __forceinline__ bool xblock_ready(const MegaArgs& a, int l, int p, int kb) {
+    switch (p) {
+        case P_QKV: return ld_acquire(l == 0 ? fptr(a, 0, K_STATS, kb >> 1) : fptr(a, l - 1, K_DOWN, kb >> 1)) >= 1u;
+        case P_O: {
+            const int group = a.n_heads / a.n_kv;
+            const int h0 = (kb * kKB) / a.hd / group, h1 = (kb * kKB + kKB - 1) / a.hd / group;
+            for (int h = h0; h <= h1; ++h)
+                if (ld_acquire(fptr(a, l, K_ATT, h)) < static_cast<unsigned>(a.rows)) return false;
+            return true;
+        }
+        case P_GU: return ld_acquire(fptr(a, l, K_O, kb >> 1)) >= 1u;
+        default: return ld_acquire(fptr(a, l, K_GU, kb)) >= 1u;
     }
 }
 
@@ -470,9 +531,20 @@ __device__ void attention_item(const MegaArgs& a, const LayerDesc& L, int row, i
     named_sync(3, 256);
 }
 
-__device__ __forceinline__ void attention_dispatch(const MegaArgs& a, const LayerDesc& L, int row, int kvh, int at,
-                                                   float* qs, float* wst, float* ocomb, int* cols) {
+__device__ __forceinline__ void attention_dispatch(const MegaArgs& a, const LayerDesc& L, int l, int row, int kvh,
+                                                   int at, float* qs, float* wst, float* ocomb, int* cols) {
     const int group = a.n_heads / a.n_kv;
+    {  // wait for this kv head's QKV tiles: its q heads, K and V
+        const int q0 = kvh * group * a.hd / kM, q1 = ((kvh + 1) * group * a.hd - 1) / kM;
+        const int kt = (a.qd + kvh * a.hd) / kM, kt1 = (a.qd + kvh * a.hd + a.hd - 1) / kM;
+        const int vt = (a.qd + a.kvd + kvh * a.hd) / kM, vt1 = (a.qd + a.kvd + kvh * a.hd + a.hd - 1) / kM;
+        const int nq = q1 - q0 + 1, nk = kt1 - kt + 1, nv = vt1 - vt + 1;
+        if (at < nq + nk + nv) {
+            const int t = at < nq ? q0 + at : (at < nq + nk ? kt + at - nq : vt + at - nq - nk);
+            wait_ge(fptr(a, l, K_QKV, t), 1u);
+        }
+        named_sync(3, 256);
+    }
     if (group <= 4) {
         switch (a.hd) {
             case 64: attention_item<64, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
@@ -486,6 +558,7 @@ __device__ __forceinline__ void attention_dispatch(const MegaArgs& a, const Laye
             default: attention_item<32, 8>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
         }
     }
+    if (at == 0) signal_add(fptr(a, l, K_ATT, kvh), 1u);  // item's att rows + image are published
 }
 
 // A CTA's walk over its weight units: (layer, phase, unit) in stream order.
@@ -621,7 +694,13 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         tc_fence_after();
                         const uint32_t d = tmem + acc * kAccCols;
                         for (int kb = lo; kb < hi; ++kb) {
-                            mwait_acc(&full[stage], ph, a.trace != nullptr, wacc);
+                            if (a.spin_mma) {
+                                unsigned long long sp = 0;
+                                while (!mbar_test(&full[stage], ph))
+                                    if (++sp > (1ull << 30)) asm volatile("trap;");
+                            } else {
+                                mwait_acc(&full[stage], ph, a.trace != nullptr, wacc);
+                            }
                             tc_fence_after();
                             const uint32_t sa = smem_u32(smem + stage * kStageBytes);
                             const uint64_t da = smem_desc(sa), db = smem_desc(sa + kABytes);
@@ -657,21 +736,33 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                 if (f < a.H && r < a.rows) put_split(a.xim[P_QKV], f, r, hv[r] * gf);
             }
             tile_sumsq(hv, xch + 64 * kRows, a.ss_d + static_cast<size_t>(t) * kRows, et);
+            fence_proxy_async_global();
+            named_sync(1, 128);
+            if (et == 0) {
+                __threadfence();
+                red_add(fptr(a, 0, K_STATS, t), 1u);
+                red_add(fptr(a, 0, K_STATS, tilesH), 1u);
+            }
         }
-        fence_proxy_async_global();
-        named_sync(1, 128);
-        if (et == 0) arrive_id(a.bar, 0);
+        if (a.trace && et == 0) *tslot(a, c, 0, 2) = gtimer();
         int acc = 0;
         uint32_t acc_ph = 0;
+        int gp = 0;  // running phase index: stream-K partial buffers alternate by its parity
         for (int l = 0; l < a.nlayers; ++l) {
             const LayerDesc& L = a.layers[l];
-            for (int p = 0; p < 4; ++p) {
+            for (int p = 0; p < 4; ++p, ++gp) {
                 const Geo g = geom(a, p);
                 const long long U = static_cast<long long>(g.tiles) * g.KB;
+                const int kind = K_QKV + (p == P_QKV ? 0 : p + 1);
+                float* parts = a.partials + (gp & 1) * a.part_stride;
+                int* cnts = a.counters + (gp & 1) * a.cnt_stride;
                 long long st, en;
                 unit_range(g, c, st, en);
-                if ((p == P_QKV || p == P_GU) && st < en) {  // per-row 1/rms from the ss partials
-                    if (et == 0) wait_id(a.bar, input_barrier(l, p), G);
+                if ((p == P_QKV || p == P_GU) && st < en) {  // per-row 1/rms: needs every producer tile
+                    if (et == 0)
+                        wait_ge(p == P_QKV ? (l == 0 ? fptr(a, 0, K_STATS, tilesH) : fptr(a, l - 1, K_DOWN, tilesH))
+                                           : fptr(a, l, K_O, tilesH),
+                                static_cast<unsigned>(tilesH));
                     named_sync(1, 128);
                     if (et < kRows) {
                         const float* ssb = p == P_QKV ? a.ss_d : a.ss_o;
@@ -705,30 +796,32 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     float y[kRows];
 #pragma unroll
                     for (int r = 0; r < kRows; ++r) y[r] = (v[r] + v[kRows + r]) + v[2 * kRows + r];
+                    bool done_tile = false;
                     if (lo == 0 && hi == g.KB) {
                         epi_final(a, L, p, t, m, et, y, xch, rs);
+                        done_tile = true;
                     } else {  // stream-K fixup: last arriver sums the pieces in k order
                         const long long first_u = static_cast<long long>(t) * g.KB;
                         const int c_first = static_cast<int>(((first_u + 1) * g.G - 1) / U);
                         const int piece = c - c_first;
                         const int n_pieces = static_cast<int>(((first_u + g.KB) * g.G - 1) / U) - c_first + 1;
-                        float* slot = a.partials + (static_cast<size_t>(t) * kMaxPieces + piece) * kRows * kM;
+                        float* slot = parts + (static_cast<size_t>(t) * kMaxPieces + piece) * kRows * kM;
 #pragma unroll
                         for (int r = 0; r < kRows; ++r) slot[r * kM + m] = y[r];
                         __threadfence();
                         if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 8) = gtimer();
                         named_sync(1, 128);
                         if (et == 0) {
-                            const int old = atomicAdd(&a.counters[t], 1);
+                            const int old = atomicAdd(&cnts[t], 1);
                             *flag = (old == n_pieces - 1) ? 1 : 0;
-                            if (old == n_pieces - 1) a.counters[t] = 0;
+                            if (old == n_pieces - 1) cnts[t] = 0;
                         }
                         named_sync(1, 128);
                         if (*flag) {
                             if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 9) = gtimer();
                             __threadfence();
-                            float s[kRows];
-                            const float* p0 = a.partials + static_cast<size_t>(t) * kMaxPieces * kRows * kM;
+                            float sacc[kRows];
+                            const float* p0 = parts + static_cast<size_t>(t) * kMaxPieces * kRows * kM;
                             // pieces in k order; the loads of 4 pieces are in flight together
                             for (int pc0 = 0; pc0 < n_pieces; pc0 += 4) {
                                 float t4[4][kRows];
@@ -743,86 +836,100 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                                 for (int j = 0; j < 4; ++j) {
                                     if (pc0 + j >= n_pieces) break;
 #pragma unroll
-                                    for (int r = 0; r < kRows; ++r) s[r] = (pc0 + j == 0) ? t4[j][r] : s[r] + t4[j][r];
+                                    for (int r = 0; r < kRows; ++r) sacc[r] = (pc0 + j == 0) ? t4[j][r] : sacc[r] + t4[j][r];
                                 }
                             }
                             if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 10) = gtimer();
-                            epi_final(a, L, p, t, m, et, s, xch, rs);
+                            epi_final(a, L, p, t, m, et, sacc, xch, rs);
                             if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 11) = gtimer();
+                            done_tile = true;
                         }
+                    }
+                    if (done_tile) {  // publish the tile: outputs, next input image, ss partials
+                        fence_proxy_async_global();
+                        named_sync(1, 128);
+                        if (et == 0) {  // one fence publishes both the tile flag and the phase count
+                            __threadfence();
+                            red_add(fptr(a, l, kind, t), 1u);
+                            red_add(fptr(a, l, kind, g.tiles), 1u);
+                        }
+                    } else {
                         named_sync(1, 128);
                     }
                     u = static_cast<long long>(t) * g.KB + hi;
                 }
-                if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 7) = gtimer();
-                fence_proxy_async_global();
-                named_sync(1, 128);
-                if (et == 0) {
+                if (a.trace && et == 0) {
                     const int id = 5 * l + (p == P_QKV ? 1 : p + 2);
-                    if (a.trace) {
-                        *tslot(a, c, id, 2) = gtimer();
-                        *tslot(a, c, input_barrier(l, p), 6) = t_acc;
-                    }
-                    arrive_id(a.bar, id);
+                    *tslot(a, c, input_barrier(l, p), 7) = gtimer();
+                    *tslot(a, c, id, 2) = gtimer();
+                    *tslot(a, c, input_barrier(l, p), 6) = t_acc;
                 }
-                if (p == P_QKV) {  // attention phase, shared with the activation warps
-                    if (et == 0) wait_id(a.bar, 5 * l + 1, G);
-                    named_sync(1, 128);
-                    __threadfence();
+                if (p == P_QKV) {  // attention, shared with the activation warps
                     for (int it = c; it < a.rows * a.n_kv; it += G)
-                        attention_dispatch(a, L, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst, ocomb, cols);
-                    named_sync(3, 256);
-                    if (et == 0) {
-                        if (a.trace) *tslot(a, c, 5 * l + 2, 2) = gtimer();
-                        arrive_id(a.bar, 5 * l + 2);
-                    }
+                        attention_dispatch(a, L, l, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst, ocomb, cols);
+                    if (a.trace && et == 0) *tslot(a, c, 5 * l + 2, 2) = gtimer();
                 }
             }
         }
-    } else {  // ── activation loader (warp 6 lane 0) + attention (warps 6..9)
+    } else {  // ── activation loader (warp 6) + attention (warps 6..9)
         const int xt = threadIdx.x - 192;
         int stage = 0;
         uint32_t ph = 0;
         for (int l = 0; l < a.nlayers; ++l) {
             const LayerDesc& L = a.layers[l];
             for (int p = 0; p < 4; ++p) {
-                if (xt == 0) {
-                    // after the phase's input barrier, one bulk copy per stage
-                    // brings the unit's k-block of the prebuilt input image
-                    wait_id(a.bar, input_barrier(l, p), G);
-                    fence_proxy_async_global();
-                    if (a.trace) *tslot(a, c, input_barrier(l, p), 0) = gtimer();
+                if (warp == 6) {
+                    // one bulk copy per stage of the unit's k-block of the prebuilt
+                    // input image, as soon as the producer tiles of that block are
+                    // published (the 32 lanes poll the next 32 units' flags at once)
                     const Geo g = geom(a, p);
                     long long st, en;
                     unit_range(g, c, st, en);
                     const uint8_t* X = a.xim[p];
                     unsigned long long xwacc = 0;
+                    long long ready = st;
+                    bool first = true;
                     for (long long u = st; u < en; ++u) {
-                        mwait_acc(&empty[stage], ph ^ 1, a.trace != nullptr, xwacc);
-                        mbar_expect_tx(&full[stage], kBBytes);
-                        bulk_g2s(smem + stage * kStageBytes + kABytes, X + static_cast<size_t>(u % g.KB) * kBBytes,
-                                 kBBytes, &full[stage]);
+                        if (u >= ready) {
+                            unsigned long long spins = 0;
+                            while (u >= ready) {
+                                const long long uu = ready + lane;
+                                const bool ok = uu >= en || xblock_ready(a, l, p, static_cast<int>(uu % g.KB));
+                                const unsigned mk = __ballot_sync(0xffffffffu, ok);
+                                const int k = mk == 0xffffffffu ? 32 : __ffs(~mk) - 1;
+                                ready += k;
+                                if (k == 0) {
+                                    __nanosleep(32);
+                                    if (++spins > (1ull << 27)) asm volatile("trap;");
+                                }
+                            }
+                            if (lane == 0) fence_proxy_async_global();
+                            if (first && a.trace && lane == 0) *tslot(a, c, input_barrier(l, p), 0) = gtimer();
+                            first = false;
+                        }
+                        if (lane == 0) {
+                            mwait_acc(&empty[stage], ph ^ 1, a.trace != nullptr, xwacc);
+                            mbar_expect_tx(&full[stage], kBBytes);
+                            bulk_g2s(smem + stage * kStageBytes + kABytes, X + static_cast<size_t>(u % g.KB) * kBBytes,
+                                     kBBytes, &full[stage]);
+                        }
                         if (++stage == S) {
                             stage = 0;
                             ph ^= 1;
                         }
                     }
-                    if (a.trace) {
+                    if (a.trace && lane == 0) {
                         *tslot(a, c, input_barrier(l, p), 1) = gtimer();
                         *tslot(a, c, input_barrier(l, p), 3) = xwacc;
                     }
+                    __syncwarp();
                 }
-                __syncwarp();
-                if (p == P_QKV) {  // join the attention phase
-                    if (xt == 0) wait_id(a.bar, 5 * l + 1, G);
-                    named_sync(2, 128);
-                    __threadfence();
+                if (p == P_QKV)  // join the attention phase
                     for (int it = c; it < a.rows * a.n_kv; it += G)
-                        attention_dispatch(a, L, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst, ocomb, cols);
-                    named_sync(3, 256);
-                }
+                        attention_dispatch(a, L, l, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst, ocomb, cols);
             }
         }
+        (void)xt;
     }
     tc_fence_before();
     __syncthreads();
@@ -830,12 +937,18 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
         tc_fence_after();
         tmem_free(tmem, kTmemCols);
     }
-    if (threadIdx.x == 0) {  // last CTA out resets the barrier for the next launch
+    // last CTA out resets the dataflow flags and the exit counter for the next launch
+    if (threadIdx.x == 0) {
         __threadfence();
-        const unsigned prev = atomicAdd(a.bar + kBarSlots, 1u);
-        if (prev == static_cast<unsigned>(G) - 1) {
-            const int nbar = 1 + 5 * a.nlayers;
-            for (int i = 0; i < nbar; ++i) atomicExch(a.bar + i, 0u);
+        *flag = atomicAdd(a.bar + kBarSlots, 1u) == static_cast<unsigned>(G) - 1 ? 1 : 0;
+    }
+    __syncthreads();
+    if (*flag) {
+        __threadfence();
+        for (int i = threadIdx.x; i < a.nflags; i += blockDim.x) a.flags[i] = 0u;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
             atomicExch(a.bar + kBarSlots, 0u);
         }
     }
@@ -873,12 +986,20 @@ struct MegaState {
     float* ss = nullptr;
     unsigned long long* trace = nullptr;
     uint8_t* xim = nullptr;  // the four phases' input images, back to back
+    float* partials = nullptr;  // 2 parity buffers of stream-K partials
+    int* counters = nullptr;    // 2 parity arrays of per-tile arrival counters
+    unsigned* flags = nullptr;  // dataflow completion flags
+    size_t part_stride = 0;
+    int cnt_stride = 0, nflags = 0;
     ~MegaState() {
         if (d_layers) cudaFree(d_layers);
         if (bar) cudaFree(bar);
         if (ss) cudaFree(ss);
         if (trace) cudaFree(trace);
         if (xim) cudaFree(xim);
+        if (partials) cudaFree(partials);
+        if (counters) cudaFree(counters);
+        if (flags) cudaFree(flags);
     }
 };
 }  // namespace
@@ -941,6 +1062,21 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         SFG_CUDA(cudaMalloc(&st.ss, sizeof(float) * 2 * tilesH * tc::kRows));
         const size_t xblocks = static_cast<size_t>(2 * c.hidden_dim + c.q_dim() + c.ffn_dim) / tc::kKB;
         SFG_CUDA(cudaMalloc(&st.xim, xblocks * tc::kBBytes));
+        {
+            const int tQ = (c.q_dim() + 2 * c.kv_dim() + tc::kM - 1) / tc::kM, tG = c.ffn_dim / 64;
+            const int tiles_max = std::max(std::max(tQ, tG), tilesH);
+            st.part_stride = static_cast<size_t>(tiles_max) * kMaxPieces * tc::kRows * tc::kM;
+            st.cnt_stride = tiles_max;
+            SFG_CUDA(cudaMalloc(&st.partials, sizeof(float) * 2 * st.part_stride));
+            SFG_CUDA(cudaMalloc(&st.counters, sizeof(int) * 2 * st.cnt_stride));
+            SFG_CUDA(cudaMemset(st.counters, 0, sizeof(int) * 2 * st.cnt_stride));
+            // must match fptr(): stats tiles + counter, then per layer
+            // (QKV, attention kv heads, O, gate|up, down) tiles + counter each
+            const int lay = (tQ + 1) + (c.n_kv_heads + 1) + (tilesH + 1) + (tG + 1) + (tilesH + 1);
+            st.nflags = tilesH + 1 + (le - lb) * lay;
+            SFG_CUDA(cudaMalloc(&st.flags, sizeof(unsigned) * st.nflags));
+            SFG_CUDA(cudaMemset(st.flags, 0, sizeof(unsigned) * st.nflags));
+        }
         SFG_CUDA(cudaMemset(st.xim, 0, xblocks * tc::kBBytes));
         SFG_CUDA(cudaDeviceSynchronize());
         b.mega = holder;
@@ -1001,8 +1137,12 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     a.prior = ws.meta;
     a.row_off = ws.row_off;
     a.runs = ws.runs;
-    a.partials = fast_partials(c, ws);
-    a.counters = fast_counters(c, ws);
+    a.partials = stp->partials;
+    a.counters = stp->counters;
+    a.part_stride = stp->part_stride;
+    a.cnt_stride = stp->cnt_stride;
+    a.flags = stp->flags;
+    a.nflags = stp->nflags;
     a.bar = stp->bar;
     a.status = ws.status;
     {
@@ -1016,6 +1156,11 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
             return v ? atoi(v) : 1;
         }();
         a.evict_first = ef_env;
+        static const int spin_env = [] {
+            const char* v = getenv("SFG_MEGA_SPIN");
+            return v ? atoi(v) : 0;
+        }();
+        a.spin_mma = spin_env;
     }
     {
         const size_t kbH = c.hidden_dim / tc::kKB, kbQ = c.q_dim() / tc::kKB;
