@@ -294,6 +294,12 @@ __device__ __forceinline__ void put_split(uint8_t* img, int k, int r, float x) {
     *reinterpret_cast<__nv_bfloat16*>(blk + sw128_off(2 * kRows + r, kk)) = lb;
 }
 
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // per-launch constants staged in shared memory at kernel entry
 __shared__ int sh_pos[kRows];
 __shared__ int sh_prior;
@@ -304,7 +310,8 @@ __shared__ int sh_prior;
 // epilogue scales its accumulator by the per-row 1/rms (rs[r]), which needs
 // the whole row's sum of squares and so is only known after the barrier.
 __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int p, int tile, int m, int et,
-                          const float (&yin)[kRows], float* xch, const float* rs) {
+                          const float (&yin)[kRows], float* xch, const float* rs, const float* ropeT,
+                          const float* hpre) {
     float y[kRows];
 #pragma unroll
     for (int r = 0; r < kRows; ++r) y[r] = (p == P_QKV || p == P_GU) ? yin[r] * rs[r] : yin[r];
@@ -316,18 +323,12 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int p, int tile
         const int d = fl % a.hd, half = a.hd >> 1, i = d >> 1;
         const bool odd = (m & 1) != 0;
         const int prior = sh_prior;
-        // all table loads first (stores below could alias them and would
-        // otherwise serialise one L2 round trip per row)
+        // the rows' cos/sin were staged in shared memory at kernel entry
         float cs[kRows], sn[kRows];
 #pragma unroll
         for (int r = 0; r < kRows; ++r) {
-            cs[r] = 1.0f;
-            sn[r] = 0.0f;
-            if (valid && seg != 2 && r < a.rows) {
-                const size_t o = static_cast<size_t>(sh_pos[r]) * half + i;
-                cs[r] = __ldg(a.rope_cos + o);
-                sn[r] = __ldg(a.rope_sin + o);
-            }
+            cs[r] = ropeT[r * a.hd + i];
+            sn[r] = ropeT[r * a.hd + half + i];
         }
 #pragma unroll
         for (int r = 0; r < kRows; ++r) {
@@ -374,9 +375,12 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int p, int tile
         const float* gn = p == P_O ? L.ffn_norm : L.next_attn_norm;
         uint8_t* img = p == P_O ? a.xim[P_GU] : a.xim[P_QKV];
         const float gf = (gn && f < a.H) ? __ldg(gn + f) : 0.0f;
+        // residual rows were prefetched into shared memory (cp.async) while
+        // the accumulator was still being produced
+        cp_async_wait_all();
         float hn[kRows];
 #pragma unroll
-        for (int r = 0; r < kRows; ++r) hn[r] = (f < a.H && r < a.rows) ? __ldcg(a.h + static_cast<size_t>(r) * a.H + f) : 0.0f;
+        for (int r = 0; r < kRows; ++r) hn[r] = (f < a.H && r < a.rows) ? hpre[r * kM + m] : 0.0f;
 #pragma unroll
         for (int r = 0; r < kRows; ++r) {
             if (f < a.H && r < a.rows) {
@@ -615,11 +619,22 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
     float* wst = qs + kMaxGroup * a.hd;                        // [8][kMaxGroup][2]
     float* ocomb = wst + 8 * kMaxGroup * 2;                    // [8][group][hd]
     int* cols = reinterpret_cast<int*>(ocomb + 8 * (a.n_heads / a.n_kv) * a.hd);  // [max_len]
+    float* ropeT = reinterpret_cast<float*>(cols + a.max_len);  // [16][hd]: cos | sin of the rows' positions
+    float* hpre = ropeT + kRows * a.hd;                         // [16][128] residual prefetch
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = gridDim.x, c = blockIdx.x;
     if (threadIdx.x == 0 && a.trace) *tslot(a, c, kBarSlots - 1, 0) = gtimer();
     if (threadIdx.x < kRows) sh_pos[threadIdx.x] = static_cast<int>(threadIdx.x) < a.rows ? a.pos[threadIdx.x] : 0;
+    for (int i = threadIdx.x; i < kRows * a.hd; i += blockDim.x) {  // RoPE table rows (host-libm values)
+        const int r = i / a.hd, j = i % a.hd, half = a.hd >> 1;
+        float v = j < half ? 1.0f : 0.0f;
+        if (r < a.rows) {
+            const size_t o = static_cast<size_t>(a.pos[r]) * half + (j < half ? j : j - half);
+            v = j < half ? a.rope_cos[o] : a.rope_sin[o];
+        }
+        ropeT[i] = v;
+    }
     if (threadIdx.x == 0) sh_prior = *a.prior;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -772,11 +787,25 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     }
                     named_sync(1, 128);
                 }
+                if ((p == P_O || p == P_DOWN) && st < en) {  // residual rows of this phase are final
+                    if (et == 0) {
+                        if (p == P_DOWN) wait_ge(fptr(a, l, K_O, tilesH), static_cast<unsigned>(tilesH));
+                        else if (l > 0) wait_ge(fptr(a, l - 1, K_DOWN, tilesH), static_cast<unsigned>(tilesH));
+                    }
+                    named_sync(1, 128);
+                }
                 unsigned long long t_acc = 0;
                 for (long long u = st; u < en;) {
                     const int t = static_cast<int>(u / g.KB);
                     const int lo = static_cast<int>(u - static_cast<long long>(t) * g.KB);
                     const int hi = static_cast<int>(min(en - static_cast<long long>(t) * g.KB, static_cast<long long>(g.KB)));
+                    if (p == P_O || p == P_DOWN) {  // prefetch this tile's residual rows while the MMA runs
+                        cp_async_wait_all();   // a previous (unused) prefetch must not land late
+                        const int f = t * kM + m;
+                        if (f < a.H)
+                            for (int r = 0; r < a.rows; ++r) cp_async4(hpre + r * kM + m, a.h + static_cast<size_t>(r) * a.H + f);
+                        cp_async_commit();
+                    }
                     mwait(&tfull[acc], acc_ph);
                     if (a.trace && et == 0) t_acc = gtimer();
                     tc_fence_after();
@@ -798,7 +827,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     for (int r = 0; r < kRows; ++r) y[r] = (v[r] + v[kRows + r]) + v[2 * kRows + r];
                     bool done_tile = false;
                     if (lo == 0 && hi == g.KB) {
-                        epi_final(a, L, p, t, m, et, y, xch, rs);
+                        epi_final(a, L, p, t, m, et, y, xch, rs, ropeT, hpre);
                         done_tile = true;
                     } else {  // stream-K fixup: last arriver sums the pieces in k order
                         const long long first_u = static_cast<long long>(t) * g.KB;
@@ -840,7 +869,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                                 }
                             }
                             if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 10) = gtimer();
-                            epi_final(a, L, p, t, m, et, sacc, xch, rs);
+                            epi_final(a, L, p, t, m, et, sacc, xch, rs, ropeT, hpre);
                             if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 11) = gtimer();
                             done_tile = true;
                         }
@@ -956,7 +985,8 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
 
 size_t smem_bytes(int stages, int hd, int group, int max_len) {
     return 1024 + static_cast<size_t>(stages) * kStageBytes + (2 * kMaxStages + 4) * 8 + 32 +
-           sizeof(float) * (64 * kRows + 5 * kRows + kMaxGroup * hd + 8 * kMaxGroup * 2 + 8 * group * hd) +
+           sizeof(float) * (64 * kRows + 5 * kRows + kMaxGroup * hd + 8 * kMaxGroup * 2 + 8 * group * hd +
+                            kRows * hd + kRows * kM) +
            sizeof(int) * static_cast<size_t>(max_len);
 }
 
