@@ -300,9 +300,12 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// per-launch constants staged in shared memory at kernel entry
+// per-launch constants staged in shared memory at kernel entry (the layer
+// table too: the epilogue dereferences it on the critical path of every tile)
+constexpr int kMaxMegaLayers = 64;
 __shared__ int sh_pos[kRows];
 __shared__ int sh_prior;
+__shared__ LayerDesc sh_layers[kMaxMegaLayers];
 
 // ── epilogues (thread = feature m of the tile; y[r] for 16 rows) ─────────
 // RMSNorm is split across the two sides of the GEMM: the producing epilogue
@@ -374,7 +377,8 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int p, int tile
         // or of the next layer's attn_norm (after down; none after the last)
         const float* gn = p == P_O ? L.ffn_norm : L.next_attn_norm;
         uint8_t* img = p == P_O ? a.xim[P_GU] : a.xim[P_QKV];
-        const float gf = (gn && f < a.H) ? __ldg(gn + f) : 0.0f;
+        cp_async_wait_all();
+        const float gf = (gn && f < a.H) ? hpre[kRows * kM + m] : 0.0f;  // prefetched with the residual
         // residual rows were prefetched into shared memory (cp.async) while
         // the accumulator was still being produced
         cp_async_wait_all();
@@ -636,6 +640,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
         ropeT[i] = v;
     }
     if (threadIdx.x == 0) sh_prior = *a.prior;
+    for (int i = threadIdx.x; i < a.nlayers; i += blockDim.x) sh_layers[i] = a.layers[i];
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 2);   // weight bytes + activation bytes (two expect_tx arrivals)
@@ -743,7 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
         // and the first QKV GEMM's input image split(h * attn_norm)
         for (int t = c; t < tilesH; t += G) {
             const int f = t * kM + m;
-            const float gf = f < a.H ? __ldg(a.layers[0].attn_norm + f) : 0.0f;
+            const float gf = f < a.H ? __ldg(sh_layers[0].attn_norm + f) : 0.0f;
             float hv[kRows];
 #pragma unroll
             for (int r = 0; r < kRows; ++r) {
@@ -764,7 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
         uint32_t acc_ph = 0;
         int gp = 0;  // running phase index: stream-K partial buffers alternate by its parity
         for (int l = 0; l < a.nlayers; ++l) {
-            const LayerDesc& L = a.layers[l];
+            const LayerDesc& L = sh_layers[l];
             for (int p = 0; p < 4; ++p, ++gp) {
                 const Geo g = geom(a, p);
                 const long long U = static_cast<long long>(g.tiles) * g.KB;
@@ -802,8 +807,11 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     if (p == P_O || p == P_DOWN) {  // prefetch this tile's residual rows while the MMA runs
                         cp_async_wait_all();   // a previous (unused) prefetch must not land late
                         const int f = t * kM + m;
-                        if (f < a.H)
+                        const float* gn = p == P_O ? L.ffn_norm : L.next_attn_norm;
+                        if (f < a.H) {
                             for (int r = 0; r < a.rows; ++r) cp_async4(hpre + r * kM + m, a.h + static_cast<size_t>(r) * a.H + f);
+                            if (gn) cp_async4(hpre + kRows * kM + m, gn + f);
+                        }
                         cp_async_commit();
                     }
                     mwait(&tfull[acc], acc_ph);
@@ -905,7 +913,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
         int stage = 0;
         uint32_t ph = 0;
         for (int l = 0; l < a.nlayers; ++l) {
-            const LayerDesc& L = a.layers[l];
+            const LayerDesc& L = sh_layers[l];
             for (int p = 0; p < 4; ++p) {
                 if (warp == 6) {
                     // one bulk copy per stage of the unit's k-block of the prebuilt
@@ -986,7 +994,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
 size_t smem_bytes(int stages, int hd, int group, int max_len) {
     return 1024 + static_cast<size_t>(stages) * kStageBytes + (2 * kMaxStages + 4) * 8 + 32 +
            sizeof(float) * (64 * kRows + 5 * kRows + kMaxGroup * hd + 8 * kMaxGroup * 2 + 8 * group * hd +
-                            kRows * hd + kRows * kM) +
+                            kRows * hd + kRows * kM + kM) +
            sizeof(int) * static_cast<size_t>(max_len);
 }
 
