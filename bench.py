@@ -37,6 +37,15 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 H_7B = dict(vocab_size=32768, n_layers=32, hidden_dim=4096, n_heads=32, n_kv_heads=8, head_dim=128, ffn_dim=14336,
             max_seq_len=4096, rope_base=1e6, rms_eps=1e-5, seed=1234)
+# configs[3]: NeMo-12B width.  The reference's validate() needs n_heads*head_dim
+# == hidden_dim, so the 12B shape is run as its head_dim-160 variant (SURVEY
+# Appendix B.3): same d, layers, kv heads, ffn and vocab.
+H_12B = dict(vocab_size=131072, n_layers=40, hidden_dim=5120, n_heads=32, n_kv_heads=8, head_dim=160,
+             ffn_dim=14336, max_seq_len=4096, rope_base=1e6, rms_eps=1e-5, seed=1234)
+MODELS = {"7b": H_7B, "12b": H_12B}
+MODEL = H_7B
+SHAPE_TEXT = {"7b": "mistral-7b (32L d4096 32q/8kv x128 ffn14336 V32768)",
+              "12b": "nemo-12b width (40L d5120 32q/8kv x160 ffn14336 V131072; head_dim-160 variant)"}
 SPLIT = 2
 W, NG, G = 5, 3, 5
 PROMPT_LEN = 24
@@ -123,11 +132,11 @@ def dist_sum(ws, local, x: float) -> float:
 
 # ── CPU baseline: the reference's own forward_layers on the host ─────────
 def cpu_sample(threads: int, ctx: int, rows: int = 16):
-    """One 7B-wide middle layer over `rows` rows per host thread (oracle/_ref =
+    """One middle layer of the bench model over `rows` rows per host thread (oracle/_ref =
     the unmodified reference; port fallback), extrapolated to a full step:
     (28 middle + 4 local) layers + LM head over the rows."""
     import pyoracle as po
-    cfg = po.ModelCfg(**H_7B)
+    cfg = po.ModelCfg(**MODEL)
     if po.ref_available():
         lib, kind = po.Ref(), "reference"
         m = lib.timing_model(cfg, (2, 3), False)
@@ -139,7 +148,7 @@ def cpu_sample(threads: int, ctx: int, rows: int = 16):
 def cpu_head_time(lib, threads: int) -> float:
     """finalize() for one row at 7B width (LM head 4096 x 32768)."""
     import pyoracle as po
-    cfg = po.ModelCfg(**H_7B)
+    cfg = po.ModelCfg(**MODEL)
     mh = lib.timing_model(cfg, (0, 0), True)
     return lib.lib.ref_time_finalize(mh.h, 1, threads)
 
@@ -153,7 +162,7 @@ def run_reference(args, ws, rank):
     s = cpu_sample(threads, PROMPT_LEN, 16)
     lib, m = s["lib"], s["model"]
     t_head1 = cpu_head_time(lib, threads)
-    layers = H_7B["n_layers"]
+    layers = MODEL["n_layers"]
     steps = []
     rows = 4  # rows are independent in forward_layers: 4-row sample x4 = the B=16 step
     for i in range(args.warmup + args.steps):
@@ -163,7 +172,7 @@ def run_reference(args, ws, rank):
             steps.append(t_step)
     mean = sum(steps) / len(steps)
     tok_s = threads * 1.0 / mean
-    sample = (f"per step: one 7B-wide middle layer x {rows} rows on each of {threads} host threads "
+    sample = (f"per step: one {args.model} middle layer x {rows} rows on each of {threads} host threads "
               f"(forward_layers, oracle/_ref), scaled to 16 rows and x{layers} layers + LM head x16 rows; "
               f"1 committed token per step (forced-B16 junk-candidate workload)")
     line = {"metric": "lookahead step latency (ms) & tok/s at Mistral-7B shape vs HBM roofline",
@@ -177,12 +186,15 @@ def run_reference(args, ws, rank):
 
 
 def config_dict(args, ws):
-    return {"workload": "mistral7b-shape lookahead step, 2+2 local split (28 middle layers), W=5 N=3 G=5, "
-                        "forced B=16 (seeded n-gram pool)",
-            "model_shape": "mistral-7b (32L d4096 32q/8kv x128 ffn14336 V32768)", "rows_per_step": 16,
+    nl = MODEL["n_layers"]
+    mid = nl - 2 * SPLIT
+    name = "mistral7b" if args.model == "7b" else "nemo12b"
+    return {"workload": f"{name}-shape lookahead step, {SPLIT}+{SPLIT} local split ({mid} middle layers), "
+                        "W=5 N=3 G=5, forced B=16 (seeded n-gram pool)",
+            "model_shape": SHAPE_TEXT[args.model], "rows_per_step": 16,
             "prompt_len": PROMPT_LEN, "rtt_ms": args.rtt_ms, "math": args.math, "wire": "f16",
             "sessions_per_gpu": 1, "parallelism": f"replicas x{ws} (independent sessions)",
-            "l2": "inputs larger than L2 (12.2 GB of middle-layer weights streamed per step)"}
+            "l2": "inputs larger than L2 (the middle-layer weights, >10 GB, are streamed every step)"}
 
 
 def seed_pool(sfg, pool, vocab, g, rng):
@@ -209,7 +221,7 @@ def run_ours(args, ws, rank, local):
 
     L = _lib.lib()
     math = sfg.FAST if args.math == "fast" else sfg.EXACT
-    cfg = sfg.ModelConfig(**H_7B)
+    cfg = sfg.ModelConfig(**MODEL)
     t0 = time.time()
     eng = sfg.Engine(cfg, math=math, device=local)
     t_init = time.time() - t0
@@ -308,6 +320,26 @@ def run_ours(args, ws, rank, local):
             sweep[f"{int(rtt)}ms"] = {"tok_s": nt / dt, "ms_per_step": dt / k * 1000.0}
             L.sfg_decoder_destroy(d)
 
+    # ── privacy-depth sweep (configs[2]): 2/4/8 local layers each side ─────
+    privacy = {}
+    if not args.no_sweep:
+        for dloc in (2, 4, 8):
+            srv_d = srv if dloc == SPLIT else sfg.ServerEngine(eng, sfg.ServerConfig(dloc, nl - dloc, max_sessions=64))
+            cl = sfg.SplitClient(eng, sfg.SplitConfig(dloc, dloc, sfg.F16, 0.0), srv_d,
+                                 session_id=f"bench-priv{dloc}-{rank}")
+            d = make_decoder(cl)
+            for _ in range(3):
+                step(d)
+            k = max(3, min(args.steps, 8))
+            ms = []
+            for _ in range(k):
+                step(d)
+                L.sfg_client_last_profile(cl.h, C.byref(prof))
+                ms.append(prof.step_ms)
+            privacy[str(dloc)] = {"local_layers_each_side": dloc, "middle_layers": nl - 2 * dloc,
+                                  "device_ms_per_step": sum(ms) / len(ms)}
+            L.sfg_decoder_destroy(d)
+
     if rank != 0:
         return
     hbm, tflops, peak_kind = peaks()
@@ -346,6 +378,7 @@ def run_ours(args, ws, rank, local):
         "server_ms_per_step": sum(srv_ms) / len(srv_ms), "wall_ms_per_step": wall / args.steps * 1000.0,
         "batch_rows": sorted(set(batches)), "acceptance": toks / args.steps, "weights_init_s": t_init,
         "rtt_sweep": sweep,
+        "privacy_sweep": privacy,
         "clocks": clk.summary(),
     }
     if ws == 1 and not args.no_cpu:
@@ -355,8 +388,8 @@ def run_ours(args, ws, rank, local):
             t_step = s["t_layer_s"] * cfg.n_layers + th * 16
             line["cpu_baseline"] = {
                 "value": (toks / args.steps) / t_step, "unit": "tok/s", "cores": 1, "kind": s["kind"],
-                "sample": "one 7B-wide middle layer x 16 rows (forward_layers, oracle/_ref, 1 thread) + "
-                          "one LM-head row, extrapolated x32 layers and x16 head rows",
+                "sample": f"one {args.model} middle layer x 16 rows (forward_layers, oracle/_ref, 1 thread) + "
+                          f"one LM-head row, extrapolated x{cfg.n_layers} layers and x16 head rows",
                 "ms_per_step": t_step * 1000.0}
         except Exception as e:  # the checker must not take the GPU line down
             line["cpu_baseline"] = {"value": None, "unit": "tok/s", "cores": 1, "kind": "reference",
@@ -371,10 +404,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--math", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--model", default="7b", choices=sorted(MODELS))
     ap.add_argument("--rtt-ms", type=float, default=0.0)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    global MODEL
+    MODEL = MODELS[args.model]
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     ws, rank, local = dist_setup()
     if args.impl == "reference":

@@ -122,3 +122,21 @@ def test_fast_seven_b_layer_within_tolerance(ref):
     out = eng.forward_layers(2, 3, h, list(range(16)), eng.bank(2, 3))
     a = mr.bank(2, 3).forward(2, 3, h[:4], list(range(4)))
     assert rel(out[:4], a) <= HIDDEN_TOL
+
+
+def test_fast_seven_b_privacy_depths_lookahead_equals_sequential():
+    """configs[2]: Mistral-7B shape (32 layers, seeded reference init, bf16) with
+    2/4/8 local layers on each side of the split: lookahead decoding commits
+    exactly the sequential greedy tokens, with bitwise-equal logits."""
+    cfg = po.mistral7b_cfg(max_seq_len=256)
+    eng = sfg.Engine(scfg(cfg), math=sfg.FAST)
+    la = sfg.LookaheadConfig(ngram_n=3, window_w=5, max_candidates_g=5)
+    prompt = [3, 1, 4, 1, 5, 9, 2, 6, 5, 3, 5, 8, 9, 7, 9, 3]
+    for d in (2, 4, 8):
+        srv = sfg.ServerEngine(eng, sfg.ServerConfig(d, cfg.n_layers - d))
+        s = sfg.decode_sequential(sfg.SplitClient(eng, sfg.SplitConfig(d, d, sfg.F16), srv), prompt, 12,
+                                  want_logits=True)
+        a = sfg.decode_lookahead(sfg.SplitClient(eng, sfg.SplitConfig(d, d, sfg.F16), srv), prompt, 12, la,
+                                 want_logits=True)
+        assert s.tokens == a.tokens, d
+        assert np.array_equal(s.committed_logits, a.committed_logits), d
