@@ -88,6 +88,8 @@ struct MegaArgs {
     int pf;            // L2 prefetch distance in weight units (0: off)
     int evict_first;   // stream weights with an L2 evict-first policy
     int spin_mma;      // dev knob: MMA issuer spins on test_wait instead of try_wait
+    int bpf;           // bubble L2 prefetch depth in units (0: off)
+    long long bpf_cycles;  // ring-full wait (SM cycles) that counts as a bubble
     uint8_t* xim[4];   // per phase: the GEMM's input as [KB][48 x 64] split bf16 images (put_split)
     // optional [G][kBarSlots][kTraceW] (tools/trace_mega.py): per CTA and
     // barrier id, globaltimer stamps and wait totals (see tslot users)
@@ -671,6 +673,12 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
             Cursor pf{0, 0, 0, 0};
             cursor_begin(a, c, pf);
             for (int i = 0; i < a.pf; ++i) cursor_prefetch_next(a, c, pf);
+            // bubble prefetch: while the ring stays full for longer than a
+            // steady-state refill (grid-wide dependencies, attention, epilogue
+            // tails), prefetch the next units into L2 so HBM keeps streaming
+            Cursor bp{0, 0, 0, 0};
+            cursor_begin(a, c, bp);
+            long long n_cur = 0, n_bp = 0;
             for (int l = 0; l < a.nlayers; ++l)
                 for (int p = 0; p < 4; ++p) {
                     const Geo g = geom(a, p);
@@ -678,8 +686,30 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     long long st, en;
                     unit_range(g, c, st, en);
                     unsigned long long wacc = 0;
-                    for (long long u = st; u < en; ++u) {
-                        mwait_acc(&empty[stage], ph ^ 1, a.trace != nullptr, wacc);
+                    for (long long u = st; u < en; ++u, ++n_cur) {
+                        if (a.bpf > 0) {
+                            if (!mbar_test(&empty[stage], ph ^ 1)) {
+                                const long long t0 = clock64();
+                                unsigned long long spins = 0;
+                                while (!mbar_test(&empty[stage], ph ^ 1)) {
+                                    if (clock64() - t0 > a.bpf_cycles) {
+                                        while (n_bp < n_cur && bp.l < a.nlayers) {  // already being loaded
+                                            ++bp.u;
+                                            cursor_norm(a, c, bp);
+                                            ++n_bp;
+                                        }
+                                        if (n_bp < n_cur + a.bpf && bp.l < a.nlayers) {
+                                            cursor_prefetch_next(a, c, bp);
+                                            ++n_bp;
+                                        }
+                                    }
+                                    __nanosleep(20);
+                                    if (++spins > (1ull << 30)) asm volatile("trap;");
+                                }
+                            }
+                        } else {
+                            mwait_acc(&empty[stage], ph ^ 1, a.trace != nullptr, wacc);
+                        }
                         mbar_expect_tx(&full[stage], kABytes);
                         if (a.evict_first)
                             bulk_g2s_stream(smem + stage * kStageBytes, W + static_cast<size_t>(u) * kABytes, kABytes, &full[stage], pol);
@@ -1199,6 +1229,16 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
             return v ? atoi(v) : 0;
         }();
         a.spin_mma = spin_env;
+        static const int bpf_env = [] {
+            const char* v = getenv("SFG_MEGA_BPF");
+            return v ? atoi(v) : 0;
+        }();
+        static const long long bpfc_env = [] {
+            const char* v = getenv("SFG_MEGA_BPF_CYC");
+            return v ? atoll(v) : 2000LL;
+        }();
+        a.bpf = bpf_env;
+        a.bpf_cycles = bpfc_env;
     }
     {
         const size_t kbH = c.hidden_dim / tc::kKB, kbQ = c.q_dim() / tc::kKB;
