@@ -185,6 +185,29 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+def ncu_traffic(args):
+    """roofline.traffic from the committed `ncu --set full` capture of the
+    dominant kernel (profiles/r01_ncu_full_mega_summary.csv: one 28-layer
+    server launch of the megakernel), next to that launch's algorithmic bytes."""
+    import csv
+    path = os.path.join(ROOT, "profiles", "r01_ncu_full_mega_summary.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+        h, u, v = rows[0], rows[1], rows[2]
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+        rd = float(v[h.index("dram__bytes_read.sum")]) * scale[u[h.index("dram__bytes_read.sum")]]
+        wr = float(v[h.index("dram__bytes_write.sum")]) * scale[u[h.index("dram__bytes_write.sum")]]
+        if args.model != "7b":
+            raise ValueError("capture is of the 7B shape")
+        m = MODEL
+        H, qd, kvd, F = m["hidden_dim"], m["n_heads"] * m["head_dim"], m["n_kv_heads"] * m["head_dim"], m["ffn_dim"]
+        layer = 2 * (H * (qd + 2 * kvd) + qd * H + 3 * H * F)
+        return {"traffic": rd + wr, "traffic_launch": "one 28-layer server launch (ncu --set full)",
+                "traffic_launch_algorithmic_bytes": 28 * layer}
+    except Exception:
+        return {"traffic": None}
+
+
 def config_dict(args, ws):
     nl = MODEL["n_layers"]
     mid = nl - 2 * SPLIT
@@ -367,7 +390,7 @@ def run_ours(args, ws, rank, local):
                 "path": "frames through sfg_server_handle (C ABI), host buffers"},
         "gpu_launches": int(sum(launches)),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": None,
+                     "frac": achieved / hbm, "peak_kind": peak_kind, **ncu_traffic(args),
                      "launches": cnt, "avg_launch_us": avg_ms * 1000.0,
                      "algorithmic_bytes_per_launch": by / max(cnt, 1)},
         "step_roofline": {"algorithmic_bytes_per_step": step_bytes,
