@@ -421,6 +421,7 @@ def run_ours(args, ws, rank, local):
 
 
 def main():
+    global MODEL, PROMPT_LEN
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -429,11 +430,13 @@ def main():
     ap.add_argument("--math", default="fast", choices=["fast", "exact"])
     ap.add_argument("--model", default="7b", choices=sorted(MODELS))
     ap.add_argument("--rtt-ms", type=float, default=0.0)
+    ap.add_argument("--prompt-len", type=int, default=PROMPT_LEN,
+                    help="KV context before the first step (configs[4]: 2048)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    global MODEL
     MODEL = MODELS[args.model]
+    PROMPT_LEN = args.prompt_len
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     ws, rank, local = dist_setup()
     if args.impl == "reference":
