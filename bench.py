@@ -216,6 +216,7 @@ def config_dict(args, ws):
                         "W=5 N=3 G=5, forced B=16 (seeded n-gram pool)",
             "model_shape": SHAPE_TEXT[args.model], "rows_per_step": 16,
             "prompt_len": PROMPT_LEN, "rtt_ms": args.rtt_ms, "math": args.math, "wire": "f16",
+            "attention": os.environ.get("SFG_ATTN", "rows"),
             "sessions_per_gpu": 1, "parallelism": f"replicas x{ws} (independent sessions)",
             "l2": "inputs larger than L2 (the middle-layer weights, >10 GB, are streamed every step)"}
 
@@ -437,6 +438,10 @@ def main():
     args = ap.parse_args()
     MODEL = MODELS[args.model]
     PROMPT_LEN = args.prompt_len
+    # attention kernel of the layer-stack: per-(row, kv head) items for short
+    # contexts, key-chunked items sharing K/V across rows for long ones (both
+    # batch invariant; fixed for the whole run)
+    os.environ.setdefault("SFG_ATTN", "chunked" if PROMPT_LEN >= 512 else "rows")
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     ws, rank, local = dist_setup()
     if args.impl == "reference":

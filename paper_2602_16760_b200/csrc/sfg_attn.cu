@@ -189,7 +189,7 @@ int launch_hd(const float* q, const float* kc, const float* vc, const int32_t* r
                         static_cast<size_t>(d.max_len) * (sizeof(int) + sizeof(float)) +
                         sizeof(float) * static_cast<size_t>(d.n_heads / d.n_kv) * d.max_len;
     static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    if (smem > configured) {  // opt in even near 48 KB: static smem counts against the default limit
         if (smem > 220 * 1024) throw Error(Kind::config, "max_seq_len too large for the FAST attention kernel");
         SFG_CUDA(cudaFuncSetAttribute(attn_fast_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));

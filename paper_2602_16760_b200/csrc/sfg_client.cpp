@@ -210,6 +210,7 @@ void Client::stage_inputs(int seq, const int32_t* ids, const int32_t* pos, const
     std::memcpy(p + L.pos, pos, sizeof(int32_t) * seq);
     std::memcpy(p + L.roff, mr.row_off.data(), sizeof(int32_t) * mr.row_off.size());
     std::memcpy(p + L.runs, mr.runs.data(), sizeof(MaskRun) * mr.runs.size());
+    ws.additive_mask = !mega_mask_ok(mr, prefix_->len());
 }
 
 // [inputs H2D] -> compaction -> embed -> prefix layers

@@ -250,7 +250,7 @@ int launch_kv_compact_meta(float* kcache, float* vcache, int layers, int n_kv, i
     if (layers <= 0) return 0;
     const size_t smem = sizeof(float) * (size_t)max_keep * hd;
     static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    if (smem > configured) {
         cudaFuncSetAttribute(kv_compact_meta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = smem;
     }

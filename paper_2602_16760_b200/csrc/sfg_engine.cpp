@@ -68,6 +68,19 @@ ModelCfg ModelCfg::from_c(const sfg_model_config& c) {
 }
 
 // ── masks → runs ──────────────────────────────────────────────────────────
+bool mega_mask_ok(const MaskRuns& mr, int prior) {
+    for (const MaskRun& r : mr.runs)
+        if (r.mval != 0.0f) return false;
+    const int rows = static_cast<int>(mr.row_off.size()) - 1;
+    if (prior == 0) return true;
+    for (int i = 0; i < rows; ++i) {
+        if (mr.row_off[i] >= mr.row_off[i + 1]) return false;
+        const MaskRun& first = mr.runs[mr.row_off[i]];
+        if (first.start != 0 || first.end < prior) return false;
+    }
+    return true;
+}
+
 MaskRuns causal_runs(int rows, int committed) {
     MaskRuns m;
     m.row_off.resize(rows + 1);
@@ -645,8 +658,7 @@ void Engine::forward_host(Bank& b, int lb, int le, int seq, const float* h, cons
     Workspace& ws = b.ws();
     cudaStream_t s = b.stream();
     ensure_ws(ws, seq, static_cast<int>(mr.runs.size()), 0);
-    ws.additive_mask = false;
-    for (const MaskRun& r : mr.runs) ws.additive_mask = ws.additive_mask || r.mval != 0.0f;
+    ws.additive_mask = !mega_mask_ok(mr, prior);
     SFG_CUDA(cudaMemcpyAsync(ws.h, h, sizeof(float) * seq * H, cudaMemcpyHostToDevice, s));
     SFG_CUDA(cudaMemcpyAsync(ws.pos, pos, sizeof(int32_t) * seq, cudaMemcpyHostToDevice, s));
     SFG_CUDA(cudaMemcpyAsync(ws.row_off, mr.row_off.data(), sizeof(int32_t) * (seq + 1), cudaMemcpyHostToDevice, s));

@@ -95,7 +95,10 @@ struct Workspace {
     void* stage_pin = nullptr;     // pinned [ids | pos | row_off | runs] at cap-derived offsets
     size_t stage_bytes = 0;
     uint64_t generation = 0;       // bumped whenever a buffer is reallocated
-    bool additive_mask = false;    // some visible column carries a non-zero mask value
+    // the mask is outside the layer-stack megakernel's contract: some visible
+    // column carries a non-zero (additive) value, or some row does not see the
+    // whole cached prefix [0, prior) (see mega_mask_ok)
+    bool additive_mask = false;
     void release();
 };
 
@@ -174,6 +177,10 @@ struct MaskRuns {
 MaskRuns causal_runs(int rows, int committed);
 // Dense fp32 additive mask [rows x kv] with -inf = masked.
 MaskRuns runs_from_dense(const float* mask, int rows, int kv);
+// The megakernel's attention walks each row's visible keys in compacted order
+// and shares the cached prefix between rows: every row must see all of
+// [0, prior) with mask value 0 (causal, lookahead and branch masks do).
+bool mega_mask_ok(const MaskRuns& mr, int prior);
 
 class Engine {
 public:

@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <string>
 
 #include "sfg_engine.h"
 #include "sfg_prof.h"
@@ -91,6 +92,9 @@ struct MegaArgs {
     int bpf;           // bubble L2 prefetch depth in units (0: off)
     long long bpf_cycles;  // ring-full wait (SM cycles) that counts as a bubble
     uint8_t* xim[4];   // per phase: the GEMM's input as [KB][48 x 64] split bf16 images (put_split)
+    int attn_rows;     // 1: per-(row, kv head) attention; 0: key-chunked, rows share K/V (long contexts)
+    float* apart;      // attention chunk partials [n_kv][ceil(max_len/kKeyChunk)][128 queries][hd + 2]
+    unsigned* acnt;    // [n_kv] chunk arrival counters (reset by the merging chunk)
     // optional [G][kBarSlots][kTraceW] (tools/trace_mega.py): per CTA and
     // barrier id, globaltimer stamps and wait totals (see tslot users)
     unsigned long long* trace;
@@ -299,6 +303,9 @@ __device__ __forceinline__ void put_split(uint8_t* img, int k, int r, float x) {
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -308,6 +315,9 @@ constexpr int kMaxMegaLayers = 64;
 __shared__ int sh_pos[kRows];
 __shared__ int sh_prior;
 __shared__ LayerDesc sh_layers[kMaxMegaLayers];
+// per row: compacted visible-key count and its tail slots (columns >= prior)
+__shared__ int sh_ncols[kRows];
+__shared__ int sh_tail[kRows][kRows];
 
 // ── epilogues (thread = feature m of the tile; y[r] for 16 rows) ─────────
 // RMSNorm is split across the two sides of the GEMM: the producing epilogue
@@ -403,7 +413,7 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int p, int tile
 // ── attention for one (row, kv head): flash-decode over the row's visible
 // keys with a fixed key partition (chunk i of 32 keys -> warp i % 8).
 template <int HD, int GR>  // GR: compile-time bound on the GQA group (register arrays)
-__device__ void attention_item(const MegaArgs& a, const LayerDesc& L, int row, int kvh, int at, float* qs,
+__device__ void attention_row_item(const MegaArgs& a, const LayerDesc& L, int row, int kvh, int at, float* qs,
                                float* wst, float* ocomb, int* cols) {
     const int group = a.n_heads / a.n_kv;
     const int warp = at >> 5, lane = at & 31;
@@ -541,7 +551,7 @@ __device__ void attention_item(const MegaArgs& a, const LayerDesc& L, int row, i
     named_sync(3, 256);
 }
 
-__device__ __forceinline__ void attention_dispatch(const MegaArgs& a, const LayerDesc& L, int l, int row, int kvh,
+__device__ __forceinline__ void attention_rows_dispatch(const MegaArgs& a, const LayerDesc& L, int l, int row, int kvh,
                                                    int at, float* qs, float* wst, float* ocomb, int* cols) {
     const int group = a.n_heads / a.n_kv;
     {  // wait for this kv head's QKV tiles: its q heads, K and V
@@ -557,18 +567,306 @@ __device__ __forceinline__ void attention_dispatch(const MegaArgs& a, const Laye
     }
     if (group <= 4) {
         switch (a.hd) {
-            case 64: attention_item<64, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
-            case 128: attention_item<128, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
-            case 160: attention_item<160, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
-            default: attention_item<32, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
+            case 64: attention_row_item<64, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
+            case 128: attention_row_item<128, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
+            case 160: attention_row_item<160, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
+            default: attention_row_item<32, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
         }
     } else {
         switch (a.hd) {
-            case 64: attention_item<64, 8>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
-            default: attention_item<32, 8>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
+            case 64: attention_row_item<64, 8>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
+            default: attention_row_item<32, 8>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
         }
     }
     if (at == 0) signal_add(fptr(a, l, K_ATT, kvh), 1u);  // item's att rows + image are published
+}
+
+// ── attention over the KV cache ─────────────────────────────────────────
+// Work item = (kv head, key chunk, query group).  A chunk is kKeyChunk keys at
+// ABSOLUTE positions, walked in blocks of kKeyBlock keys that the whole CTA
+// stages into shared memory once (cp.async) and shares across its queries
+// (rows x the group's q heads; each warp owns QPW of them).  Blocks are
+// combined in key order with an online softmax, invisible keys contribute
+// exact zeros, and several chunks of a head are merged in chunk order by the
+// last one to finish: a row's result does not depend on the batch around it
+// (lookahead == sequential, bitwise) nor on how queries are grouped.
+constexpr int kKeyChunk = 128;
+constexpr int kKeyBlock = 16;
+
+__device__ __forceinline__ bool key_visible(const MegaArgs& a, int row, int key) {
+    const int r0 = a.row_off[row], r1 = a.row_off[row + 1];
+    for (int i = r0; i < r1; ++i) {
+        const MaskRun rr = a.runs[i];
+        if (key >= rr.start && key < rr.end) return true;
+    }
+    return false;
+}
+
+template <int HD, int QPW>
+__device__ void attention_chunk(const MegaArgs& a, const LayerDesc& L, int l, int kvh, int chunk, int nchunks,
+                                int qg, int at, float* sq, float* sp, float* skv, float* part, unsigned* acnt,
+                                int* flag) {
+    constexpr int QI = 8 * QPW;    // queries per item
+    constexpr int C4 = HD / 4;     // float4 columns per key row
+    constexpr int DPL = HD / 32;   // value dims per lane
+    constexpr int HH = HD / 2;     // score dims per lane (2 lanes per key)
+    const int group = a.n_heads / a.n_kv;
+    const int NQ = a.rows * group;  // query q = row * group + g
+    const int qbase = qg * QI;
+    const int nq = min(QI, NQ - qbase);
+    const int warp = at >> 5, lane = at & 31;
+    const int prior = sh_prior;
+    const int ncmax = prior + a.rows;  // bound on every row's compacted key count
+    // keys are walked in each row's COMPACTED order: index i < prior is cache
+    // slot i (shared by every row), i >= prior is the row's own tail slot
+    const int k0 = chunk * kKeyChunk, k1 = min(ncmax, k0 + kKeyChunk);
+    for (int t = at; t < nq * HD; t += 256) {
+        const int q = qbase + t / HD, d = t % HD, r = q / group, g = q % group;
+        sq[t] = __ldcg(a.q + static_cast<size_t>(r) * a.qd + static_cast<size_t>(kvh * group + g) * HD + d);
+    }
+    const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(HD));
+    const float* kbase = L.kc + static_cast<size_t>(kvh) * a.max_len * HD;
+    const float* vbase = L.vc + static_cast<size_t>(kvh) * a.max_len * HD;
+    float* sk = skv;                          // [kKeyBlock][C4] float4, column XOR-swizzled by row & 7
+    float* sv = sk + kKeyBlock * HD;          // [kKeyBlock][HD]
+    float* skt = sv + kKeyBlock * HD;         // tail slots [prior, prior + rows): K (swizzled) | V
+    float* svt = skt + kRows * HD;
+    const int q0 = warp * QPW;                // the warp's queries (item-local)
+    const int key_l = lane & 15, half = lane >> 4;
+    if (k1 > prior) {  // this chunk reaches the rows' own tails: stage them once
+        for (int t = at; t < kRows * C4; t += 256) {
+            const int j = t / C4, c4 = t % C4;
+            float4* dk = reinterpret_cast<float4*>(skt) + j * C4 + (c4 ^ (j & 7));
+            float4* dv = reinterpret_cast<float4*>(svt) + j * C4 + c4;
+            if (j < a.rows) {
+                cp_async16(dk, kbase + static_cast<size_t>(prior + j) * HD + 4 * c4);
+                cp_async16(dv, vbase + static_cast<size_t>(prior + j) * HD + 4 * c4);
+            } else {
+                *dk = make_float4(0.f, 0.f, 0.f, 0.f);
+                *dv = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        cp_async_commit();
+    }
+    float m_run[QPW], l_run[QPW], o[QPW][DPL];
+#pragma unroll
+    for (int i = 0; i < QPW; ++i) {
+        m_run[i] = -INFINITY;
+        l_run[i] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) o[i][j] = 0.0f;
+    }
+    float* myp = sp + warp * QPW * kKeyBlock;
+    for (int kb0 = k0; kb0 < k1; kb0 += kKeyBlock) {
+        const int np = max(0, min(kKeyBlock, prior - kb0));  // shared-prefix keys of this block
+        named_sync(3, 256);  // previous block fully consumed
+        for (int t = at; t < kKeyBlock * C4; t += 256) {
+            const int j = t / C4, c4 = t % C4;
+            float4* dk = reinterpret_cast<float4*>(sk) + j * C4 + (c4 ^ (j & 7));
+            float4* dv = reinterpret_cast<float4*>(sv) + j * C4 + c4;
+            if (j < np) {
+                cp_async16(dk, kbase + static_cast<size_t>(kb0 + j) * HD + 4 * c4);
+                cp_async16(dv, vbase + static_cast<size_t>(kb0 + j) * HD + 4 * c4);
+            } else {
+                *dk = make_float4(0.f, 0.f, 0.f, 0.f);
+                *dv = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        cp_async_commit();
+        cp_async_wait_all();
+        named_sync(3, 256);
+        if (q0 < nq) {
+            const int ci = kb0 + key_l;  // this lane's compacted key index
+            // K row of (query i, lane): shared block or the query row's tail slot
+            auto krow = [&](int i, int& sw) -> const float4* {
+                if (ci < prior) {
+                    sw = key_l & 7;
+                    return reinterpret_cast<const float4*>(sk) + key_l * C4;
+                }
+                const int r = (qbase + q0 + i) / group;
+                const int t = ci - prior < kRows ? sh_tail[r][ci - prior] - prior : 0;
+                sw = t & 7;
+                return reinterpret_cast<const float4*>(skt) + t * C4;
+            };
+            float sc[QPW];
+#pragma unroll
+            for (int i = 0; i < QPW; ++i) {
+                sc[i] = 0.0f;
+                int sw;
+                const float4* kr = krow(i, sw);
+#pragma unroll 4
+                for (int c = 0; c < HH / 4; ++c) {
+                    const int c4 = half * (HH / 4) + c;
+                    const float4 k4 = kr[c4 ^ sw];
+                    const float4 q4 = reinterpret_cast<const float4*>(sq + (q0 + i) * HD)[c4];
+                    sc[i] += q4.x * k4.x + q4.y * k4.y + q4.z * k4.z + q4.w * k4.w;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < QPW; ++i) {
+                sc[i] += __shfl_xor_sync(0xffffffffu, sc[i], 16);
+                const int q = qbase + q0 + i;
+                const bool vis = q0 + i < nq && ci < sh_ncols[q / group];
+                const float s = vis ? sc[i] * inv_sqrt_hd : -INFINITY;
+                float mb = s;
+                for (int off = 8; off > 0; off >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, off));
+                const float mn = fmaxf(m_run[i], mb);
+                const float scale_old = m_run[i] == -INFINITY ? (mn == -INFINITY ? 1.0f : 0.0f) : expf(m_run[i] - mn);
+                const float pj = vis ? expf(s - mn) : 0.0f;
+                float ps = pj;
+                for (int off = 8; off > 0; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+                l_run[i] = l_run[i] * scale_old + ps;
+                m_run[i] = mn;
+#pragma unroll
+                for (int j = 0; j < DPL; ++j) o[i][j] *= scale_old;
+                if (half == 0) myp[i * kKeyBlock + key_l] = pj;
+            }
+            __syncwarp();
+            // values: lane = dims, the block's keys in compacted order
+            if (np == kKeyBlock) {  // shared prefix block: one V row for every query
+#pragma unroll 4
+                for (int j = 0; j < kKeyBlock; ++j) {
+                    float v[DPL];
+#pragma unroll
+                    for (int dd = 0; dd < DPL; ++dd) v[dd] = sv[j * HD + lane + 32 * dd];
+#pragma unroll
+                    for (int i = 0; i < QPW; ++i) {
+                        const float pj = myp[i * kKeyBlock + j];
+#pragma unroll
+                        for (int dd = 0; dd < DPL; ++dd) o[i][dd] += pj * v[dd];
+                    }
+                }
+            } else {
+                for (int j = 0; j < kKeyBlock; ++j) {
+                    const int cj = kb0 + j;
+#pragma unroll
+                    for (int i = 0; i < QPW; ++i) {
+                        const int r = (qbase + q0 + min(i, nq - 1 - q0)) / group;
+                        const float* vr = cj < prior ? sv + j * HD
+                                                     : svt + (cj - prior < kRows ? sh_tail[r][cj - prior] - prior : 0) * HD;
+                        const float pj = myp[i * kKeyBlock + j];
+#pragma unroll
+                        for (int dd = 0; dd < DPL; ++dd) o[i][dd] += pj * vr[lane + 32 * dd];
+                    }
+                }
+            }
+        }
+    }
+    // publish: one chunk -> final values; several -> partials, the last chunk merges
+    auto finish = [&](int q, float lsum, const float* ov) {
+        const int r = q / group, g = q % group;
+        if (!(lsum > 0.0f) && lane == 0) atomicOr(a.status, ST_EMPTY_ROW);
+#pragma unroll
+        for (int dd = 0; dd < DPL; ++dd) {
+            const int d = lane + 32 * dd;
+            const float val = ov[dd] / lsum;
+            const int f = (kvh * group + g) * HD + d;
+            a.att[static_cast<size_t>(r) * a.qd + f] = val;
+            put_split(a.xim[P_O], f, r, val);
+        }
+    };
+    const int cpk = (a.max_len + kKeyChunk - 1) / kKeyChunk;  // chunk slots per kv head
+    const size_t qstride = HD + 2;
+    if (nchunks > 1) {
+        float* pc = part + (static_cast<size_t>(kvh) * cpk + chunk) * 128 * qstride;
+#pragma unroll
+        for (int i = 0; i < QPW; ++i) {
+            const int q = qbase + q0 + i;
+            if (q0 + i >= nq) continue;
+            float* dst = pc + q * qstride;
+            if (lane == 0) {
+                dst[0] = m_run[i];
+                dst[1] = l_run[i];
+            }
+#pragma unroll
+            for (int dd = 0; dd < DPL; ++dd) dst[2 + lane + 32 * dd] = o[i][dd];
+        }
+        __threadfence();
+        named_sync(3, 256);
+        if (at == 0) {
+            unsigned* cnt = acnt + kvh * 16 + qg;
+            const unsigned old = atomicAdd(cnt, 1u);
+            *flag = old == static_cast<unsigned>(nchunks - 1) ? 1 : 0;
+            if (old == static_cast<unsigned>(nchunks - 1)) *cnt = 0u;
+        }
+        named_sync(3, 256);
+        if (!*flag) return;
+        __threadfence();
+        const float* p0 = part + static_cast<size_t>(kvh) * cpk * 128 * qstride;
+        for (int qi = warp; qi < nq; qi += 8) {  // merge this group's queries, chunks in key order
+            const int q = qbase + qi;
+            float M = -INFINITY;
+            for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, __ldcg(p0 + (static_cast<size_t>(ch) * 128 + q) * qstride));
+            float lsum = 0.0f, ov[DPL];
+#pragma unroll
+            for (int dd = 0; dd < DPL; ++dd) ov[dd] = 0.0f;
+            for (int ch = 0; ch < nchunks; ++ch) {
+                const float* src = p0 + (static_cast<size_t>(ch) * 128 + q) * qstride;
+                const float mc = __ldcg(src);
+                const float w = mc == -INFINITY ? 0.0f : expf(mc - M);
+                lsum += __ldcg(src + 1) * w;
+#pragma unroll
+                for (int dd = 0; dd < DPL; ++dd) ov[dd] += __ldcg(src + 2 + lane + 32 * dd) * w;
+            }
+            finish(q, lsum, ov);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < QPW; ++i)
+            if (q0 + i < nq) finish(qbase + q0 + i, l_run[i], o[i]);
+    }
+    fence_proxy_async_global();
+    named_sync(3, 256);
+    if (at == 0) {  // these rows of this kv head are published
+        __threadfence();
+        atomicAdd(fptr(a, l, K_ATT, kvh), static_cast<unsigned>(nq / group));
+    }
+}
+
+// queries per warp for this launch: fewer queries per item (more items) when
+// there are few key chunks.  Numerics do not depend on this choice.
+__device__ __forceinline__ int attn_qpw(const MegaArgs& a, int nchunks) { return nchunks * a.n_kv >= 64 ? 8 : 2; }
+
+__device__ __forceinline__ void attention_dispatch(const MegaArgs& a, const LayerDesc& L, int l, int item, int nchunks,
+                                                   int at, float* sq, float* sp, float* skv, float* part,
+                                                   unsigned* acnt, int* flag) {
+    const int group = a.n_heads / a.n_kv;
+    const int qpw = attn_qpw(a, nchunks);
+    const int nqg = (a.rows * group + 8 * qpw - 1) / (8 * qpw);
+    const int kvh = item / (nchunks * nqg), rem = item % (nchunks * nqg), chunk = rem / nqg, qg = rem % nqg;
+    {  // wait for this kv head's QKV tiles: its q heads, K and V
+        const int q0 = kvh * group * a.hd / kM, q1 = ((kvh + 1) * group * a.hd - 1) / kM;
+        const int kt = (a.qd + kvh * a.hd) / kM, kt1 = (a.qd + kvh * a.hd + a.hd - 1) / kM;
+        const int vt = (a.qd + a.kvd + kvh * a.hd) / kM, vt1 = (a.qd + a.kvd + kvh * a.hd + a.hd - 1) / kM;
+        const int nq = q1 - q0 + 1, nk = kt1 - kt + 1, nv = vt1 - vt + 1;
+        if (at < nq + nk + nv) {
+            const int t = at < nq ? q0 + at : (at < nq + nk ? kt + at - nq : vt + at - nq - nk);
+            wait_ge(fptr(a, l, K_QKV, t), 1u);
+        }
+        named_sync(3, 256);
+    }
+#define SFG_ATT(HDV, Q) attention_chunk<HDV, Q>(a, L, l, kvh, chunk, nchunks, qg, at, sq, sp, skv, part, acnt, flag)
+    if (qpw == 8) {
+        switch (a.hd) {
+            case 64: SFG_ATT(64, 8); break;
+            case 128: SFG_ATT(128, 8); break;
+            case 160: SFG_ATT(160, 8); break;
+            default: SFG_ATT(32, 8); break;
+        }
+    } else {
+        switch (a.hd) {
+            case 64: SFG_ATT(64, 2); break;
+            case 128: SFG_ATT(128, 2); break;
+            case 160: SFG_ATT(160, 2); break;
+            default: SFG_ATT(32, 2); break;
+        }
+    }
+#undef SFG_ATT
+}
+__device__ __forceinline__ int attention_items(const MegaArgs& a, int nchunks) {
+    const int qpw = attn_qpw(a, nchunks);
+    const int nqg = (a.rows * (a.n_heads / a.n_kv) + 8 * qpw - 1) / (8 * qpw);
+    return a.n_kv * nchunks * nqg;
 }
 
 // A CTA's walk over its weight units: (layer, phase, unit) in stream order.
@@ -606,9 +904,17 @@ __device__ __forceinline__ void cursor_prefetch_next(const MegaArgs& a, int c, C
     cursor_norm(a, c, k);
 }
 
+// shared-memory floats of the attention scratch: the larger of the two layouts
+__host__ __device__ __forceinline__ int attn_scratch_floats(bool rows_attn, int hd, int group, int max_len) {
+    return rows_attn ? kMaxGroup * hd + 8 * kMaxGroup * 2 + 8 * group * hd + max_len
+                     : 64 * hd + 8 * 8 * kKeyBlock + 4 * kKeyBlock * hd;
+}
+
 // ── the kernel ────────────────────────────────────────────────────────────
 // 10 warps, one CTA per SM: 3 warps share an SM sub-partition's 16K
 // registers, so 168 registers per thread is the ceiling
+// kRowsAttn: which attention design this instantiation carries (MegaArgs::attn_rows)
+template <bool kRowsAttn>
 __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant__ MegaArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -621,11 +927,15 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
     int* flag = reinterpret_cast<int*>(tmem_slot + 4);
     float* xch = reinterpret_cast<float*>(flag + 4);          // 64*16 gate|up + 4*16 sumsq
     float* rs = xch + 64 * kRows + 4 * kRows;                  // [16] per-row 1/rms of the phase
-    float* qs = rs + kRows;                                    // [group][hd]
-    float* wst = qs + kMaxGroup * a.hd;                        // [8][kMaxGroup][2]
-    float* ocomb = wst + 8 * kMaxGroup * 2;                    // [8][group][hd]
-    int* cols = reinterpret_cast<int*>(ocomb + 8 * (a.n_heads / a.n_kv) * a.hd);  // [max_len]
-    float* ropeT = reinterpret_cast<float*>(cols + a.max_len);  // [16][hd]: cos | sin of the rows' positions
+    // attention scratch, one of two layouts (MegaArgs::attn_rows):
+    float* sq = rs + kRows;                                    // chunked: [64 queries][hd] queries
+    float* sp = sq + 64 * a.hd;                                //   [8 warps][8][kKeyBlock] probabilities
+    float* skv = sp + 8 * 8 * kKeyBlock;                       //   staged K | V block + tail slots
+    float* qs = rs + kRows;                                    // per-row: [group][hd] queries
+    float* wst = qs + kMaxGroup * a.hd;                        //   [8][kMaxGroup][2] warp stats
+    float* ocomb = wst + 8 * kMaxGroup * 2;                    //   [8][group][hd] warp partials
+    int* cols = reinterpret_cast<int*>(ocomb + 8 * (a.n_heads / a.n_kv) * a.hd);  //   [max_len]
+    float* ropeT = rs + kRows + attn_scratch_floats(kRowsAttn, a.hd, a.n_heads / a.n_kv, a.max_len);  // [16][hd] cos | sin
     float* hpre = ropeT + kRows * a.hd;                         // [16][128] residual prefetch
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -643,6 +953,17 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
     }
     if (threadIdx.x == 0) sh_prior = *a.prior;
     for (int i = threadIdx.x; i < a.nlayers; i += blockDim.x) sh_layers[i] = a.layers[i];
+    if (threadIdx.x < kRows) {  // compacted key lists (mega_mask_ok: every row sees [0, prior))
+        const int r = threadIdx.x, prior = *a.prior;
+        int n = 0;
+        if (r < a.rows)
+            for (int i = a.row_off[r]; i < a.row_off[r + 1]; ++i) {
+                const MaskRun rr = a.runs[i];
+                for (int col = max(rr.start, prior); col < rr.end && n < kRows; ++col) sh_tail[r][n++] = col;
+            }
+        for (int j = n; j < kRows; ++j) sh_tail[r][j] = prior;
+        sh_ncols[r] = r < a.rows ? prior + n : 0;
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 2);   // weight bytes + activation bytes (two expect_tx arrivals)
@@ -932,8 +1253,16 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     *tslot(a, c, input_barrier(l, p), 6) = t_acc;
                 }
                 if (p == P_QKV) {  // attention, shared with the activation warps
-                    for (int it = c; it < a.rows * a.n_kv; it += G)
-                        attention_dispatch(a, L, l, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst, ocomb, cols);
+                    if constexpr (kRowsAttn) {
+                        for (int it = c; it < a.rows * a.n_kv; it += G)
+                            attention_rows_dispatch(a, L, l, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst,
+                                                    ocomb, cols);
+                    } else {
+                        const int nchunks = (sh_prior + a.rows + kKeyChunk - 1) / kKeyChunk;
+                        for (int it = c; it < attention_items(a, nchunks); it += G)
+                            attention_dispatch(a, L, l, it, nchunks, threadIdx.x - 64, sq, sp, skv, a.apart, a.acnt,
+                                               flag);
+                    }
                     if (a.trace && et == 0) *tslot(a, c, 5 * l + 2, 2) = gtimer();
                 }
             }
@@ -991,9 +1320,18 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     }
                     __syncwarp();
                 }
-                if (p == P_QKV)  // join the attention phase
-                    for (int it = c; it < a.rows * a.n_kv; it += G)
-                        attention_dispatch(a, L, l, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst, ocomb, cols);
+                if (p == P_QKV) {  // join the attention phase
+                    if constexpr (kRowsAttn) {
+                        for (int it = c; it < a.rows * a.n_kv; it += G)
+                            attention_rows_dispatch(a, L, l, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst,
+                                                    ocomb, cols);
+                    } else {
+                        const int nchunks = (sh_prior + a.rows + kKeyChunk - 1) / kKeyChunk;
+                        for (int it = c; it < attention_items(a, nchunks); it += G)
+                            attention_dispatch(a, L, l, it, nchunks, threadIdx.x - 64, sq, sp, skv, a.apart, a.acnt,
+                                               flag);
+                    }
+                }
             }
         }
         (void)xt;
@@ -1021,11 +1359,32 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
     }
 }
 
-size_t smem_bytes(int stages, int hd, int group, int max_len) {
+// dynamic shared memory available next to the kernel's static __shared__ data
+size_t dyn_smem_budget(bool rows_attn) {
+    static size_t budget[2] = {0, 0};
+    if (!budget[rows_attn]) {
+        cudaFuncAttributes fa{};
+        if (rows_attn)
+            cudaFuncGetAttributes(&fa, mega_kernel<true>);
+        else
+            cudaFuncGetAttributes(&fa, mega_kernel<false>);
+        budget[rows_attn] = 227 * 1024 - fa.sharedSizeBytes;
+    }
+    return budget[rows_attn];
+}
+
+size_t smem_bytes(bool rows_attn, int stages, int hd, int group, int max_len) {
     return 1024 + static_cast<size_t>(stages) * kStageBytes + (2 * kMaxStages + 4) * 8 + 32 +
-           sizeof(float) * (64 * kRows + 5 * kRows + kMaxGroup * hd + 8 * kMaxGroup * 2 + 8 * group * hd +
-                            kRows * hd + kRows * kM + kM) +
-           sizeof(int) * static_cast<size_t>(max_len);
+           sizeof(float) * (64 * kRows + 5 * kRows + attn_scratch_floats(rows_attn, hd, group, max_len) + kRows * hd +
+                            kRows * kM + kM) + 16;
+}
+
+bool rows_attention() {
+    static const int v = [] {
+        const char* e = getenv("SFG_ATTN");  // "chunked": key-chunked attention for long contexts
+        return e && std::string(e) == "chunked" ? 0 : 1;
+    }();
+    return v != 0;
 }
 
 }  // namespace mega
@@ -1042,8 +1401,9 @@ bool mega_supported(const Engine& e, int rows, bool additive_mask) {
     if (group > kMaxGroup || c.head_dim % 32 != 0 || c.head_dim > 160) return false;
     if (group > 4 && c.head_dim > 64) return false;  // register budget of the attention phase
     if (c.hidden_dim % tc::kKB || c.q_dim() % tc::kKB || c.ffn_dim % tc::kKB) return false;
-    const size_t sm = smem_bytes(4, c.head_dim, c.n_heads / c.n_kv_heads, c.max_seq_len);
-    return sm <= 227 * 1024;
+    const bool ra = rows_attention();
+    const size_t sm = smem_bytes(ra, 4, c.head_dim, c.n_heads / c.n_kv_heads, c.max_seq_len);
+    return sm <= dyn_smem_budget(ra);
 }
 
 namespace {
@@ -1057,6 +1417,8 @@ struct MegaState {
     float* partials = nullptr;  // 2 parity buffers of stream-K partials
     int* counters = nullptr;    // 2 parity arrays of per-tile arrival counters
     unsigned* flags = nullptr;  // dataflow completion flags
+    float* apart = nullptr;     // attention chunk partials
+    unsigned* acnt = nullptr;
     size_t part_stride = 0;
     int cnt_stride = 0, nflags = 0;
     ~MegaState() {
@@ -1068,6 +1430,8 @@ struct MegaState {
         if (partials) cudaFree(partials);
         if (counters) cudaFree(counters);
         if (flags) cudaFree(flags);
+        if (apart) cudaFree(apart);
+        if (acnt) cudaFree(acnt);
     }
 };
 }  // namespace
@@ -1143,6 +1507,10 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
             const int lay = (tQ + 1) + (c.n_kv_heads + 1) + (tilesH + 1) + (tG + 1) + (tilesH + 1);
             st.nflags = tilesH + 1 + (le - lb) * lay;
             SFG_CUDA(cudaMalloc(&st.flags, sizeof(unsigned) * st.nflags));
+            const size_t cpk = (c.max_seq_len + kKeyChunk - 1) / kKeyChunk;
+            SFG_CUDA(cudaMalloc(&st.apart, sizeof(float) * c.n_kv_heads * cpk * 128 * (c.head_dim + 2)));
+            SFG_CUDA(cudaMalloc(&st.acnt, sizeof(unsigned) * c.n_kv_heads * 16));
+            SFG_CUDA(cudaMemset(st.acnt, 0, sizeof(unsigned) * c.n_kv_heads * 16));
             SFG_CUDA(cudaMemset(st.flags, 0, sizeof(unsigned) * st.nflags));
         }
         SFG_CUDA(cudaMemset(st.xim, 0, xblocks * tc::kBBytes));
@@ -1162,17 +1530,19 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         return v ? std::min(std::max(atoi(v), 2), kMaxStages) : kMaxStages;
     }();
     int stages = stages_cap;
-    while (stages > 4 && smem_bytes(stages, c.head_dim, group, c.max_seq_len) > 227 * 1024) --stages;
-    const size_t smem = smem_bytes(stages, c.head_dim, group, c.max_seq_len);
-    static size_t configured = 0;
-    if (smem > configured) {
-        SFG_CUDA(cudaFuncSetAttribute(mega_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured = smem;
+    const bool ra = rows_attention();
+    const void* kfn = ra ? reinterpret_cast<const void*>(mega_kernel<true>) : reinterpret_cast<const void*>(mega_kernel<false>);
+    while (stages > 4 && smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len) > dyn_smem_budget(ra)) --stages;
+    const size_t smem = smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len);
+    static size_t configured[2] = {0, 0};
+    if (smem > configured[ra]) {
+        SFG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured[ra] = smem;
         int nb = 0;
-        SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, mega_kernel, kThreads, smem));
+        SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kfn, kThreads, smem));
         if (nb < 1) {
             cudaFuncAttributes fa{};
-            cudaFuncGetAttributes(&fa, mega_kernel);
+            cudaFuncGetAttributes(&fa, kfn);
             throw Error(Kind::internal, "megakernel does not fit an SM: regs " + std::to_string(fa.numRegs) +
                                             " static smem " + std::to_string(fa.sharedSizeBytes) + " dyn smem " +
                                             std::to_string(smem) + " max threads " + std::to_string(fa.maxThreadsPerBlock));
@@ -1210,6 +1580,8 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     a.part_stride = stp->part_stride;
     a.cnt_stride = stp->cnt_stride;
     a.flags = stp->flags;
+    a.apart = stp->apart;
+    a.acnt = stp->acnt;
     a.nflags = stp->nflags;
     a.bar = stp->bar;
     a.status = ws.status;
@@ -1238,6 +1610,7 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
             return v ? atoll(v) : 2000LL;
         }();
         a.bpf = bpf_env;
+        a.attn_rows = ra ? 1 : 0;
         a.bpf_cycles = bpfc_env;
     }
     {
@@ -1261,7 +1634,7 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
                              L * 2.0 * 4.0 * kvd * (b.len() + rows) + 4.0 * R * H * 2;
         const double flops = L * 2.0 * R * (H * (qd + 2 * kvd) + qd * H + 3 * H * F);
         ProfScope ps(K_LAYERS, s, bytes, flops);
-        SFG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mega_kernel), dim3(nsm), dim3(kThreads), args, smem, s));
+        SFG_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(nsm), dim3(kThreads), args, smem, s));
     }
     return 1;
 }

@@ -288,6 +288,7 @@ void Server::handle_frame(const wire::FrameView& f, std::vector<uint8_t>& resp) 
                                                                                               : wire::Dtype::f16);
     const int n = seq * c.hidden_dim;
     upload_meta(eng_, ws, hc.pos, mr, s);
+    ws.additive_mask = !mega_mask_ok(mr, bank.len());
     SFG_CUDA(cudaMemcpyAsync(ws.wire, f.tensor, f.tensor_len, cudaMemcpyHostToDevice, s));
     launch_unpack_rows(ws.wire, in_f32, n, ws.h, s);
     SFG_CUDA(cudaMemsetAsync(ws.status, 0, sizeof(uint32_t), s));
