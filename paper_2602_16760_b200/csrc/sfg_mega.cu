@@ -306,6 +306,7 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -603,7 +604,7 @@ __device__ __forceinline__ bool key_visible(const MegaArgs& a, int row, int key)
 }
 
 template <int HD, int QPW>
-__device__ void attention_chunk(const MegaArgs& a, const LayerDesc& L, int l, int kvh, int chunk, int nchunks,
+__device__ __noinline__ void attention_chunk(const MegaArgs& a, const LayerDesc& L, int l, int kvh, int chunk, int nchunks,
                                 int qg, int at, float* sq, float* sp, float* skv, float* part, unsigned* acnt,
                                 int* flag) {
     constexpr int QI = 8 * QPW;    // queries per item
@@ -627,9 +628,8 @@ __device__ void attention_chunk(const MegaArgs& a, const LayerDesc& L, int l, in
     const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(HD));
     const float* kbase = L.kc + static_cast<size_t>(kvh) * a.max_len * HD;
     const float* vbase = L.vc + static_cast<size_t>(kvh) * a.max_len * HD;
-    float* sk = skv;                          // [kKeyBlock][C4] float4, column XOR-swizzled by row & 7
-    float* sv = sk + kKeyBlock * HD;          // [kKeyBlock][HD]
-    float* skt = sv + kKeyBlock * HD;         // tail slots [prior, prior + rows): K (swizzled) | V
+    float* sk = skv;                          // 2 x { K [kKeyBlock][C4] float4 (XOR-swizzled by row & 7) | V }
+    float* skt = sk + 4 * kKeyBlock * HD;     // tail slots [prior, prior + rows): K (swizzled) | V
     float* svt = skt + kRows * HD;
     const int q0 = warp * QPW;                // the warp's queries (item-local)
     const int key_l = lane & 15, half = lane >> 4;
@@ -657,13 +657,15 @@ __device__ void attention_chunk(const MegaArgs& a, const LayerDesc& L, int l, in
         for (int j = 0; j < DPL; ++j) o[i][j] = 0.0f;
     }
     float* myp = sp + warp * QPW * kKeyBlock;
-    for (int kb0 = k0; kb0 < k1; kb0 += kKeyBlock) {
-        const int np = max(0, min(kKeyBlock, prior - kb0));  // shared-prefix keys of this block
-        named_sync(3, 256);  // previous block fully consumed
+    // K/V blocks are double buffered: block b+1 streams in while b is scored
+    auto stage = [&](int kb0, int buf) {
+        float* bk = sk + buf * 2 * kKeyBlock * HD;
+        float* bv = bk + kKeyBlock * HD;
+        const int np = max(0, min(kKeyBlock, prior - kb0));
         for (int t = at; t < kKeyBlock * C4; t += 256) {
             const int j = t / C4, c4 = t % C4;
-            float4* dk = reinterpret_cast<float4*>(sk) + j * C4 + (c4 ^ (j & 7));
-            float4* dv = reinterpret_cast<float4*>(sv) + j * C4 + c4;
+            float4* dk = reinterpret_cast<float4*>(bk) + j * C4 + (c4 ^ (j & 7));
+            float4* dv = reinterpret_cast<float4*>(bv) + j * C4 + c4;
             if (j < np) {
                 cp_async16(dk, kbase + static_cast<size_t>(kb0 + j) * HD + 4 * c4);
                 cp_async16(dv, vbase + static_cast<size_t>(kb0 + j) * HD + 4 * c4);
@@ -673,33 +675,60 @@ __device__ void attention_chunk(const MegaArgs& a, const LayerDesc& L, int l, in
             }
         }
         cp_async_commit();
-        cp_async_wait_all();
+    };
+    if (a.trace && at == 0) *tslot(a, blockIdx.x, 5 * l + 2, 12) = gtimer();
+    if (k0 < k1) stage(k0, 0);
+    int buf = 0;
+    for (int kb0 = k0; kb0 < k1; kb0 += kKeyBlock, buf ^= 1) {
+        const int np = max(0, min(kKeyBlock, prior - kb0));  // shared-prefix keys of this block
+        if (kb0 + kKeyBlock < k1) {
+            stage(kb0 + kKeyBlock, buf ^ 1);
+            cp_async_wait_1();
+        } else {
+            cp_async_wait_all();
+        }
         named_sync(3, 256);
+        const float* bk = sk + buf * 2 * kKeyBlock * HD;
+        const float* bv = bk + kKeyBlock * HD;
         if (q0 < nq) {
             const int ci = kb0 + key_l;  // this lane's compacted key index
-            // K row of (query i, lane): shared block or the query row's tail slot
-            auto krow = [&](int i, int& sw) -> const float4* {
-                if (ci < prior) {
-                    sw = key_l & 7;
-                    return reinterpret_cast<const float4*>(sk) + key_l * C4;
-                }
-                const int r = (qbase + q0 + i) / group;
-                const int t = ci - prior < kRows ? sh_tail[r][ci - prior] - prior : 0;
-                sw = t & 7;
-                return reinterpret_cast<const float4*>(skt) + t * C4;
-            };
             float sc[QPW];
 #pragma unroll
-            for (int i = 0; i < QPW; ++i) {
-                sc[i] = 0.0f;
-                int sw;
-                const float4* kr = krow(i, sw);
+            for (int i = 0; i < QPW; ++i) sc[i] = 0.0f;
+            if (np == kKeyBlock) {  // shared prefix: one K row per lane for every query
+                const float4* kr = reinterpret_cast<const float4*>(bk) + key_l * C4;
+                const int sw = key_l & 7;
 #pragma unroll 4
                 for (int c = 0; c < HH / 4; ++c) {
                     const int c4 = half * (HH / 4) + c;
                     const float4 k4 = kr[c4 ^ sw];
-                    const float4 q4 = reinterpret_cast<const float4*>(sq + (q0 + i) * HD)[c4];
-                    sc[i] += q4.x * k4.x + q4.y * k4.y + q4.z * k4.z + q4.w * k4.w;
+#pragma unroll
+                    for (int i = 0; i < QPW; ++i) {
+                        const float4 q4 = reinterpret_cast<const float4*>(sq + (q0 + i) * HD)[c4];
+                        sc[i] += q4.x * k4.x + q4.y * k4.y + q4.z * k4.z + q4.w * k4.w;
+                    }
+                }
+            } else {  // block reaching the rows' tails: K row per query row
+#pragma unroll
+                for (int i = 0; i < QPW; ++i) {
+                    const float4* kr;
+                    int sw;
+                    if (ci < prior) {
+                        kr = reinterpret_cast<const float4*>(bk) + key_l * C4;
+                        sw = key_l & 7;
+                    } else {
+                        const int r = (qbase + q0 + min(i, nq - 1 - q0)) / group;
+                        const int t = ci - prior < kRows ? sh_tail[r][ci - prior] - prior : 0;
+                        kr = reinterpret_cast<const float4*>(skt) + t * C4;
+                        sw = t & 7;
+                    }
+#pragma unroll 4
+                    for (int c = 0; c < HH / 4; ++c) {
+                        const int c4 = half * (HH / 4) + c;
+                        const float4 k4 = kr[c4 ^ sw];
+                        const float4 q4 = reinterpret_cast<const float4*>(sq + (q0 + i) * HD)[c4];
+                        sc[i] += q4.x * k4.x + q4.y * k4.y + q4.z * k4.z + q4.w * k4.w;
+                    }
                 }
             }
 #pragma unroll
@@ -728,7 +757,7 @@ __device__ void attention_chunk(const MegaArgs& a, const LayerDesc& L, int l, in
                 for (int j = 0; j < kKeyBlock; ++j) {
                     float v[DPL];
 #pragma unroll
-                    for (int dd = 0; dd < DPL; ++dd) v[dd] = sv[j * HD + lane + 32 * dd];
+                    for (int dd = 0; dd < DPL; ++dd) v[dd] = bv[j * HD + lane + 32 * dd];
 #pragma unroll
                     for (int i = 0; i < QPW; ++i) {
                         const float pj = myp[i * kKeyBlock + j];
@@ -742,7 +771,7 @@ __device__ void attention_chunk(const MegaArgs& a, const LayerDesc& L, int l, in
 #pragma unroll
                     for (int i = 0; i < QPW; ++i) {
                         const int r = (qbase + q0 + min(i, nq - 1 - q0)) / group;
-                        const float* vr = cj < prior ? sv + j * HD
+                        const float* vr = cj < prior ? bv + j * HD
                                                      : svt + (cj - prior < kRows ? sh_tail[r][cj - prior] - prior : 0) * HD;
                         const float pj = myp[i * kKeyBlock + j];
 #pragma unroll
@@ -751,6 +780,7 @@ __device__ void attention_chunk(const MegaArgs& a, const LayerDesc& L, int l, in
                 }
             }
         }
+        named_sync(3, 256);  // the buffer is restaged two blocks later
     }
     // publish: one chunk -> final values; several -> partials, the last chunk merges
     auto finish = [&](int q, float lsum, const float* ov) {
@@ -765,6 +795,7 @@ __device__ void attention_chunk(const MegaArgs& a, const LayerDesc& L, int l, in
             put_split(a.xim[P_O], f, r, val);
         }
     };
+    if (a.trace && at == 0) *tslot(a, blockIdx.x, 5 * l + 2, 13) = gtimer();
     const int cpk = (a.max_len + kKeyChunk - 1) / kKeyChunk;  // chunk slots per kv head
     const size_t qstride = HD + 2;
     if (nchunks > 1) {
@@ -793,20 +824,39 @@ __device__ void attention_chunk(const MegaArgs& a, const LayerDesc& L, int l, in
         if (!*flag) return;
         __threadfence();
         const float* p0 = part + static_cast<size_t>(kvh) * cpk * 128 * qstride;
-        for (int qi = warp; qi < nq; qi += 8) {  // merge this group's queries, chunks in key order
+        for (int qi = warp; qi < nq; qi += 8) {  // merge this group's queries over the chunks
             const int q = qbase + qi;
-            float M = -INFINITY;
-            for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, __ldcg(p0 + (static_cast<size_t>(ch) * 128 + q) * qstride));
-            float lsum = 0.0f, ov[DPL];
+            // lane ch holds chunk ch's (m, l); all loads in flight together
+            float mc = -INFINITY, lc = 0.0f;
+            if (lane < nchunks) {
+                const float* src = p0 + (static_cast<size_t>(lane) * 128 + q) * qstride;
+                mc = __ldcg(src);
+                lc = __ldcg(src + 1);
+            }
+            float M = mc;
+            for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+            const float w = mc == -INFINITY ? 0.0f : expf(mc - M);
+            float lsum = lc * w;  // fixed butterfly; absent chunks add exact zeros
+            for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+            float ov[DPL];
 #pragma unroll
             for (int dd = 0; dd < DPL; ++dd) ov[dd] = 0.0f;
-            for (int ch = 0; ch < nchunks; ++ch) {
-                const float* src = p0 + (static_cast<size_t>(ch) * 128 + q) * qstride;
-                const float mc = __ldcg(src);
-                const float w = mc == -INFINITY ? 0.0f : expf(mc - M);
-                lsum += __ldcg(src + 1) * w;
+            for (int ch0 = 0; ch0 < nchunks; ch0 += 8) {  // chunks in key order, 8 rows of loads in flight
+                float t8[8][DPL];
 #pragma unroll
-                for (int dd = 0; dd < DPL; ++dd) ov[dd] += __ldcg(src + 2 + lane + 32 * dd) * w;
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int dd = 0; dd < DPL; ++dd)
+                        t8[j][dd] = ch0 + j < nchunks
+                                        ? __ldcg(p0 + (static_cast<size_t>(ch0 + j) * 128 + q) * qstride + 2 + lane + 32 * dd)
+                                        : 0.0f;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float wj = __shfl_sync(0xffffffffu, w, (ch0 + j) & 31);
+                    if (ch0 + j < nchunks)
+#pragma unroll
+                        for (int dd = 0; dd < DPL; ++dd) ov[dd] += t8[j][dd] * wj;
+                }
             }
             finish(q, lsum, ov);
         }
@@ -825,7 +875,7 @@ __device__ void attention_chunk(const MegaArgs& a, const LayerDesc& L, int l, in
 
 // queries per warp for this launch: fewer queries per item (more items) when
 // there are few key chunks.  Numerics do not depend on this choice.
-__device__ __forceinline__ int attn_qpw(const MegaArgs& a, int nchunks) { return nchunks * a.n_kv >= 64 ? 8 : 2; }
+__device__ __forceinline__ int attn_qpw(const MegaArgs& a, int nchunks) { return nchunks * a.n_kv >= 64 ? 4 : 2; }
 
 __device__ __forceinline__ void attention_dispatch(const MegaArgs& a, const LayerDesc& L, int l, int item, int nchunks,
                                                    int at, float* sq, float* sp, float* skv, float* part,
@@ -846,12 +896,12 @@ __device__ __forceinline__ void attention_dispatch(const MegaArgs& a, const Laye
         named_sync(3, 256);
     }
 #define SFG_ATT(HDV, Q) attention_chunk<HDV, Q>(a, L, l, kvh, chunk, nchunks, qg, at, sq, sp, skv, part, acnt, flag)
-    if (qpw == 8) {
+    if (qpw == 4) {
         switch (a.hd) {
-            case 64: SFG_ATT(64, 8); break;
-            case 128: SFG_ATT(128, 8); break;
-            case 160: SFG_ATT(160, 8); break;
-            default: SFG_ATT(32, 8); break;
+            case 64: SFG_ATT(64, 4); break;
+            case 128: SFG_ATT(128, 4); break;
+            case 160: SFG_ATT(160, 4); break;
+            default: SFG_ATT(32, 4); break;
         }
     } else {
         switch (a.hd) {
@@ -907,7 +957,7 @@ __device__ __forceinline__ void cursor_prefetch_next(const MegaArgs& a, int c, C
 // shared-memory floats of the attention scratch: the larger of the two layouts
 __host__ __device__ __forceinline__ int attn_scratch_floats(bool rows_attn, int hd, int group, int max_len) {
     return rows_attn ? kMaxGroup * hd + 8 * kMaxGroup * 2 + 8 * group * hd + max_len
-                     : 64 * hd + 8 * 8 * kKeyBlock + 4 * kKeyBlock * hd;
+                     : 32 * hd + 8 * 4 * kKeyBlock + 4 * kKeyBlock * hd + 2 * kRows * hd;
 }
 
 // ── the kernel ────────────────────────────────────────────────────────────
@@ -928,9 +978,9 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
     float* xch = reinterpret_cast<float*>(flag + 4);          // 64*16 gate|up + 4*16 sumsq
     float* rs = xch + 64 * kRows + 4 * kRows;                  // [16] per-row 1/rms of the phase
     // attention scratch, one of two layouts (MegaArgs::attn_rows):
-    float* sq = rs + kRows;                                    // chunked: [64 queries][hd] queries
-    float* sp = sq + 64 * a.hd;                                //   [8 warps][8][kKeyBlock] probabilities
-    float* skv = sp + 8 * 8 * kKeyBlock;                       //   staged K | V block + tail slots
+    float* sq = rs + kRows;                                    // chunked: [32 queries][hd] queries
+    float* sp = sq + 32 * a.hd;                                //   [8 warps][4][kKeyBlock] probabilities
+    float* skv = sp + 8 * 4 * kKeyBlock;                       //   2 staged K | V blocks + tail slots
     float* qs = rs + kRows;                                    // per-row: [group][hd] queries
     float* wst = qs + kMaxGroup * a.hd;                        //   [8][kMaxGroup][2] warp stats
     float* ocomb = wst + 8 * kMaxGroup * 2;                    //   [8][group][hd] warp partials

@@ -23,16 +23,17 @@ eng = sfg.Engine(sfg.ModelConfig(**{k: getattr(cfg, k) for k in po.ModelCfg.__da
                  layers=(2, 2 + NL), with_embedding=False, with_head=False)
 bank = eng.bank(2, 2 + NL)
 rng = np.random.default_rng(0)
-h = (rng.standard_normal((24, 4096)) * 0.5).astype(np.float32)
-eng.forward_layers(2, 2 + NL, h, list(range(24)), bank)
-bank.mark_committed(24)
+PRIOR = int(os.environ.get("PRIOR", "24"))
+h = (rng.standard_normal((PRIOR, 4096)) * 0.5).astype(np.float32)
+eng.forward_layers(2, 2 + NL, h, list(range(PRIOR)), bank)
+bank.mark_committed(PRIOR)
 L.sfg_debug_mega_trace(1)
 h16 = (rng.standard_normal((16, 4096)) * 0.5).astype(np.float32)
 times = []
 for it in range(4):
-    bank.crop(24)
+    bank.crop(PRIOR)
     t0 = time.perf_counter()
-    eng.forward_layers(2, 2 + NL, h16, list(range(24, 40)), bank)
+    eng.forward_layers(2, 2 + NL, h16, list(range(PRIOR, PRIOR + 16)), bank)
     times.append(time.perf_counter() - t0)
 print("wall per forward (ms):", [round(t * 1000, 3) for t in times])
 G = 148
@@ -91,3 +92,12 @@ for l in range(1, NL - 1):
         tot += s1 - s0
         over_tot += s1 - s0 - ideal
 print(f"per layer: {tot / (NL - 2):.1f} us, overhead {over_tot / (NL - 2):.1f} us")
+# attention items (chunked design): start of the key walk (12) and its end (13)
+for l in range(1, NL - 1):
+    bid = 5 * l + 2
+    st, en = tr[:, bid, 12], tr[:, bid, 13]
+    m = (st > 0) & (en > 0)
+    if m.any():
+        d = (en[m] - st[m]) / 1000
+        print(f"L{l} attention key walk per CTA: median {np.median(d):.1f} us max {d.max():.1f} us over {m.sum()} CTAs;"
+              f" first start {(st[m].min() - t0) / 1000:.1f} last end {(en[m].max() - t0) / 1000:.1f}")
