@@ -109,6 +109,17 @@ int32_t sfg_engine_create_seeded(const sfg_model_config* cfg, const sfg_engine_o
  * (PROTOCOL.md "Weight snapshots"; tinyformer.cpp:83-98).                    */
 int32_t sfg_engine_create_from_params(const sfg_model_config* cfg, const sfg_engine_options* opt,
                                       const float* params, sfg_engine** out);
+/* Tensor parallelism (configs[3]: NeMo-12B at TP=2): `tp_size`
+ * engines, one process and GPU each, every engine holding 1/tp_size of each
+ * layer's heads (QKV, O) and FFN columns (gate|up, down).  Row-parallel
+ * outputs are summed with an NCCL all-reduce over NVLink (2 per layer).
+ * Rank 0 creates the group id with sfg_tp_unique_id and shares its
+ * SFG_TP_ID_BYTES with the other ranks (e.g. torch.distributed broadcast).
+ * FAST math only; every rank must run the same calls in the same order.     */
+enum { SFG_TP_ID_BYTES = 128 };
+int32_t sfg_tp_unique_id(uint8_t* out /* SFG_TP_ID_BYTES */);
+int32_t sfg_engine_create_tp(const sfg_model_config* cfg, const sfg_engine_options* opt, int32_t tp_size,
+                             int32_t tp_rank, const uint8_t* tp_unique_id, sfg_engine** out);
 void sfg_engine_destroy(sfg_engine* eng);
 /* bytes of device memory held by the engine's weights */
 int64_t sfg_engine_weight_bytes(const sfg_engine* eng);

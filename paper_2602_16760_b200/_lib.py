@@ -100,6 +100,9 @@ def lib() -> C.CDLL:
         "sfg_engine_create_from_params": (i32, [C.POINTER(ModelConfig), C.POINTER(EngineOptions), f32p,
                                                 C.POINTER(vp)]),
         "sfg_engine_destroy": (None, [vp]),
+        "sfg_tp_unique_id": (i32, [C.POINTER(C.c_uint8)]),
+        "sfg_engine_create_tp": (i32, [C.POINTER(ModelConfig), C.POINTER(EngineOptions), i32, i32,
+                                       C.POINTER(C.c_uint8), C.POINTER(vp)]),
         "sfg_engine_weight_bytes": (C.c_int64, [vp]),
         "sfg_bank_create": (i32, [vp, i32, i32, C.POINTER(vp)]),
         "sfg_bank_destroy": (None, [vp]),

@@ -49,12 +49,12 @@ const char* sfg_last_error(void) { return g_err.c_str(); }
 const char* sfg_version(void) { return "sfg 0.1 (sm_100a)"; }
 
 static int32_t make_engine(const sfg_model_config* cfg, const sfg_engine_options* opt, const float* params,
-                           sfg_engine** out) {
+                           sfg_engine** out, const TpConfig& tp = TpConfig{}) {
     SFG_GUARD({
         if (!cfg || !opt || !out) throw Error(Kind::input, "null argument");
         auto* h = new sfg_engine;
         try {
-            h->e = std::make_unique<Engine>(ModelCfg::from_c(*cfg), *opt, params);
+            h->e = std::make_unique<Engine>(ModelCfg::from_c(*cfg), *opt, params, tp);
         } catch (...) {
             delete h;
             throw;
@@ -73,6 +73,20 @@ int32_t sfg_engine_create_from_params(const sfg_model_config* cfg, const sfg_eng
         return SFG_ERR_INPUT;
     }
     return make_engine(cfg, opt, params, out);
+}
+int32_t sfg_tp_unique_id(uint8_t* out) {
+    SFG_GUARD({
+        if (!out) throw Error(Kind::input, "null argument");
+        tp_unique_id(out, SFG_TP_ID_BYTES);
+    })
+}
+int32_t sfg_engine_create_tp(const sfg_model_config* cfg, const sfg_engine_options* opt, int32_t tp_size,
+                             int32_t tp_rank, const uint8_t* tp_unique_id, sfg_engine** out) {
+    TpConfig tp;
+    tp.size = tp_size;
+    tp.rank = tp_rank;
+    tp.unique_id = tp_unique_id;
+    return make_engine(cfg, opt, nullptr, out, tp);
 }
 void sfg_engine_destroy(sfg_engine* eng) { delete eng; }
 int64_t sfg_engine_weight_bytes(const sfg_engine* eng) { return eng ? eng->e->weight_bytes() : 0; }

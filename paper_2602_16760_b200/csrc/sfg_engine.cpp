@@ -310,8 +310,9 @@ void Bank::read_kv(int layer, int head, int pos, float* k, float* v) {
 // ── engine: weights ───────────────────────────────────────────────────────
 Dims Engine::dims() const {
     const ModelCfg& c = cfg_;
-    return Dims{c.hidden_dim, c.q_dim(), c.kv_dim(), c.ffn_dim, c.vocab_size, c.n_heads,
-                c.n_kv_heads, c.head_dim, c.max_seq_len, c.rms_eps};
+    const int t = tp_size_;
+    return Dims{c.hidden_dim, c.q_dim() / t, c.kv_dim() / t, c.ffn_dim / t, c.vocab_size, c.n_heads / t,
+                c.n_kv_heads / t, c.head_dim, c.max_seq_len, c.rms_eps};
 }
 
 static float bf16_rne_host(float v) {
@@ -324,9 +325,16 @@ static float bf16_rne_host(float v) {
     return v;
 }
 
-Engine::Engine(const ModelCfg& cfg, const sfg_engine_options& opt, const float* params)
-    : cfg_(cfg), opt_(opt) {
+Engine::Engine(const ModelCfg& cfg, const sfg_engine_options& opt, const float* params, const TpConfig& tp)
+    : cfg_(cfg), opt_(opt), tp_size_(tp.size), tp_rank_(tp.rank) {
     cfg_.validate();
+    if (tp_size_ < 1 || tp_rank_ < 0 || tp_rank_ >= tp_size_) throw Error(Kind::config, "invalid tensor-parallel rank");
+    if (tp_size_ > 1) {
+        if (opt_.math != SFG_MATH_FAST) throw Error(Kind::config, "tensor parallelism runs FAST math");
+        if (cfg_.n_kv_heads % tp_size_ || cfg_.ffn_dim % (64 * tp_size_) || (cfg_.q_dim() / tp_size_) % 64)
+            throw Error(Kind::config, "kv heads, ffn_dim/64 and q_dim/64 must split evenly over the tensor-parallel group");
+        if (!tp.unique_id) throw Error(Kind::input, "tensor parallelism needs the group's NCCL unique id");
+    }
     if (opt_.layer_begin < 0 || opt_.layer_end > cfg_.n_layers || opt_.layer_begin > opt_.layer_end)
         throw Error(Kind::config, "hosted layer range must lie inside the model");
     if (opt_.math != SFG_MATH_EXACT && opt_.math != SFG_MATH_FAST)
@@ -338,6 +346,7 @@ Engine::Engine(const ModelCfg& cfg, const sfg_engine_options& opt, const float* 
         throw Error(Kind::internal, "no CUDA device: the B200 engine has no CPU fallback");
     if (opt_.device < 0 || opt_.device >= ndev) throw Error(Kind::config, "CUDA device ordinal out of range");
     DeviceGuard g(opt_.device);
+    if (tp_size_ > 1) tp_comm_ = tp_comm_init(tp_size_, tp_rank_, tp.unique_id);
     cudaDeviceProp prop{};
     SFG_CUDA(cudaGetDeviceProperties(&prop, opt_.device));
     if (prop.major != 10) throw Error(Kind::internal, "libsfg is built for sm_100a (B200) only");
@@ -364,6 +373,11 @@ Engine::~Engine() {
     if (rope_cos_) cudaFree(rope_cos_);
     if (rope_sin_) cudaFree(rope_sin_);
     cudaStreamDestroy(stream_);
+    tp_comm_destroy(tp_comm_);
+}
+
+void Engine::tp_allreduce(float* buf, size_t n, cudaStream_t s) {
+    if (tp_size_ > 1) tp_allreduce_sum(tp_comm_, buf, n, s);
 }
 
 // Upload n fp32 values (already on device staging) into storage dtype `wt`.
@@ -519,7 +533,7 @@ void Engine::build_fast_layouts() {
         fast_build_layer(*this, L, stream_);
         SFG_CUDA(cudaStreamSynchronize(stream_));
         const size_t H = cfg_.hidden_dim, qd = cfg_.q_dim(), kvd = cfg_.kv_dim(), F = cfg_.ffn_dim;
-        weight_bytes_ -= static_cast<int64_t>(2 * (H * qd + 2 * H * kvd + qd * H + 3 * H * F));
+        weight_bytes_ -= static_cast<int64_t>(2 * (H * qd + 2 * H * kvd + qd * H + 3 * H * F));  // full copies released
         release(L.wq);
         release(L.wk);
         release(L.wv);
@@ -553,7 +567,8 @@ int Engine::forward_device(Bank& b, int lb, int le, int rows, Workspace& ws, cud
     const int prior = b.len();
     int n = 0;
     if (lb >= le) return 0;
-    if (fast() && mega_env_enabled() && le - lb <= 50 && mega_supported(*this, rows, ws.additive_mask)) {
+    if (fast() && tp_size_ == 1 && mega_env_enabled() && le - lb <= 50 &&
+        mega_supported(*this, rows, ws.additive_mask)) {
         for (int layer = lb; layer < le; ++layer)
             if (!layers_[layer].hosted) throw Error(Kind::internal, "layer not hosted by this engine");
         return mega_forward(*this, b, lb, le, rows, ws, s);

@@ -182,9 +182,20 @@ MaskRuns runs_from_dense(const float* mask, int rows, int kv);
 // [0, prior) with mask value 0 (causal, lookahead and branch masks do).
 bool mega_mask_ok(const MaskRuns& mr, int prior);
 
+// Tensor parallelism over NCCL (sfg_tp.cpp): a group of `size` engines, one
+// per GPU, each holding 1/size of every layer's heads and FFN columns.
+struct TpConfig {
+    int size = 1, rank = 0;
+    const uint8_t* unique_id = nullptr;  // ncclUniqueId bytes (same on every rank)
+};
+void tp_unique_id(uint8_t* out, size_t n);
+void* tp_comm_init(int size, int rank, const uint8_t* uid);
+void tp_comm_destroy(void* comm);
+void tp_allreduce_sum(void* comm, float* buf, size_t n, cudaStream_t s);
+
 class Engine {
 public:
-    Engine(const ModelCfg& cfg, const sfg_engine_options& opt, const float* params);
+    Engine(const ModelCfg& cfg, const sfg_engine_options& opt, const float* params, const TpConfig& tp = TpConfig{});
     ~Engine();
 
     const ModelCfg& cfg() const { return cfg_; }
@@ -193,7 +204,13 @@ public:
     bool fast() const { return opt_.math == SFG_MATH_FAST; }
     int wt() const { return opt_.weight_dtype == SFG_WEIGHTS_F32 ? W_F32 : W_BF16; }
     int64_t weight_bytes() const { return weight_bytes_; }
+    // dims of THIS engine's shard: with tensor parallelism q/kv heads and the
+    // FFN width are the local 1/tp slice (hidden_dim stays whole)
     Dims dims() const;
+    int tp_size() const { return tp_size_; }
+    int tp_rank() const { return tp_rank_; }
+    // in-place sum over the tensor-parallel group (no-op at tp == 1)
+    void tp_allreduce(float* buf, size_t n, cudaStream_t s);
     const LayerWeights& layer(int i) const { return layers_[i]; }
 
     // Ensure ws holds `rows` rows / `runs` runs / `logit_rows` logit rows.
@@ -248,6 +265,8 @@ private:
     cudaStream_t stream_ = nullptr;
     Workspace ws_;
     std::mutex mu_;
+    int tp_size_ = 1, tp_rank_ = 0;
+    void* tp_comm_ = nullptr;
 };
 
 // Process-wide switch: capture/replay the device part of decode steps as

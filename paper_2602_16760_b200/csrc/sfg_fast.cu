@@ -56,7 +56,9 @@ struct GemmArgs {
     float* partials;    // [tiles][kMaxPieces][kRows][kM]
     int* counters;      // [tiles]
     int rows, row0;     // valid rows of this pass, global row offset
-    // EPI_RESID: out[(row0+r)*ld + f] += y
+    // EPI_RESID: out[(row0+r)*ld + f] += y   (store_only: = y, a tensor-parallel
+    // rank's partial that the all-reduce adds to rank 0's h + partial)
+    int store_only;
     // EPI_GATEUP: out[(row0+r)*ld + f] = silu(g)*u
     // EPI_HEAD: out (nullable) logits [(row0+r)*ld + f]
     float* out;
@@ -168,7 +170,7 @@ __device__ __forceinline__ void final_epilogue(const GemmArgs& a, int tile, int 
             for (int r = 0; r < kRows; ++r)
                 if (r < a.rows) {
                     float* o = a.out + static_cast<size_t>(a.row0 + r) * a.ld + f;
-                    *o = *o + y[r];
+                    *o = a.store_only ? y[r] : *o + y[r];
                 }
     } else if constexpr (EPI == EPI_QKV) {
         // features: [0,qd) q | [qd, qd+kvd) k | [qd+kvd, qd+2kvd) v; RoPE pairs
@@ -518,9 +520,11 @@ __global__ void head_argmax_kernel(const float* __restrict__ val, const int32_t*
 // ── weight re-layout: reference [K x N] (row-major, in x out) -> tiled SW128 W^T
 // kind 0: plain (feature f = tile*128 + m from src0 with ld n0)
 // kind 1: q|k|v concat   kind 2: gate/up interleave (64 + 64 per tile)
+// s0/s1/s2 are [K x ld] reference-layout matrices; the first n columns are
+// taken (ld > n: a tensor-parallel column slice, the pointer pre-offset)
 __global__ void relayout_kernel(const __nv_bfloat16* __restrict__ s0, const __nv_bfloat16* __restrict__ s1,
-                                const __nv_bfloat16* __restrict__ s2, int n0, int n1, int n2, int kind, int K,
-                                int tiles, uint8_t* __restrict__ dst) {
+                                const __nv_bfloat16* __restrict__ s2, int n0, int n1, int n2, int ld0, int ld1,
+                                int ld2, int kind, int K, int tiles, uint8_t* __restrict__ dst) {
     const int KB = K / kKB;
     const size_t total = static_cast<size_t>(tiles) * KB * kM * kKB;
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
@@ -536,15 +540,15 @@ __global__ void relayout_kernel(const __nv_bfloat16* __restrict__ s0, const __nv
         __nv_bfloat16 v = __float2bfloat16_rn(0.0f);
         if (kind == 0) {
             const int f = t * kM + m;
-            if (f < n0) v = s0[static_cast<size_t>(k) * n0 + f];
+            if (f < n0) v = s0[static_cast<size_t>(k) * ld0 + f];
         } else if (kind == 1) {
             const int f = t * kM + m;
-            if (f < n0) v = s0[static_cast<size_t>(k) * n0 + f];
-            else if (f < n0 + n1) v = s1[static_cast<size_t>(k) * n1 + (f - n0)];
-            else if (f < n0 + n1 + n2) v = s2[static_cast<size_t>(k) * n2 + (f - n0 - n1)];
+            if (f < n0) v = s0[static_cast<size_t>(k) * ld0 + f];
+            else if (f < n0 + n1) v = s1[static_cast<size_t>(k) * ld1 + (f - n0)];
+            else if (f < n0 + n1 + n2) v = s2[static_cast<size_t>(k) * ld2 + (f - n0 - n1)];
         } else {
             const int f = t * 64 + (m & 63);
-            if (f < n0) v = (m < 64 ? s0 : s1)[static_cast<size_t>(k) * n0 + f];
+            if (f < n0) v = (m < 64 ? s0 : s1)[static_cast<size_t>(k) * ld0 + f];
         }
         uint8_t* tileb = dst + (static_cast<size_t>(t) * KB + kb) * kABytes;
         *reinterpret_cast<__nv_bfloat16*>(tileb + sw128_off(m, kk)) = v;
@@ -632,26 +636,37 @@ static void check_fast_shape(const ModelCfg& c) {
 }
 
 static void* relayout(Engine& e, const void* s0, const void* s1, const void* s2, int n0, int n1, int n2, int kind,
-                      int K, int tiles, cudaStream_t s) {
+                      int K, int tiles, cudaStream_t s, int ld0 = 0, int ld1 = 0, int ld2 = 0) {
     void* dst = nullptr;
     const size_t bytes = static_cast<size_t>(tiles) * (K / kKB) * kABytes;
     SFG_CUDA(cudaMalloc(&dst, bytes));
     relayout_kernel<<<2048, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(s0), static_cast<const __nv_bfloat16*>(s1),
-                                         static_cast<const __nv_bfloat16*>(s2), n0, n1, n2, kind, K, tiles,
-                                         static_cast<uint8_t*>(dst));
+                                         static_cast<const __nv_bfloat16*>(s2), n0, n1, n2, ld0 ? ld0 : n0,
+                                         ld1 ? ld1 : n1, ld2 ? ld2 : n2, kind, K, tiles, static_cast<uint8_t*>(dst));
     SFG_CUDA(cudaGetLastError());
     e.adopt(dst, bytes);
     return dst;
 }
 
+// Tensor parallelism: QKV and gate|up are split by output columns (whole
+// heads / FFN columns), O and down by input rows; rank r takes slice r.
 void fast_build_layer(Engine& e, LayerWeights& L, cudaStream_t s) {
     const ModelCfg& c = e.cfg();
     check_fast_shape(c);
     const int H = c.hidden_dim, qd = c.q_dim(), kvd = c.kv_dim(), F = c.ffn_dim;
-    L.f_qkv = relayout(e, L.wq, L.wk, L.wv, qd, kvd, kvd, 1, H, tiles_for(qd + 2 * kvd), s);
-    L.f_o = relayout(e, L.wo, nullptr, nullptr, H, 0, 0, 0, qd, tiles_for(H), s);
-    L.f_gu = relayout(e, L.w_gate, L.w_up, nullptr, F, 0, 0, 2, H, (F + 63) / 64, s);
-    L.f_down = relayout(e, L.w_down, nullptr, nullptr, H, 0, 0, 0, F, tiles_for(H), s);
+    const int t = e.tp_size(), r = e.tp_rank();
+    const int ql = qd / t, kl = kvd / t, fl = F / t;
+    const auto* wq = static_cast<const __nv_bfloat16*>(L.wq) + static_cast<size_t>(r) * ql;
+    const auto* wk = static_cast<const __nv_bfloat16*>(L.wk) + static_cast<size_t>(r) * kl;
+    const auto* wv = static_cast<const __nv_bfloat16*>(L.wv) + static_cast<size_t>(r) * kl;
+    const auto* wo = static_cast<const __nv_bfloat16*>(L.wo) + static_cast<size_t>(r) * ql * H;
+    const auto* wg = static_cast<const __nv_bfloat16*>(L.w_gate) + static_cast<size_t>(r) * fl;
+    const auto* wu = static_cast<const __nv_bfloat16*>(L.w_up) + static_cast<size_t>(r) * fl;
+    const auto* wd = static_cast<const __nv_bfloat16*>(L.w_down) + static_cast<size_t>(r) * fl * H;
+    L.f_qkv = relayout(e, wq, wk, wv, ql, kl, kl, 1, H, tiles_for(ql + 2 * kl), s, qd, kvd, kvd);
+    L.f_o = relayout(e, wo, nullptr, nullptr, H, 0, 0, 0, ql, tiles_for(H), s);
+    L.f_gu = relayout(e, wg, wu, nullptr, fl, 0, 0, 2, H, (fl + 63) / 64, s, F);
+    L.f_down = relayout(e, wd, nullptr, nullptr, H, 0, 0, 0, fl, tiles_for(H), s);
 }
 
 void* fast_build_head(Engine& e, const void* lm_head, cudaStream_t s) {
@@ -733,10 +748,13 @@ int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, i
         a.n_out = d.H;
         a.out = ws.h;
         a.ld = d.H;
+        a.store_only = e.tp_rank() > 0;  // rank 0 adds the residual, the others their partial
         {
             ProfScope ps(K_OPROJ, s, 2.0 * d.qd * d.H + 4.0 * pr * (d.qd + 2.0 * d.H), 2.0 * pr * d.qd * d.H);
             launch_gemm<EPI_RESID>(a, grid_for(a.tiles, a.KB), s);
         }
+        e.tp_allreduce(ws.h + static_cast<size_t>(p0) * d.H, static_cast<size_t>(pr) * d.H, s);
+        a.store_only = 0;
         // FFN RMSNorm + split, gate|up + SiLU*up
         prep_kernel<<<pr, kPrepThreads, 0, s>>>(ws.h + static_cast<size_t>(p0) * d.H, d.H, d.H, L.ffn_norm, d.eps, f.xs);
         a.W = static_cast<const uint8_t*>(L.f_gu);
@@ -757,10 +775,13 @@ int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, i
         a.n_out = d.H;
         a.out = ws.h;
         a.ld = d.H;
+        a.store_only = e.tp_rank() > 0;
         {
             ProfScope ps(K_DOWN, s, 2.0 * d.F * d.H + 4.0 * pr * (d.F + 2.0 * d.H), 2.0 * pr * d.F * d.H);
             launch_gemm<EPI_RESID>(a, grid_for(a.tiles, a.KB), s);
         }
+        e.tp_allreduce(ws.h + static_cast<size_t>(p0) * d.H, static_cast<size_t>(pr) * d.H, s);
+        a.store_only = 0;
         n += 6;
     }
     SFG_CUDA(cudaGetLastError());

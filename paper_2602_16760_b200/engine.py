@@ -67,12 +67,22 @@ class ModelConfig:
         return cls(**{k: getattr(c, k) for k in cls.__dataclass_fields__})
 
 
+def tp_unique_id() -> bytes:
+    """A fresh NCCL group id for a tensor-parallel engine group (rank 0 makes
+    it and shares it with the other ranks)."""
+    buf = (C.c_uint8 * 128)()
+    check(_lib.lib().sfg_tp_unique_id(buf))
+    return bytes(buf)
+
+
 class Engine:
     """Weights of a layer range resident on one B200."""
 
     def __init__(self, cfg, math: int = EXACT, weights: str = "bf16", layers: tuple | None = None,
                  with_embedding: bool = True, with_head: bool = True, device: int = 0,
-                 params: np.ndarray | None = None):
+                 params: np.ndarray | None = None, tp: tuple | None = None):
+        """tp = (size, rank, unique_id bytes): this engine is rank `rank` of a
+        tensor-parallel group (see tp_unique_id; FAST math, seeded weights)."""
         self.cfg = ModelConfig.from_any(cfg)
         L = _lib.lib()
         lb, le = layers if layers is not None else (0, self.cfg.n_layers)
@@ -80,7 +90,12 @@ class Engine:
                                  int(with_head))
         h = C.c_void_p()
         cc = self.cfg.to_c()
-        if params is None:
+        if tp is not None and tp[0] > 1:
+            if params is not None:
+                raise ValueError("tensor-parallel engines take the seeded weights")
+            uid = (C.c_uint8 * 128).from_buffer_copy(bytes(tp[2]))
+            check(L.sfg_engine_create_tp(C.byref(cc), C.byref(opt), int(tp[0]), int(tp[1]), uid, C.byref(h)))
+        elif params is None:
             check(L.sfg_engine_create_seeded(C.byref(cc), C.byref(opt), C.byref(h)))
         else:
             p = _f32(params)
