@@ -217,7 +217,9 @@ def config_dict(args, ws):
             "model_shape": SHAPE_TEXT[args.model], "rows_per_step": 16,
             "prompt_len": PROMPT_LEN, "rtt_ms": args.rtt_ms, "math": args.math, "wire": "f16",
             "attention": os.environ.get("SFG_ATTN", "rows"),
-            "sessions_per_gpu": 1, "parallelism": f"replicas x{ws} (independent sessions)",
+            "sessions_per_gpu": 1 if args.tp == 1 else 1.0 / args.tp,
+            "parallelism": f"replicas x{ws} (independent sessions)" if args.tp == 1 else
+                           f"tp{args.tp} (one session, NCCL all-reduce of O/down over NVLink)",
             "l2": "inputs larger than L2 (the middle-layer weights, >10 GB, are streamed every step)"}
 
 
@@ -247,7 +249,19 @@ def run_ours(args, ws, rank, local):
     math = sfg.FAST if args.math == "fast" else sfg.EXACT
     cfg = sfg.ModelConfig(**MODEL)
     t0 = time.time()
-    eng = sfg.Engine(cfg, math=math, device=local)
+    if args.tp > 1:
+        # one tensor-parallel group over all ranks: rank 0 makes the NCCL id
+        if ws != args.tp:
+            raise SystemExit("--tp N runs as one group: launch exactly N ranks")
+        import torch
+        import torch.distributed as dist
+        buf = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(sfg.tp_unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, src=0)
+        eng = sfg.Engine(cfg, math=math, device=local, tp=(args.tp, rank, bytes(buf.cpu().numpy().tobytes())))
+    else:
+        eng = sfg.Engine(cfg, math=math, device=local)
     t_init = time.time() - t0
     nl = cfg.n_layers
     srv = sfg.ServerEngine(eng, sfg.ServerConfig(SPLIT, nl - SPLIT, max_sessions=64))
@@ -303,7 +317,8 @@ def run_ours(args, ws, rank, local):
     barrier(ws, local)
     dev_total = sum(dev_ms) / 1000.0
     dev_total_max = barrier_max(ws, local, dev_total)
-    toks_all = dist_sum(ws, local, float(toks))
+    # tensor parallelism: the ranks cooperate on ONE session (count it once)
+    toks_all = dist_sum(ws, local, float(toks)) / max(1, args.tp)
     stats = {}
     for ci, name in enumerate(KCLASS):
         cnt, ms, by, fl = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
@@ -326,7 +341,7 @@ def run_ours(args, ws, rank, local):
         ebatch.append(b)
     e_wall = time.perf_counter() - te
     e_wall_max = barrier_max(ws, local, e_wall)
-    etoks_all = dist_sum(ws, local, float(etoks))
+    etoks_all = dist_sum(ws, local, float(etoks)) / max(1, args.tp)
     L.sfg_decoder_destroy(fdec)
 
     # ── RTT sweep on the device-linked path (SimChannel semantics) ───────
@@ -383,7 +398,8 @@ def run_ours(args, ws, rank, local):
     line = {
         "metric": "lookahead step latency (ms) & tok/s at Mistral-7B shape vs HBM roofline",
         "value": toks_all / dev_total_max, "unit": "tok/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "weak" if args.tp == 1 else "strong",
         "vs_baseline": None, "dtype": "bf16" if args.math == "fast" else "f32", "data": "synthetic",
         "config": config_dict(args, ws),
         "e2e": {"value": etoks_all / e_wall_max, "unit": "tok/s", "h2d_bytes_per_step": h2d,
@@ -430,6 +446,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--math", default="fast", choices=["fast", "exact"])
     ap.add_argument("--model", default="7b", choices=sorted(MODELS))
+    ap.add_argument("--tp", type=int, default=1, help="tensor-parallel group size (configs[3]: --model 12b --tp 2)")
     ap.add_argument("--rtt-ms", type=float, default=0.0)
     ap.add_argument("--prompt-len", type=int, default=PROMPT_LEN,
                     help="KV context before the first step (configs[4]: 2048)")

@@ -363,6 +363,37 @@ Engine::Engine(const ModelCfg& cfg, const sfg_engine_options& opt, const float* 
     }
     if (staging_) cudaFree(staging_);
     staging_ = nullptr;
+    if (tp_size_ == 2 && fast()) tp_setup_peer();
+}
+
+// Allocate this rank's inbox, share its CUDA IPC handle over the NCCL group
+// and map the peer's (TP = 2: one peer over NVLink).
+void Engine::tp_setup_peer() {
+    const ModelCfg& c = cfg_;
+    const size_t tilesH = (c.hidden_dim + 127) / 128;
+    tp_peer_.data_floats = static_cast<size_t>(c.n_layers) * 2 * tilesH * 16 * 128;
+    const size_t nflags = static_cast<size_t>(c.n_layers) * 2 * tilesH;
+    const size_t bytes = tp_peer_.data_floats * sizeof(float) + nflags * sizeof(unsigned) + 256;
+    SFG_CUDA(cudaMalloc(&tp_peer_.base, bytes));
+    SFG_CUDA(cudaMemset(tp_peer_.base, 0, bytes));
+    SFG_CUDA(cudaMalloc(&tp_peer_.epoch, sizeof(unsigned)));
+    SFG_CUDA(cudaMemset(tp_peer_.epoch, 0, sizeof(unsigned)));
+    tp_peer_.inbox = static_cast<float*>(tp_peer_.base);
+    tp_peer_.inflag = reinterpret_cast<unsigned*>(tp_peer_.inbox + tp_peer_.data_floats);
+    cudaIpcMemHandle_t mine{};
+    SFG_CUDA(cudaIpcGetMemHandle(&mine, tp_peer_.base));
+    void* dev = nullptr;
+    SFG_CUDA(cudaMalloc(&dev, 2 * sizeof(cudaIpcMemHandle_t) + sizeof(cudaIpcMemHandle_t)));
+    char* all = static_cast<char*>(dev) + sizeof(cudaIpcMemHandle_t);
+    SFG_CUDA(cudaMemcpy(dev, &mine, sizeof(mine), cudaMemcpyHostToDevice));
+    tp_allgather_bytes(tp_comm_, dev, all, sizeof(cudaIpcMemHandle_t), stream_);
+    SFG_CUDA(cudaStreamSynchronize(stream_));
+    cudaIpcMemHandle_t handles[2];
+    SFG_CUDA(cudaMemcpy(handles, all, sizeof(handles), cudaMemcpyDeviceToHost));
+    cudaFree(dev);
+    SFG_CUDA(cudaIpcOpenMemHandle(&tp_peer_.peer_base, handles[1 - tp_rank_], cudaIpcMemLazyEnablePeerAccess));
+    tp_peer_.peer_inbox = static_cast<float*>(tp_peer_.peer_base);
+    tp_peer_.peer_inflag = reinterpret_cast<unsigned*>(tp_peer_.peer_inbox + tp_peer_.data_floats);
 }
 
 Engine::~Engine() {
@@ -373,6 +404,9 @@ Engine::~Engine() {
     if (rope_cos_) cudaFree(rope_cos_);
     if (rope_sin_) cudaFree(rope_sin_);
     cudaStreamDestroy(stream_);
+    if (tp_peer_.peer_base) cudaIpcCloseMemHandle(tp_peer_.peer_base);
+    if (tp_peer_.base) cudaFree(tp_peer_.base);
+    if (tp_peer_.epoch) cudaFree(tp_peer_.epoch);
     tp_comm_destroy(tp_comm_);
 }
 
@@ -567,7 +601,7 @@ int Engine::forward_device(Bank& b, int lb, int le, int rows, Workspace& ws, cud
     const int prior = b.len();
     int n = 0;
     if (lb >= le) return 0;
-    if (fast() && tp_size_ == 1 && mega_env_enabled() && le - lb <= 50 &&
+    if (fast() && (tp_size_ == 1 || tp_peer_.peer_inbox) && mega_env_enabled() && le - lb <= 50 &&
         mega_supported(*this, rows, ws.additive_mask)) {
         for (int layer = lb; layer < le; ++layer)
             if (!layers_[layer].hosted) throw Error(Kind::internal, "layer not hosted by this engine");

@@ -192,6 +192,22 @@ void tp_unique_id(uint8_t* out, size_t n);
 void* tp_comm_init(int size, int rank, const uint8_t* uid);
 void tp_comm_destroy(void* comm);
 void tp_allreduce_sum(void* comm, float* buf, size_t n, cudaStream_t s);
+void tp_allgather_bytes(void* comm, const void* src, void* dst, size_t n, cudaStream_t s);
+
+// Peer-memory exchange for the layer-stack megakernel at TP=2: each rank owns
+// an inbox (row-parallel partial tiles + epoch flags) that the peer writes
+// over NVLink (CUDA IPC mapping), so the O / down all-reduce happens inside
+// the producing tile's epilogue instead of as a separate collective.
+struct TpPeer {
+    float* inbox = nullptr;          // mine: [layers][2][tilesH][16][128] partial tiles
+    unsigned* inflag = nullptr;      // mine: [layers][2][tilesH] epoch flags
+    float* peer_inbox = nullptr;     // the peer's, mapped
+    unsigned* peer_inflag = nullptr;
+    unsigned* epoch = nullptr;       // launch counter (device), bumped by each launch's last CTA
+    void* base = nullptr;            // my allocation
+    void* peer_base = nullptr;       // the peer's mapping
+    size_t data_floats = 0;
+};
 
 class Engine {
 public:
@@ -209,6 +225,7 @@ public:
     Dims dims() const;
     int tp_size() const { return tp_size_; }
     int tp_rank() const { return tp_rank_; }
+    const TpPeer& tp_peer() const { return tp_peer_; }
     // in-place sum over the tensor-parallel group (no-op at tp == 1)
     void tp_allreduce(float* buf, size_t n, cudaStream_t s);
     const LayerWeights& layer(int i) const { return layers_[i]; }
@@ -267,6 +284,8 @@ private:
     std::mutex mu_;
     int tp_size_ = 1, tp_rank_ = 0;
     void* tp_comm_ = nullptr;
+    TpPeer tp_peer_;
+    void tp_setup_peer();
 };
 
 // Process-wide switch: capture/replay the device part of decode steps as

@@ -93,6 +93,14 @@ struct MegaArgs {
     long long bpf_cycles;  // ring-full wait (SM cycles) that counts as a bubble
     uint8_t* xim[4];   // per phase: the GEMM's input as [KB][48 x 64] split bf16 images (put_split)
     int attn_rows;     // 1: per-(row, kv head) attention; 0: key-chunked, rows share K/V (long contexts)
+    // tensor parallelism (TP = 2): O / down partial tiles are exchanged with the
+    // peer GPU through its inbox (CUDA IPC over NVLink) inside the epilogue
+    int tp, tp_rank;
+    float* inbox;          // mine, written by the peer
+    unsigned* inflag;      // mine: epoch flags per (layer, O|down, tile)
+    float* peer_inbox;     // the peer's (mapped)
+    unsigned* peer_inflag;
+    unsigned* epoch_ptr;   // launch counter
     float* apart;      // attention chunk partials [n_kv][ceil(max_len/kKeyChunk)][128 queries][hd + 2]
     unsigned* acnt;    // [n_kv] chunk arrival counters (reset by the merging chunk)
     // optional [G][kBarSlots][kTraceW] (tools/trace_mega.py): per CTA and
@@ -318,6 +326,7 @@ __shared__ int sh_prior;
 __shared__ LayerDesc sh_layers[kMaxMegaLayers];
 // per row: compacted visible-key count and its tail slots (columns >= prior)
 __shared__ int sh_ncols[kRows];
+__shared__ unsigned sh_epoch;
 __shared__ int sh_tail[kRows][kRows];
 
 // ── epilogues (thread = feature m of the tile; y[r] for 16 rows) ─────────
@@ -325,7 +334,21 @@ __shared__ int sh_tail[kRows][kRows];
 // stores split(h * gain) (gain is per input feature), and the consuming
 // epilogue scales its accumulator by the per-row 1/rms (rs[r]), which needs
 // the whole row's sum of squares and so is only known after the barrier.
-__device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int p, int tile, int m, int et,
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ float ld_relaxed_sys(const float* p) {
+    float v;
+    asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, int tile, int m, int et,
                           const float (&yin)[kRows], float* xch, const float* rs, const float* ropeT,
                           const float* hpre) {
     float y[kRows];
@@ -386,6 +409,31 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int p, int tile
         named_sync(1, 128);
     } else {  // residual add + sum-of-squares partials for the next RMSNorm
         const int f = tile * kM + m;
+        if (a.tp > 1) {
+            // row-parallel output: swap partial tiles with the peer over NVLink
+            // and sum them in rank order (bitwise identical on both GPUs)
+            const int tilesH = (a.H + kM - 1) / kM;
+            const size_t slot = (static_cast<size_t>(l) * 2 + (p == P_O ? 0 : 1)) * tilesH + tile;
+            float* dst = a.peer_inbox + slot * kRows * kM;
+            for (int r = 0; r < a.rows; ++r) dst[r * kM + m] = y[r];
+            __threadfence_system();
+            named_sync(1, 128);
+            if (et == 0) {
+                st_release_sys(a.peer_inflag + slot, sh_epoch);
+                unsigned long long spins = 0;
+                while (ld_acquire_sys(a.inflag + slot) < sh_epoch) {
+                    __nanosleep(32);
+                    if (++spins > (1ull << 27)) asm volatile("trap;");  // peer gone: fail, do not hang
+                }
+            }
+            named_sync(1, 128);
+            const float* src = a.inbox + slot * kRows * kM;
+#pragma unroll
+            for (int r = 0; r < kRows; ++r) {
+                const float other = r < a.rows ? ld_relaxed_sys(src + r * kM + m) : 0.0f;
+                y[r] = a.tp_rank == 0 ? y[r] + other : other + y[r];
+            }
+        }
         // the next GEMM's input image: split(h * gain) of ffn_norm (after O)
         // or of the next layer's attn_norm (after down; none after the last)
         const float* gn = p == P_O ? L.ffn_norm : L.next_attn_norm;
@@ -1002,6 +1050,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
         ropeT[i] = v;
     }
     if (threadIdx.x == 0) sh_prior = *a.prior;
+    if (threadIdx.x == 0) sh_epoch = a.tp > 1 ? *a.epoch_ptr + 1u : 0u;
     for (int i = threadIdx.x; i < a.nlayers; i += blockDim.x) sh_layers[i] = a.layers[i];
     if (threadIdx.x < kRows) {  // compacted key lists (mega_mask_ok: every row sees [0, prior))
         const int r = threadIdx.x, prior = *a.prior;
@@ -1236,7 +1285,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     for (int r = 0; r < kRows; ++r) y[r] = (v[r] + v[kRows + r]) + v[2 * kRows + r];
                     bool done_tile = false;
                     if (lo == 0 && hi == g.KB) {
-                        epi_final(a, L, p, t, m, et, y, xch, rs, ropeT, hpre);
+                        epi_final(a, L, l, p, t, m, et, y, xch, rs, ropeT, hpre);
                         done_tile = true;
                     } else {  // stream-K fixup: last arriver sums the pieces in k order
                         const long long first_u = static_cast<long long>(t) * g.KB;
@@ -1278,7 +1327,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                                 }
                             }
                             if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 10) = gtimer();
-                            epi_final(a, L, p, t, m, et, sacc, xch, rs, ropeT, hpre);
+                            epi_final(a, L, l, p, t, m, et, sacc, xch, rs, ropeT, hpre);
                             if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 11) = gtimer();
                             done_tile = true;
                         }
@@ -1404,6 +1453,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
+            if (a.tp > 1) atomicAdd(a.epoch_ptr, 1u);  // next launch's exchange epoch
             atomicExch(a.bar + kBarSlots, 0u);
         }
     }
@@ -1604,13 +1654,25 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     a.nlayers = le - lb;
     a.rows = rows;
     a.stages = stages;
-    a.H = c.hidden_dim;
-    a.qd = c.q_dim();
-    a.kvd = c.kv_dim();
-    a.F = c.ffn_dim;
-    a.hd = c.head_dim;
-    a.n_heads = c.n_heads;
-    a.n_kv = c.n_kv_heads;
+    const Dims dl = e.dims();  // this engine's shard (tensor parallelism: local heads / FFN columns)
+    a.H = dl.H;
+    a.qd = dl.qd;
+    a.kvd = dl.kvd;
+    a.F = dl.F;
+    a.hd = dl.hd;
+    a.n_heads = dl.n_heads;
+    a.n_kv = dl.n_kv;
+    a.tp = e.tp_size();
+    a.tp_rank = e.tp_rank();
+    if (a.tp > 1) {
+        const TpPeer& tpp = e.tp_peer();
+        if (!tpp.peer_inbox) throw Error(Kind::internal, "tensor-parallel peer inbox not mapped");
+        a.inbox = tpp.inbox;
+        a.inflag = tpp.inflag;
+        a.peer_inbox = tpp.peer_inbox;
+        a.peer_inflag = tpp.peer_inflag;
+        a.epoch_ptr = tpp.epoch;
+    }
     a.max_len = c.max_seq_len;
     a.eps = c.rms_eps;
     a.h = ws.h;

@@ -21,6 +21,7 @@ struct NcclApi {
     ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                                cudaStream_t) = nullptr;
     ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*error_string)(ncclResult_t) = nullptr;
 };
 
@@ -35,6 +36,7 @@ const NcclApi& nccl() {
         api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
         api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
         api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
         api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
     });
     if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce || !api.comm_destroy)
@@ -69,6 +71,11 @@ void* tp_comm_init(int size, int rank, const uint8_t* uid) {
 
 void tp_comm_destroy(void* comm) {
     if (comm) nccl().comm_destroy(static_cast<ncclComm_t>(comm));
+}
+
+// Every rank's `n` bytes (device) -> [size][n] on every rank.
+void tp_allgather_bytes(void* comm, const void* src, void* dst, size_t n, cudaStream_t s) {
+    check(nccl().all_gather(src, dst, n, ncclUint8, static_cast<ncclComm_t>(comm), s), "AllGather");
 }
 
 // In-place fp32 sum over the tensor-parallel ranks.  With two ranks every
