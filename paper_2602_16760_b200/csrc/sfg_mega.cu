@@ -468,31 +468,12 @@ __device__ void attention_row_item(const MegaArgs& a, const LayerDesc& L, int ro
     const int warp = at >> 5, lane = at & 31;
     for (int t = at; t < group * HD; t += 256)
         qs[t] = __ldcg(a.q + static_cast<size_t>(row) * a.qd + static_cast<size_t>(kvh * group) * HD + t);
-    // expand visibility runs into compacted columns
-    __shared__ int n_s, roff_s[65];
-    const int r0 = a.row_off[row], r1 = a.row_off[row + 1];
-    int total = 0;
-    for (int base = r0; base < r1; base += 64) {
-        const int nr = min(64, r1 - base);
-        if (at == 0) {
-            int off = total;
-            for (int r = 0; r < nr; ++r) {
-                roff_s[r] = off;
-                off += a.runs[base + r].end - a.runs[base + r].start;
-            }
-            roff_s[64] = off;
-        }
-        named_sync(3, 256);
-        for (int r = 0; r < nr; ++r) {
-            const MaskRun rr = a.runs[base + r];
-            for (int j = rr.start + at; j < rr.end; j += 256) cols[roff_s[r] + j - rr.start] = j;
-        }
-        total = roff_s[64];
-        named_sync(3, 256);
-    }
-    if (at == 0) n_s = total;
-    named_sync(3, 256);
-    const int n = n_s;
+    // the row's visible keys in compacted order: cache slots [0, prior) then
+    // its own tail slots (staged per launch in sh_tail / sh_ncols; the host
+    // guarantees every row sees the whole cached prefix, mega_mask_ok)
+    const int prior = sh_prior;
+    const int n = sh_ncols[row];
+    named_sync(3, 256);  // queries staged
     // NOTE: frame masks carry mval == 0 for every visible column; additive
     // masks (seam 2) take the per-GEMM path (see mega_supported()).
     const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(HD));
@@ -516,7 +497,7 @@ __device__ void attention_row_item(const MegaArgs& a, const LayerDesc& L, int ro
     for (int ch = warp; ch < nchunks; ch += 8) {
         const int c = ch * 8 + kk;
         const bool live = c < n;
-        const int col = live ? cols[c] : 0;
+        const int col = !live ? 0 : (c < prior ? c : sh_tail[row][c - prior]);
         const float4* kr = reinterpret_cast<const float4*>(kb + static_cast<size_t>(col) * HD + sub * (HD / 4));
         float4 k4[Q4];
 #pragma unroll
@@ -1004,7 +985,7 @@ __device__ __forceinline__ void cursor_prefetch_next(const MegaArgs& a, int c, C
 
 // shared-memory floats of the attention scratch: the larger of the two layouts
 __host__ __device__ __forceinline__ int attn_scratch_floats(bool rows_attn, int hd, int group, int max_len) {
-    return rows_attn ? kMaxGroup * hd + 8 * kMaxGroup * 2 + 8 * group * hd + max_len
+    return rows_attn ? kMaxGroup * hd + 8 * kMaxGroup * 2 + 8 * group * hd
                      : 32 * hd + 8 * 4 * kKeyBlock + 4 * kKeyBlock * hd + 2 * kRows * hd;
 }
 
