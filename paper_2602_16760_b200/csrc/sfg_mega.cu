@@ -443,6 +443,7 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
         // residual rows were prefetched into shared memory (cp.async) while
         // the accumulator was still being produced
         cp_async_wait_all();
+        if (a.trace && et == 0) *tslot(a, blockIdx.x, input_barrier(l, p), 12) = gtimer();
         float hn[kRows];
 #pragma unroll
         for (int r = 0; r < kRows; ++r) hn[r] = (f < a.H && r < a.rows) ? hpre[r * kM + m] : 0.0f;
@@ -455,7 +456,9 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
             }
         }
         float* ss = (p == P_O ? a.ss_o : a.ss_d) + static_cast<size_t>(tile) * kRows;
+        if (a.trace && et == 0) *tslot(a, blockIdx.x, input_barrier(l, p), 13) = gtimer();
         tile_sumsq(hn, xch + 64 * kRows, ss, et);
+        if (a.trace && et == 0) *tslot(a, blockIdx.x, input_barrier(l, p), 14) = gtimer();
     }
 }
 

@@ -74,7 +74,8 @@ for out_id, in_id in ((6, 5), (8, 7), (9, 8), (10, 9)):
         def ts(k, row=in_id):
             v = tr[c, row, k]
             return f"{(v - t0) / 1000:7.1f}" if v > 0 else "      -"
-        print(f"   {int(c):4d}:", " ".join(ts(k) for k in (6, 8, 9, 10, 11, 7)), ts(2, out_id))
+        print(f"   {int(c):4d}:", " ".join(ts(k) for k in (6, 8, 9, 10, 11, 7)), ts(2, out_id),
+              "| epi: h ready, stores done, sumsq done:", " ".join(ts(k) for k in (12, 13, 14)))
 # per-phase critical path: input barrier complete (max arrive) -> output barrier
 # complete, against the phase's weight bytes at the measured HBM peak
 H, QD, KVD, F = 4096, 4096, 1024, 14336
