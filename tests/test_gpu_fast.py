@@ -140,3 +140,17 @@ def test_fast_seven_b_privacy_depths_lookahead_equals_sequential():
                                  want_logits=True)
         assert s.tokens == a.tokens, d
         assert np.array_equal(s.committed_logits, a.committed_logits), d
+
+
+def test_fast_twelve_b_width_layer_within_tolerance(ref):
+    """One NeMo-12B-width middle layer (d=5120, 32q/8kv x160, ffn 14336; the
+    head_dim-160 variant the reference accepts) at B=16 against the
+    reference's own forward_layers (4 rows checked), through the layer-stack
+    megakernel (head_dim 160 attention path)."""
+    cfg = po.nemo12b_parity_cfg(max_seq_len=256)
+    eng = sfg.Engine(scfg(cfg), math=sfg.FAST, layers=(2, 3), with_embedding=False, with_head=False)
+    mr = ref.model(cfg, bf16=True, layers=(2, 3), with_head=False)
+    h = (np.random.default_rng(3).standard_normal((16, 5120)) * 0.5).astype(np.float32)
+    out = eng.forward_layers(2, 3, h, list(range(16)), eng.bank(2, 3))
+    a = mr.bank(2, 3).forward(2, 3, h[:4], list(range(4)))
+    assert rel(out[:4], a) <= HIDDEN_TOL
