@@ -90,6 +90,7 @@ struct MegaArgs {
     int evict_first;   // stream weights with an L2 evict-first policy
     int spin_mma;      // dev knob: MMA issuer spins on test_wait instead of try_wait
     int bpf;           // bubble L2 prefetch depth in units (0: off)
+    int G[4];          // per phase: CTAs sharing its stream-K split (phase_ctas)
     long long bpf_cycles;  // ring-full wait (SM cycles) that counts as a bubble
     uint8_t* xim[4];   // per phase: the GEMM's input as [KB][48 x 64] split bf16 images (put_split)
     int attn_rows;     // 1: per-(row, kv head) attention; 0: key-chunked, rows share K/V (long contexts)
@@ -143,8 +144,35 @@ __device__ __forceinline__ Geo geom(const MegaArgs& a, int p) {
         case P_GU: t = a.F / 64; kb = a.H / kKB; break;
         default: t = (a.H + kM - 1) / kM; kb = a.F / kKB; break;
     }
-    return {t, kb, split_ctas(t, kb, gridDim.x)};
+    return {t, kb, a.G[p]};  // CTAs sharing the phase's stream-K split (host: phase_ctas)
 }
+// CTAs of a phase's split.  A tile-aligned split is used when it keeps at
+// least align_pct % of the grid busy: every CTA then gets exactly one 1/P piece
+// of one tile (tiles <= grid, P | KB) or k whole tiles (tiles > grid, k |
+// tiles) -- one accumulator and at most one fixup per CTA, while the idle CTAs'
+// producers already stream the next GEMM's weights.  Otherwise stream-K over
+// the whole grid (split_ctas).
+inline int phase_ctas(int tiles, int KB, int grid, int align_pct) {
+    if (align_pct > 0) {
+        int ga = 0;
+        if (tiles <= grid) {
+            for (int P = std::min(kMaxPieces, grid / tiles); P >= 1; --P)
+                if (KB % P == 0) {
+                    ga = tiles * P;
+                    break;
+                }
+        } else {
+            for (int k = (tiles + grid - 1) / grid; k <= tiles; ++k)
+                if (tiles % k == 0) {
+                    ga = tiles / k;
+                    break;
+                }
+        }
+        if (ga * 100 >= align_pct * grid) return ga;
+    }
+    return split_ctas(tiles, KB, grid);
+}
+
 // this CTA's unit range [st, en) of a phase (empty when c >= g.G)
 __device__ __forceinline__ void unit_range(const Geo& g, int c, long long& st, long long& en) {
     const long long U = static_cast<long long>(g.tiles) * g.KB;
@@ -1706,6 +1734,15 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
             return v ? atoll(v) : 2000LL;
         }();
         a.bpf = bpf_env;
+        static const int al_env = [] {
+            const char* v = getenv("SFG_MEGA_ALIGN");
+            return v ? atoi(v) : 85;
+        }();
+        const int tQ = (dl.qd + 2 * dl.kvd + tc::kM - 1) / tc::kM, tH = (dl.H + tc::kM - 1) / tc::kM;
+        a.G[P_QKV] = phase_ctas(tQ, dl.H / tc::kKB, nsm, al_env);
+        a.G[P_O] = phase_ctas(tH, dl.qd / tc::kKB, nsm, al_env);
+        a.G[P_GU] = phase_ctas(dl.F / 64, dl.H / tc::kKB, nsm, al_env);
+        a.G[P_DOWN] = phase_ctas(tH, dl.F / tc::kKB, nsm, al_env);
         a.attn_rows = ra ? 1 : 0;
         a.bpf_cycles = bpfc_env;
     }
