@@ -129,9 +129,9 @@ struct Geo {
 // ceil((KB-1)/(kMaxPieces-1)) k-blocks so a tile never has more than
 // kMaxPieces pieces; CTAs >= G get no units in this phase.
 __host__ __device__ __forceinline__ int split_ctas(int tiles, int KB, int grid) {
-    const long long U = static_cast<long long>(tiles) * KB;
+    const int U = tiles * KB;
     const int min_units = (KB - 1 + kMaxPieces - 2) / (kMaxPieces - 1);
-    long long g = min_units > 0 ? U / min_units : U;
+    int g = min_units > 0 ? U / min_units : U;
     if (g > grid) g = grid;
     if (g < 1) g = 1;
     return static_cast<int>(g);
@@ -174,8 +174,9 @@ inline int phase_ctas(int tiles, int KB, int grid, int align_pct) {
 }
 
 // this CTA's unit range [st, en) of a phase (empty when c >= g.G)
-__device__ __forceinline__ void unit_range(const Geo& g, int c, long long& st, long long& en) {
-    const long long U = static_cast<long long>(g.tiles) * g.KB;
+// (unit counts are small: tiles x k-blocks < 2^31, 32-bit math throughout)
+__device__ __forceinline__ void unit_range(const Geo& g, int c, int& st, int& en) {
+    const int U = g.tiles * g.KB;
     if (c >= g.G) {
         st = en = 0;
         return;
@@ -982,7 +983,7 @@ __device__ __forceinline__ int attention_items(const MegaArgs& a, int nchunks) {
 // A CTA's walk over its weight units: (layer, phase, unit) in stream order.
 struct Cursor {
     int l, p;
-    long long u, en;
+    int u, en;
 };
 __device__ __forceinline__ void cursor_norm(const MegaArgs& a, int c, Cursor& k) {
     while (k.l < a.nlayers && k.u >= k.en) {
@@ -991,7 +992,7 @@ __device__ __forceinline__ void cursor_norm(const MegaArgs& a, int c, Cursor& k)
             ++k.l;
         }
         if (k.l >= a.nlayers) break;
-        long long st, en;
+        int st, en;
         unit_range(geom(a, k.p), c, st, en);
         k.u = st;
         k.en = en;
@@ -1110,15 +1111,15 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
             // tails), prefetch the next units into L2 so HBM keeps streaming
             Cursor bp{0, 0, 0, 0};
             cursor_begin(a, c, bp);
-            long long n_cur = 0, n_bp = 0;
+            int n_cur = 0, n_bp = 0;
             for (int l = 0; l < a.nlayers; ++l)
                 for (int p = 0; p < 4; ++p) {
                     const Geo g = geom(a, p);
                     const uint8_t* W = a.layers[l].w[p];
-                    long long st, en;
+                    int st, en;
                     unit_range(g, c, st, en);
                     unsigned long long wacc = 0;
-                    for (long long u = st; u < en; ++u, ++n_cur) {
+                    for (int u = st; u < en; ++u, ++n_cur) {
                         if (a.bpf > 0) {
                             if (!mbar_test(&empty[stage], ph ^ 1)) {
                                 const long long t0 = clock64();
@@ -1163,15 +1164,15 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
             for (int l = 0; l < a.nlayers; ++l)
                 for (int p = 0; p < 4; ++p) {
                     const Geo g = geom(a, p);
-                    const long long U = static_cast<long long>(g.tiles) * g.KB;
-                    long long st, en;
+                    const int U = g.tiles * g.KB;
+                    int st, en;
                 (void)U;
                 unit_range(g, c, st, en);
                     unsigned long long wacc = 0;
-                    for (long long u = st; u < en;) {
+                    for (int u = st; u < en;) {
                         const int t = static_cast<int>(u / g.KB);
-                        const int lo = static_cast<int>(u - static_cast<long long>(t) * g.KB);
-                        const int hi = static_cast<int>(min(en - static_cast<long long>(t) * g.KB, static_cast<long long>(g.KB)));
+                        const int lo = u - t * g.KB;
+                        const int hi = min(en - t * g.KB, g.KB);
                         mwait(&tempty[acc], acc_ph ^ 1);
                         tc_fence_after();
                         const uint32_t d = tmem + acc * kAccCols;
@@ -1199,7 +1200,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                             acc = 0;
                             acc_ph ^= 1;
                         }
-                        u = static_cast<long long>(t) * g.KB + hi;
+                        u = t * g.KB + hi;
                     }
                     if (a.trace) *tslot(a, c, input_barrier(l, p), 4) = wacc;
                 }
@@ -1234,11 +1235,11 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
             const LayerDesc& L = sh_layers[l];
             for (int p = 0; p < 4; ++p, ++gp) {
                 const Geo g = geom(a, p);
-                const long long U = static_cast<long long>(g.tiles) * g.KB;
+                const int U = g.tiles * g.KB;
                 const int kind = K_QKV + (p == P_QKV ? 0 : p + 1);
                 float* parts = a.partials + (gp & 1) * a.part_stride;
                 int* cnts = a.counters + (gp & 1) * a.cnt_stride;
-                long long st, en;
+                int st, en;
                 unit_range(g, c, st, en);
                 if ((p == P_QKV || p == P_GU) && st < en) {  // per-row 1/rms: needs every producer tile
                     if (et == 0)
@@ -1262,10 +1263,10 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     named_sync(1, 128);
                 }
                 unsigned long long t_acc = 0;
-                for (long long u = st; u < en;) {
+                for (int u = st; u < en;) {
                     const int t = static_cast<int>(u / g.KB);
-                    const int lo = static_cast<int>(u - static_cast<long long>(t) * g.KB);
-                    const int hi = static_cast<int>(min(en - static_cast<long long>(t) * g.KB, static_cast<long long>(g.KB)));
+                    const int lo = u - t * g.KB;
+                    const int hi = min(en - t * g.KB, g.KB);
                     if (p == P_O || p == P_DOWN) {  // prefetch this tile's residual rows while the MMA runs
                         cp_async_wait_all();   // a previous (unused) prefetch must not land late
                         const int f = t * kM + m;
@@ -1300,7 +1301,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         epi_final(a, L, l, p, t, m, et, y, xch, rs, ropeT, hpre);
                         done_tile = true;
                     } else {  // stream-K fixup: last arriver sums the pieces in k order
-                        const long long first_u = static_cast<long long>(t) * g.KB;
+                        const int first_u = t * g.KB;
                         const int c_first = static_cast<int>(((first_u + 1) * g.G - 1) / U);
                         const int piece = c - c_first;
                         const int n_pieces = static_cast<int>(((first_u + g.KB) * g.G - 1) / U) - c_first + 1;
@@ -1355,7 +1356,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     } else {
                         named_sync(1, 128);
                     }
-                    u = static_cast<long long>(t) * g.KB + hi;
+                    u = t * g.KB + hi;
                 }
                 if (a.trace && et == 0) {
                     const int id = 5 * l + (p == P_QKV ? 1 : p + 2);
@@ -1390,17 +1391,17 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     // input image, as soon as the producer tiles of that block are
                     // published (the 32 lanes poll the next 32 units' flags at once)
                     const Geo g = geom(a, p);
-                    long long st, en;
+                    int st, en;
                     unit_range(g, c, st, en);
                     const uint8_t* X = a.xim[p];
                     unsigned long long xwacc = 0;
-                    long long ready = st;
+                    int ready = st;
                     bool first = true;
-                    for (long long u = st; u < en; ++u) {
+                    for (int u = st; u < en; ++u) {
                         if (u >= ready) {
                             unsigned long long spins = 0;
                             while (u >= ready) {
-                                const long long uu = ready + lane;
+                                const int uu = ready + lane;
                                 const bool ok = uu >= en || xblock_ready(a, l, p, static_cast<int>(uu % g.KB));
                                 const unsigned mk = __ballot_sync(0xffffffffu, ok);
                                 const int k = mk == 0xffffffffu ? 32 : __ffs(~mk) - 1;
