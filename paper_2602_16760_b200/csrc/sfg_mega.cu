@@ -91,6 +91,7 @@ struct MegaArgs {
     int spin_mma;      // dev knob: MMA issuer spins on test_wait instead of try_wait
     int bpf;           // bubble L2 prefetch depth in units (0: off)
     int G[4];          // per phase: CTAs sharing its stream-K split (phase_ctas)
+    int fl_base, fl_lay, fl_off[6];  // dataflow flag layout (see fptr)
     long long bpf_cycles;  // ring-full wait (SM cycles) that counts as a bubble
     uint8_t* xim[4];   // per phase: the GEMM's input as [KB][48 x 64] split bf16 images (put_split)
     int attn_rows;     // 1: per-(row, kv head) attention; 0: key-chunked, rows share K/V (long contexts)
@@ -235,15 +236,11 @@ __device__ __forceinline__ int kind_tiles(const MegaArgs& a, int k) {
     }
 }
 // flag of tile t (t == kind_tiles: the kind's completed-tile counter)
+// offsets precomputed on the host (flag_layout): a.fl_off[k] within a layer
+// block of a.fl_lay flags that starts after the statistics flags
 __device__ __forceinline__ unsigned* fptr(const MegaArgs& a, int l, int k, int t) {
-    const int tH = kind_tiles(a, K_STATS);
     if (k == K_STATS) return a.flags + t;
-    int off = tH + 1;
-    int lay = 0;
-    for (int j = K_QKV; j <= K_DOWN; ++j) lay += kind_tiles(a, j) + 1;
-    off += l * lay;
-    for (int j = K_QKV; j < k; ++j) off += kind_tiles(a, j) + 1;
-    return a.flags + off + t;
+    return a.flags + a.fl_base + l * a.fl_lay + a.fl_off[k] + t;
 }
 __device__ __forceinline__ void red_add(unsigned* f, unsigned v) {
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
@@ -1744,6 +1741,18 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         a.G[P_O] = phase_ctas(tH, dl.qd / tc::kKB, nsm, al_env);
         a.G[P_GU] = phase_ctas(dl.F / 64, dl.H / tc::kKB, nsm, al_env);
         a.G[P_DOWN] = phase_ctas(tH, dl.F / tc::kKB, nsm, al_env);
+        // flag layout (must match kind_tiles): statistics tiles + counter, then
+        // per layer QKV, attention kv heads, O, gate|up, down tiles + counter each
+        const int kt[6] = {tH, tQ, dl.n_kv, tH, dl.F / 64, tH};
+        a.fl_base = tH + 1;
+        int off = 0;
+        for (int k = mega::K_QKV; k <= mega::K_DOWN; ++k) {
+            a.fl_off[k] = off;
+            off += kt[k] + 1;
+        }
+        a.fl_off[mega::K_STATS] = 0;
+        a.fl_lay = off;
+        if (a.fl_base + (le - lb) * a.fl_lay > stp->nflags) throw Error(Kind::internal, "flag buffer too small");
         a.attn_rows = ra ? 1 : 0;
         a.bpf_cycles = bpfc_env;
     }
