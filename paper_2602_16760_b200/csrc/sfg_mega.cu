@@ -1244,10 +1244,18 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                                            : fptr(a, l, K_O, tilesH),
                                 static_cast<unsigned>(tilesH));
                     named_sync(1, 128);
-                    if (et < kRows) {
+                    {  // 8 threads per row, loads in flight together, fixed-order combine
                         const float* ssb = p == P_QKV ? a.ss_d : a.ss_o;
+                        const int r = et & 15, j = et >> 4;
+                        float part = 0.0f;
+                        for (int t = j; t < tilesH; t += 8) part += __ldcg(ssb + t * kRows + r);
+                        xch[j * kRows + r] = part;
+                    }
+                    named_sync(1, 128);
+                    if (et < kRows) {
                         float ss = 0.0f;
-                        for (int t = 0; t < tilesH; ++t) ss += __ldcg(ssb + t * kRows + et);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) ss += xch[j * kRows + et];
                         rs[et] = 1.0f / sqrtf(ss / static_cast<float>(a.H) + a.eps);
                     }
                     named_sync(1, 128);
