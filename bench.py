@@ -359,6 +359,33 @@ def run_ours(args, ws, rank, local):
             sweep[f"{int(rtt)}ms"] = {"tok_s": nt / dt, "ms_per_step": dt / k * 1000.0}
             L.sfg_decoder_destroy(d)
 
+    # ── concurrent sessions per GPU (configs[4]): K sessions stepped
+    # round-robin on this GPU (one weight pass per session step: cross-session
+    # batching is the next step); aggregate = all ranks' tokens
+    sessions = {}
+    if not args.no_sweep:
+        for k in (1, 4, 16):
+            cls = [sfg.SplitClient(eng, sfg.SplitConfig(SPLIT, SPLIT, sfg.F16, 0.0), srv,
+                                   session_id=f"bench-s{k}-{i}-{rank}") for i in range(k)]
+            decs = [make_decoder(cl) for cl in cls]
+            for d in decs:
+                step(d)
+                step(d)
+            rounds = 3
+            barrier(ws, local)
+            tr = time.perf_counter()
+            nt = 0
+            for _ in range(rounds):
+                for d in decs:
+                    nt += step(d)[0]
+            dt = barrier_max(ws, local, time.perf_counter() - tr)
+            nt_all = dist_sum(ws, local, float(nt))
+            sessions[str(k * ws)] = {"sessions_per_gpu": k, "gpus": ws, "aggregate_tok_s": nt_all / dt,
+                                     "per_session_step_ms": dt / rounds * 1000.0}
+            for d in decs:
+                L.sfg_decoder_destroy(d)
+            del cls
+
     # ── privacy-depth sweep (configs[2]): 2/4/8 local layers each side ─────
     privacy = {}
     if not args.no_sweep:
@@ -419,6 +446,7 @@ def run_ours(args, ws, rank, local):
         "batch_rows": sorted(set(batches)), "acceptance": toks / args.steps, "weights_init_s": t_init,
         "rtt_sweep": sweep,
         "privacy_sweep": privacy,
+        "session_sweep": sessions,
         "clocks": clk.summary(),
     }
     if ws == 1 and not args.no_cpu:

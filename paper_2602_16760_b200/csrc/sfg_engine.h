@@ -147,6 +147,7 @@ public:
     void resolve_meta(const int32_t* keep, int n);
     void crop(int pos);                        // tinyformer.cpp:310-316
     float* kslab(int layer) const;
+    size_t slab_elems() const { return slab_elems_; }
     float* vslab(int layer) const;
     void read_kv(int layer, int head, int pos, float* k, float* v);
     cudaStream_t stream() const { return stream_; }

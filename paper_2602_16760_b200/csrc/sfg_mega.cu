@@ -50,6 +50,7 @@ constexpr int kAccCols = 64;
 constexpr int kTmemCols = 128;
 constexpr int kMaxPieces = 16;
 constexpr int kMaxGroup = 8;
+constexpr int kMaxBanks = 16;  // sessions per launch (one row each at least)
 enum Phase : int { P_QKV = 0, P_O = 1, P_GU = 2, P_DOWN = 3 };
 
 struct LayerDesc {
@@ -95,6 +96,14 @@ struct MegaArgs {
     long long bpf_cycles;  // ring-full wait (SM cycles) that counts as a bubble
     uint8_t* xim[4];   // per phase: the GEMM's input as [KB][48 x 64] split bf16 images (put_split)
     int attn_rows;     // 1: per-(row, kv head) attention; 0: key-chunked, rows share K/V (long contexts)
+    // KV caches: rows may belong to different sessions (cross-session batching):
+    // bank b's K slab of launch layer l is kbank[b] + l * slab_stride; row r
+    // appends at rowinfo[3r + 1] and sees rowinfo[3r + 2] cached keys of bank
+    // rowinfo[3r] (rowinfo == nullptr: one bank, slot = prior + r)
+    float* kbank[kMaxBanks];
+    float* vbank[kMaxBanks];
+    size_t slab_stride;
+    const int32_t* rowinfo;
     // tensor parallelism (TP = 2): O / down partial tiles are exchanged with the
     // peer GPU through its inbox (CUDA IPC over NVLink) inside the epilogue
     int tp, tp_rank;
@@ -349,6 +358,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 constexpr int kMaxMegaLayers = 64;
 __shared__ int sh_pos[kRows];
 __shared__ int sh_prior;
+__shared__ int sh_row_bank[kRows], sh_row_slot[kRows], sh_row_prior[kRows];
 __shared__ LayerDesc sh_layers[kMaxMegaLayers];
 // per row: compacted visible-key count and its tail slots (columns >= prior)
 __shared__ int sh_ncols[kRows];
@@ -387,7 +397,6 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
         const int fl = seg == 0 ? f : (seg == 1 ? f - a.qd : f - a.qd - a.kvd);
         const int d = fl % a.hd, half = a.hd >> 1, i = d >> 1;
         const bool odd = (m & 1) != 0;
-        const int prior = sh_prior;
         // the rows' cos/sin were staged in shared memory at kernel entry
         float cs[kRows], sn[kRows];
 #pragma unroll
@@ -408,8 +417,9 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
             if (seg == 0) {
                 a.q[static_cast<size_t>(r) * a.qd + fl] = v;
             } else {
-                float* dst = (seg == 1 ? L.kc : L.vc) +
-                             (static_cast<size_t>(fl / a.hd) * a.max_len + prior + r) * a.hd + d;
+                const int b = sh_row_bank[r];
+                float* dst = (seg == 1 ? a.kbank[b] : a.vbank[b]) + static_cast<size_t>(l) * a.slab_stride +
+                             (static_cast<size_t>(fl / a.hd) * a.max_len + sh_row_slot[r]) * a.hd + d;
                 *dst = v;
             }
         }
@@ -491,7 +501,7 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
 // ── attention for one (row, kv head): flash-decode over the row's visible
 // keys with a fixed key partition (chunk i of 32 keys -> warp i % 8).
 template <int HD, int GR>  // GR: compile-time bound on the GQA group (register arrays)
-__device__ void attention_row_item(const MegaArgs& a, const LayerDesc& L, int row, int kvh, int at, float* qs,
+__device__ void attention_row_item(const MegaArgs& a, const LayerDesc& L, int l, int row, int kvh, int at, float* qs,
                                float* wst, float* ocomb, int* cols) {
     const int group = a.n_heads / a.n_kv;
     const int warp = at >> 5, lane = at & 31;
@@ -500,14 +510,16 @@ __device__ void attention_row_item(const MegaArgs& a, const LayerDesc& L, int ro
     // the row's visible keys in compacted order: cache slots [0, prior) then
     // its own tail slots (staged per launch in sh_tail / sh_ncols; the host
     // guarantees every row sees the whole cached prefix, mega_mask_ok)
-    const int prior = sh_prior;
+    const int prior = sh_row_prior[row];
     const int n = sh_ncols[row];
     named_sync(3, 256);  // queries staged
     // NOTE: frame masks carry mval == 0 for every visible column; additive
     // masks (seam 2) take the per-GEMM path (see mega_supported()).
     const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(HD));
-    const float* kb = L.kc + static_cast<size_t>(kvh) * a.max_len * HD;
-    const float* vb = L.vc + static_cast<size_t>(kvh) * a.max_len * HD;
+    const float* kb = a.kbank[sh_row_bank[row]] + static_cast<size_t>(l) * a.slab_stride +
+                      static_cast<size_t>(kvh) * a.max_len * HD;
+    const float* vb = a.vbank[sh_row_bank[row]] + static_cast<size_t>(l) * a.slab_stride +
+                      static_cast<size_t>(kvh) * a.max_len * HD;
     // A warp takes 8 keys per iteration: 4 lanes per key split the score dot
     // (HD/4 dims each, one batch of loads), then all 32 lanes sweep head
     // dims for the value sum with the 8 value rows loaded up front.
@@ -626,15 +638,15 @@ __device__ __forceinline__ void attention_rows_dispatch(const MegaArgs& a, const
     }
     if (group <= 4) {
         switch (a.hd) {
-            case 64: attention_row_item<64, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
-            case 128: attention_row_item<128, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
-            case 160: attention_row_item<160, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
-            default: attention_row_item<32, 4>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
+            case 64: attention_row_item<64, 4>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
+            case 128: attention_row_item<128, 4>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
+            case 160: attention_row_item<160, 4>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
+            default: attention_row_item<32, 4>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
         }
     } else {
         switch (a.hd) {
-            case 64: attention_row_item<64, 8>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
-            default: attention_row_item<32, 8>(a, L, row, kvh, at, qs, wst, ocomb, cols); break;
+            case 64: attention_row_item<64, 8>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
+            default: attention_row_item<32, 8>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
         }
     }
     if (at == 0) signal_add(fptr(a, l, K_ATT, kvh), 1u);  // item's att rows + image are published
@@ -684,8 +696,8 @@ __device__ __noinline__ void attention_chunk(const MegaArgs& a, const LayerDesc&
         sq[t] = __ldcg(a.q + static_cast<size_t>(r) * a.qd + static_cast<size_t>(kvh * group + g) * HD + d);
     }
     const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(HD));
-    const float* kbase = L.kc + static_cast<size_t>(kvh) * a.max_len * HD;
-    const float* vbase = L.vc + static_cast<size_t>(kvh) * a.max_len * HD;
+    const float* kbase = a.kbank[0] + static_cast<size_t>(l) * a.slab_stride + static_cast<size_t>(kvh) * a.max_len * HD;
+    const float* vbase = a.vbank[0] + static_cast<size_t>(l) * a.slab_stride + static_cast<size_t>(kvh) * a.max_len * HD;
     float* sk = skv;                          // 2 x { K [kKeyBlock][C4] float4 (XOR-swizzled by row & 7) | V }
     float* skt = sk + 4 * kKeyBlock * HD;     // tail slots [prior, prior + rows): K (swizzled) | V
     float* svt = skt + kRows * HD;
@@ -1062,8 +1074,17 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
     if (threadIdx.x == 0) sh_prior = *a.prior;
     if (threadIdx.x == 0) sh_epoch = a.tp > 1 ? *a.epoch_ptr + 1u : 0u;
     for (int i = threadIdx.x; i < a.nlayers; i += blockDim.x) sh_layers[i] = a.layers[i];
-    if (threadIdx.x < kRows) {  // compacted key lists (mega_mask_ok: every row sees [0, prior))
-        const int r = threadIdx.x, prior = *a.prior;
+    if (threadIdx.x < kRows) {  // per-row cache, slot and compacted key list (mega_mask_ok)
+        const int r = threadIdx.x;
+        int prior = *a.prior, bank = 0, slot = prior + r;
+        if (a.rowinfo && r < a.rows) {
+            bank = a.rowinfo[3 * r];
+            slot = a.rowinfo[3 * r + 1];
+            prior = a.rowinfo[3 * r + 2];
+        }
+        sh_row_bank[r] = bank;
+        sh_row_slot[r] = slot;
+        sh_row_prior[r] = prior;
         int n = 0;
         if (r < a.rows)
             for (int i = a.row_off[r]; i < a.row_off[r + 1]; ++i) {
@@ -1693,6 +1714,10 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     }
     a.max_len = c.max_seq_len;
     a.eps = c.rms_eps;
+    a.kbank[0] = b.kslab(lb);
+    a.vbank[0] = b.vslab(lb);
+    a.slab_stride = b.slab_elems();
+    a.rowinfo = nullptr;
     a.h = ws.h;
     a.q = ws.q;
     a.att = ws.att;
