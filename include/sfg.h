@@ -162,6 +162,17 @@ void sfg_server_destroy(sfg_server* s);
  * thread-local buffer valid until the next call on the same thread.        */
 int32_t sfg_server_handle(sfg_server* s, const uint8_t* req, size_t req_len, const uint8_t** resp,
                           size_t* resp_len);
+/* handle() over n frames, in order, with the same responses handle() gives
+ * frame by frame.  Step frames of distinct sessions whose rows fit one pass
+ * (<= 16 rows total, masks within the layer-stack contract) share ONE weight
+ * pass: cross-session batching of concurrent decoders.
+ * resps[i] point into thread-local buffers valid until the next call.
+ * Replaces a loop of ServerEngine::handle (server.hpp:49) over the frames a
+ * transport has queued.                                                     */
+int32_t sfg_server_handle_batch(sfg_server* s, int32_t n, const uint8_t* const* reqs, const size_t* req_lens,
+                                const uint8_t** resps, size_t* resp_lens);
+/* How many weight passes sfg_server_handle_batch shared between sessions.  */
+uint64_t sfg_server_shared_passes(sfg_server* s);
 size_t sfg_server_expire_sessions(sfg_server* s);
 size_t sfg_server_session_count(sfg_server* s);
 int32_t sfg_server_session_view(sfg_server* s, const char* session_id, int32_t* cache_len,

@@ -120,6 +120,9 @@ def lib() -> C.CDLL:
         "sfg_server_destroy": (None, [vp]),
         "sfg_server_handle": (i32, [vp, C.POINTER(C.c_uint8), C.c_size_t, C.POINTER(C.POINTER(C.c_uint8)),
                                     C.POINTER(C.c_size_t)]),
+        "sfg_server_handle_batch": (i32, [vp, i32, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
+                                          C.POINTER(C.POINTER(C.c_uint8)), C.POINTER(C.c_size_t)]),
+        "sfg_server_shared_passes": (C.c_uint64, [vp]),
         "sfg_server_expire_sessions": (C.c_size_t, [vp]),
         "sfg_server_session_count": (C.c_size_t, [vp]),
         "sfg_server_session_view": (i32, [vp, C.c_char_p, i32p, i32p, i32p]),

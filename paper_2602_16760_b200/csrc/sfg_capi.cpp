@@ -157,6 +157,19 @@ int32_t sfg_server_handle(sfg_server* s, const uint8_t* req, size_t n, const uin
         *resp_len = g_resp.size();
     })
 }
+int32_t sfg_server_handle_batch(sfg_server* s, int32_t n, const uint8_t* const* reqs, const size_t* req_lens,
+                                const uint8_t** resps, size_t* resp_lens) {
+    SFG_GUARD({
+        if (n < 0) throw sfg::Error(sfg::Kind::input, "negative frame count");
+        thread_local std::vector<std::vector<uint8_t>> out;
+        s->s->handle_batch(n, reqs, req_lens, out);
+        for (int32_t i = 0; i < n; ++i) {
+            resps[i] = out[i].data();
+            resp_lens[i] = out[i].size();
+        }
+    })
+}
+uint64_t sfg_server_shared_passes(sfg_server* s) { return s->s->shared_passes(); }
 size_t sfg_server_expire_sessions(sfg_server* s) { return s->s->expire_sessions(); }
 size_t sfg_server_session_count(sfg_server* s) { return s->s->session_count(); }
 int32_t sfg_server_session_view(sfg_server* s, const char* sid, int32_t* len, int32_t* committed, int32_t* prov) {

@@ -315,7 +315,12 @@ float* fast_partials(const ModelCfg& c, Workspace& ws);
 int* fast_counters(const ModelCfg& c, Workspace& ws);
 // FAST layer-stack megakernel (sfg_mega.cu)
 bool mega_supported(const Engine& e, int rows, bool additive_mask);
-int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cudaStream_t s);
+// banks/rowinfo (optional): rows of several sessions in one pass -- row r
+// appends to (*banks)[rowinfo[3r]] at slot rowinfo[3r+1] and sees
+// rowinfo[3r+2] cached keys; b supplies the launch state (same layer range)
+int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cudaStream_t s,
+                 const std::vector<Bank*>* banks = nullptr, const int32_t* rowinfo = nullptr);
+bool rows_attention();
 float* mega_ss(Bank& b, int which, int tilesH);
 bool& mega_trace_enabled();
 int mega_trace_read(Bank& b, unsigned long long* out, size_t n);

@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <string>
 
 #include "sfg_engine.h"
@@ -1518,6 +1519,8 @@ size_t smem_bytes(bool rows_attn, int stages, int hd, int group, int max_len) {
                             kRows * kM + kM) + 16;
 }
 
+}  // namespace mega
+
 bool rows_attention() {
     static const int v = [] {
         const char* e = getenv("SFG_ATTN");  // "chunked": key-chunked attention for long contexts
@@ -1525,8 +1528,6 @@ bool rows_attention() {
     }();
     return v != 0;
 }
-
-}  // namespace mega
 
 using namespace mega;
 
@@ -1557,6 +1558,8 @@ struct MegaState {
     int* counters = nullptr;    // 2 parity arrays of per-tile arrival counters
     unsigned* flags = nullptr;  // dataflow completion flags
     float* apart = nullptr;     // attention chunk partials
+    int32_t* rowinfo = nullptr;      // cross-session pass: per-row (bank, slot, prior)
+    int32_t* rowinfo_pin = nullptr;
     unsigned* acnt = nullptr;
     size_t part_stride = 0;
     int cnt_stride = 0, nflags = 0;
@@ -1570,6 +1573,8 @@ struct MegaState {
         if (counters) cudaFree(counters);
         if (flags) cudaFree(flags);
         if (apart) cudaFree(apart);
+        if (rowinfo) cudaFree(rowinfo);
+        if (rowinfo_pin) cudaFreeHost(rowinfo_pin);
         if (acnt) cudaFree(acnt);
     }
 };
@@ -1596,7 +1601,8 @@ float* mega_ss(Bank& b, int which, int tilesH) {
     return st->ss + (which ? tilesH * tc::kRows : 0);
 }
 
-int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cudaStream_t s) {
+int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cudaStream_t s,
+                 const std::vector<Bank*>* banks, const int32_t* rowinfo) {
     const ModelCfg& c = e.cfg();
     // per-bank layer table (weights + this bank's KV slabs), grid barrier and
     // sum-of-squares buffers, owned by the bank
@@ -1718,6 +1724,25 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     a.vbank[0] = b.vslab(lb);
     a.slab_stride = b.slab_elems();
     a.rowinfo = nullptr;
+    if (banks && rowinfo) {  // cross-session pass
+        if (banks->size() > static_cast<size_t>(kMaxBanks) || !ra)
+            throw Error(Kind::internal, "cross-session pass needs <= 16 banks and the per-row attention");
+        for (size_t i = 0; i < banks->size(); ++i) {
+            Bank* bi = (*banks)[i];
+            if (bi->layer_begin() != b.layer_begin() || bi->layer_end() != b.layer_end() ||
+                bi->slab_elems() != b.slab_elems())
+                throw Error(Kind::internal, "cross-session pass over banks with different layer ranges");
+            a.kbank[i] = bi->kslab(lb);
+            a.vbank[i] = bi->vslab(lb);
+        }
+        if (!stp->rowinfo) {
+            SFG_CUDA(cudaMalloc(&stp->rowinfo, sizeof(int32_t) * 3 * tc::kRows));
+            SFG_CUDA(cudaMallocHost(&stp->rowinfo_pin, sizeof(int32_t) * 3 * tc::kRows));
+        }
+        std::memcpy(stp->rowinfo_pin, rowinfo, sizeof(int32_t) * 3 * rows);
+        SFG_CUDA(cudaMemcpyAsync(stp->rowinfo, stp->rowinfo_pin, sizeof(int32_t) * 3 * rows, cudaMemcpyHostToDevice, s));
+        a.rowinfo = stp->rowinfo;
+    }
     a.h = ws.h;
     a.q = ws.q;
     a.att = ws.att;

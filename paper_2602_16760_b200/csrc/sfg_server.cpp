@@ -224,43 +224,33 @@ void upload_meta(Engine& e, Workspace& ws, const std::vector<int32_t>& pos, cons
 
 }  // namespace
 
-void Server::handle_frame(const wire::FrameView& f, std::vector<uint8_t>& resp) {
+// handle_prompt / handle_step (server.cpp:203-265), host part: session state
+// machine, validation, keep/crop, mask -> runs.  Leaves the session locked.
+void Server::prepare(const wire::FrameView& f, StepState& st) {
     const ModelCfg& c = eng_.cfg();
     const auto kind = f.h.kind;
-    if (kind == wire::FrameKind::ping) {  // handle_ping (server.cpp:193-201)
-        wire::Header h;
-        h.kind = wire::FrameKind::response;
-        h.session_id = f.h.session_id;
-        h.shape = {0};
-        h.dtype = f.h.dtype;
-        h.srv_ms = 0.0;
-        wire::encode(h, nullptr, 0, nullptr, 0, resp);
-        return;
-    }
     if (kind == wire::FrameKind::response || kind == wire::FrameKind::error)
         throw Error(Kind::protocol, "response/error frames are not requests");
-    const bool prompt = kind == wire::FrameKind::prompt;
-
-    std::shared_ptr<Session> sess;
-    HiddenCheck hc;
-    if (prompt) {  // handle_prompt (server.cpp:203-224)
+    st.f = f;
+    st.prompt = kind == wire::FrameKind::prompt;
+    if (st.prompt) {  // handle_prompt (server.cpp:203-224)
         if (f.h.session_id.empty()) throw Error(Kind::protocol, "prompt frame requires a session_id");
-        hc = frame_to_hidden(f, c);
-        if (hc.seq > c.max_seq_len) throw Error(Kind::capacity, "prompt exceeds max_seq_len");
-        sess = create_or_reset_session(f.h.session_id);
+        { auto hc = frame_to_hidden(f, c); st.hc.seq = hc.seq; st.hc.pos = std::move(hc.pos); }
+        if (st.hc.seq > c.max_seq_len) throw Error(Kind::capacity, "prompt exceeds max_seq_len");
+        st.sess = create_or_reset_session(f.h.session_id);
     } else {  // handle_step (server.cpp:226-265)
-        sess = find_session(f.h.session_id);
-        if (!sess) throw Error(Kind::session, "unknown or expired session: " + f.h.session_id);
+        st.sess = find_session(f.h.session_id);
+        if (!st.sess) throw Error(Kind::session, "unknown or expired session: " + f.h.session_id);
     }
-    std::lock_guard<std::mutex> lk(sess->mutex);
-    Bank& bank = *sess->bank;
-    if (prompt) {
+    st.lock = std::unique_lock<std::mutex>(st.sess->mutex);
+    Bank& bank = *st.sess->bank;
+    if (st.prompt) {
         bank.reset();
     } else {
-        hc = frame_to_hidden(f, c);
+        { auto hc = frame_to_hidden(f, c); st.hc.seq = hc.seq; st.hc.pos = std::move(hc.pos); }
     }
-    const double t0 = steady_seconds();
-    if (!prompt) {
+    st.t0 = steady_seconds();
+    if (!st.prompt) {
         std::vector<int32_t> keep;
         if (f.h.keep) {
             keep.reserve(f.h.keep->size());
@@ -274,48 +264,191 @@ void Server::handle_frame(const wire::FrameView& f, std::vector<uint8_t>& resp) 
             bank.crop(static_cast<int>(p));
         }
     }
-    const int seq = hc.seq;
-    MaskRuns mr = mask_from_frame(f, bank.len(), seq);
-    forward_checks(bank, seq, mr, c.max_seq_len);
+    st.mr = mask_from_frame(f, bank.len(), st.hc.seq);
+    forward_checks(bank, st.hc.seq, st.mr, c.max_seq_len);
+    st.out_dt = cfg_.response_dtype < 0 ? f.h.dtype
+                                        : (cfg_.response_dtype == SFG_WIRE_F32 ? wire::Dtype::f32 : wire::Dtype::f16);
+}
 
-    // device: unpack -> middle layers -> pack
+// Device part for one step or for several sessions' steps in ONE weight
+// pass (cross-session batching): rows are concatenated, each row appends to
+// and attends over its own session's cache (mega_forward's per-row banks).
+// Every kernel is batch invariant, so each response is bitwise the one the
+// step gets alone.
+void Server::run(std::vector<StepState*>& group) {
+    const ModelCfg& c = eng_.cfg();
     DeviceGuard g(eng_.device());
-    Workspace& ws = bank.ws();
-    cudaStream_t s = bank.stream();
-    const int in_f32 = f.h.dtype == wire::Dtype::f32;
-    const wire::Dtype out_dt = cfg_.response_dtype < 0 ? f.h.dtype
-                                                       : (cfg_.response_dtype == SFG_WIRE_F32 ? wire::Dtype::f32
-                                                                                              : wire::Dtype::f16);
-    const int n = seq * c.hidden_dim;
-    upload_meta(eng_, ws, hc.pos, mr, s);
-    ws.additive_mask = !mega_mask_ok(mr, bank.len());
-    SFG_CUDA(cudaMemcpyAsync(ws.wire, f.tensor, f.tensor_len, cudaMemcpyHostToDevice, s));
-    launch_unpack_rows(ws.wire, in_f32, n, ws.h, s);
+    StepState& s0 = *group.front();
+    Bank& bank0 = *s0.sess->bank;
+    Workspace& ws = bank0.ws();
+    cudaStream_t s = bank0.stream();
+    const int k = static_cast<int>(group.size());
+    std::vector<int32_t> pos;
+    MaskRuns mr;
+    std::vector<int> row0(k);
+    int rows = 0;
+    for (int i = 0; i < k; ++i) {
+        StepState& st = *group[i];
+        row0[i] = rows;
+        pos.insert(pos.end(), st.hc.pos.begin(), st.hc.pos.end());
+        const int base = static_cast<int>(mr.runs.size());
+        for (int r = 0; r < st.hc.seq; ++r) mr.row_off.push_back(base + st.mr.row_off[r]);
+        mr.runs.insert(mr.runs.end(), st.mr.runs.begin(), st.mr.runs.end());
+        rows += st.hc.seq;
+        if (i > 0) SFG_CUDA(cudaStreamSynchronize(st.sess->bank->stream()));  // its keep/crop kernels
+    }
+    mr.row_off.push_back(static_cast<int32_t>(mr.runs.size()));
+    upload_meta(eng_, ws, pos, mr, s);
+    ws.additive_mask = k > 1 ? false : !mega_mask_ok(s0.mr, bank0.len());
+    char* wire = static_cast<char*>(ws.wire);
+    for (int i = 0; i < k; ++i) {
+        StepState& st = *group[i];
+        const int in_f32 = st.f.h.dtype == wire::Dtype::f32;
+        const size_t off = static_cast<size_t>(row0[i]) * c.hidden_dim * 4;
+        SFG_CUDA(cudaMemcpyAsync(wire + off, st.f.tensor, st.f.tensor_len, cudaMemcpyHostToDevice, s));
+        launch_unpack_rows(wire + off, in_f32, st.hc.seq * c.hidden_dim, ws.h + static_cast<size_t>(row0[i]) * c.hidden_dim, s);
+    }
     SFG_CUDA(cudaMemsetAsync(ws.status, 0, sizeof(uint32_t), s));
-    eng_.set_prior(ws, bank.len(), s);
-    eng_.forward_device(bank, cfg_.layer_begin, cfg_.layer_end, seq, ws, s);
-    launch_pack_rows(ws.h, out_dt == wire::Dtype::f32, n, ws.wire, nullptr, s);
+    eng_.set_prior(ws, bank0.len(), s);
+    if (k == 1) {
+        eng_.forward_device(bank0, cfg_.layer_begin, cfg_.layer_end, rows, ws, s);
+    } else {
+        std::vector<Bank*> banks(k);
+        std::vector<int32_t> info(3 * rows);
+        for (int i = 0; i < k; ++i) {
+            Bank* b = group[i]->sess->bank.get();
+            banks[i] = b;
+            for (int r = 0; r < group[i]->hc.seq; ++r) {
+                const int row = row0[i] + r;
+                info[3 * row] = i;
+                info[3 * row + 1] = b->len() + r;
+                info[3 * row + 2] = b->len();
+            }
+        }
+        mega_forward(eng_, bank0, cfg_.layer_begin, cfg_.layer_end, rows, ws, s, &banks, info.data());
+        shared_passes_.fetch_add(1);
+    }
+    std::vector<std::vector<uint8_t>> payload(k);
+    for (int i = 0; i < k; ++i) {
+        StepState& st = *group[i];
+        const int n = st.hc.seq * c.hidden_dim;
+        const size_t off = static_cast<size_t>(row0[i]) * c.hidden_dim * 4;
+        launch_pack_rows(ws.h + static_cast<size_t>(row0[i]) * c.hidden_dim, st.out_dt == wire::Dtype::f32, n,
+                         wire + off, nullptr, s);
+        const size_t out_bytes = static_cast<size_t>(n) * wire::width(st.out_dt);
+        payload[i].resize(out_bytes + 4);
+        SFG_CUDA(cudaMemcpyAsync(payload[i].data(), wire + off, out_bytes, cudaMemcpyDeviceToHost, s));
+    }
     SFG_CUDA(cudaGetLastError());
-    thread_local std::vector<uint8_t> payload;
-    const size_t out_bytes = static_cast<size_t>(n) * wire::width(out_dt);
-    payload.resize(out_bytes + 4);
-    uint32_t* st = reinterpret_cast<uint32_t*>(static_cast<char*>(ws.pinned) + ws.pinned_bytes - 64);
-    SFG_CUDA(cudaMemcpyAsync(st, ws.status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    SFG_CUDA(cudaMemcpyAsync(payload.data(), ws.wire, out_bytes, cudaMemcpyDeviceToHost, s));
+    uint32_t* stw = reinterpret_cast<uint32_t*>(static_cast<char*>(ws.pinned) + ws.pinned_bytes - 64);
+    SFG_CUDA(cudaMemcpyAsync(stw, ws.status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     SFG_CUDA(cudaStreamSynchronize(s));
-    if (*st & ST_EMPTY_ROW) throw Error(Kind::protocol, "mask row admits no attendable position");
-    bank.set_len(bank.len() + seq);
-    if (prompt) bank.mark_committed(bank.len());
-    sess->last_active = now_s_();
-    const double srv_ms = (steady_seconds() - t0) * 1000.0;
+    if (*stw & ST_EMPTY_ROW) throw Error(Kind::protocol, "mask row admits no attendable position");
+    for (int i = 0; i < k; ++i) {
+        StepState& st = *group[i];
+        Bank& bank = *st.sess->bank;
+        bank.set_len(bank.len() + st.hc.seq);
+        if (st.prompt) bank.mark_committed(bank.len());
+        st.sess->last_active = now_s_();
+        wire::Header h;  // hidden_to_response (server.cpp:135-146)
+        h.kind = wire::FrameKind::response;
+        h.session_id = st.f.h.session_id;
+        h.shape = {st.hc.seq, c.hidden_dim};
+        h.dtype = st.out_dt;
+        h.srv_ms = (steady_seconds() - st.t0) * 1000.0;
+        wire::encode(h, payload[i].data(), payload[i].size() - 4, nullptr, 0, *st.resp);
+    }
+}
 
-    wire::Header h;  // hidden_to_response (server.cpp:135-146)
-    h.kind = wire::FrameKind::response;
-    h.session_id = f.h.session_id;
-    h.shape = {seq, c.hidden_dim};
-    h.dtype = out_dt;
-    h.srv_ms = srv_ms;
-    wire::encode(h, payload.data(), out_bytes, nullptr, 0, resp);
+void Server::handle_frame(const wire::FrameView& f, std::vector<uint8_t>& resp) {
+    if (f.h.kind == wire::FrameKind::ping) {  // handle_ping (server.cpp:193-201)
+        wire::Header h;
+        h.kind = wire::FrameKind::response;
+        h.session_id = f.h.session_id;
+        h.shape = {0};
+        h.dtype = f.h.dtype;
+        h.srv_ms = 0.0;
+        wire::encode(h, nullptr, 0, nullptr, 0, resp);
+        return;
+    }
+    StepState st;
+    st.resp = &resp;
+    prepare(f, st);
+    std::vector<StepState*> one{&st};
+    run(one);
+}
+
+// handle() over several frames: step frames of distinct sessions whose rows
+// fit one pass (<= 16 rows, masks inside the layer-stack contract) share ONE
+// weight pass; everything else is handled frame by frame.  Responses (and
+// error frames) are exactly what handle() returns for each frame.
+void Server::handle_batch(int n, const uint8_t* const* reqs, const size_t* lens,
+                          std::vector<std::vector<uint8_t>>& resps) {
+    resps.assign(static_cast<size_t>(n), {});
+    const bool batchable = eng_.fast() && eng_.tp_size() == 1 && rows_attention() && mega_mode() == 1;
+    std::vector<std::unique_ptr<StepState>> pending;
+    std::vector<StepState*> group;
+    int group_rows = 0;
+    auto flush = [&]() {
+        if (group.empty()) return;
+        try {
+            run(group);
+        } catch (const Error& e) {  // a failed shared pass: report it on each of its frames
+            for (StepState* st : group) error_frame(st->f.h.session_id, e.what(), *st->resp);
+        }
+        group.clear();
+        group_rows = 0;
+        pending.clear();
+    };
+    for (int i = 0; i < n; ++i) {
+        wire::FrameView f;
+        try {
+            f = wire::decode(reqs[i], lens[i]);
+        } catch (const Error& e) {
+            error_frame("", e.what(), resps[i]);
+            continue;
+        }
+        bool shared = false;
+        if (batchable && f.h.kind == wire::FrameKind::step) {
+            auto sess = find_session(f.h.session_id);
+            bool dup = false;
+            for (StepState* st : group) dup = dup || st->sess == sess;
+            shared = sess && !dup;
+        }
+        if (!shared) {
+            flush();
+            handle(reqs[i], lens[i], resps[i]);
+            continue;
+        }
+        auto st = std::make_unique<StepState>();
+        st->resp = &resps[i];
+        try {
+            prepare(f, *st);
+        } catch (const Error& e) {
+            error_frame(f.h.session_id, e.what(), resps[i]);
+            continue;
+        } catch (const std::exception& e) {
+            error_frame(f.h.session_id, std::string("internal: ") + e.what(), resps[i]);
+            continue;
+        }
+        Bank& b = *st->sess->bank;
+        const bool fits = mega_mask_ok(st->mr, b.len()) && st->hc.seq <= tc_rows();
+        if (!fits) {  // run it alone (its keep/crop already applied)
+            flush();
+            std::vector<StepState*> one{st.get()};
+            try {
+                run(one);
+            } catch (const Error& e) {
+                error_frame(f.h.session_id, e.what(), resps[i]);
+            }
+            continue;
+        }
+        if (group_rows + st->hc.seq > tc_rows() || static_cast<int>(group.size()) >= 16) flush();
+        group_rows += st->hc.seq;
+        group.push_back(st.get());
+        pending.push_back(std::move(st));
+    }
+    flush();
 }
 
 // handle_prompt / handle_step (server.cpp:203-265) for a device-linked

@@ -2,6 +2,7 @@
 // KV banks + the request state machine of PROTOCOL.md, with the middle-layer
 // forward on the B200.  handle() is the FrameHandler-compatible entry point.
 #pragma once
+#include <atomic>
 #include <functional>
 #include <map>
 #include <memory>
@@ -29,6 +30,12 @@ public:
 
     // ServerEngine::handle over encoded frames; never throws.
     void handle(const uint8_t* req, size_t n, std::vector<uint8_t>& resp);
+    // handle() over several frames; step frames of distinct sessions share one
+    // weight pass when their rows fit (cross-session batching); never throws.
+    void handle_batch(int n, const uint8_t* const* reqs, const size_t* lens,
+                      std::vector<std::vector<uint8_t>>& resps);
+    // Weight passes handle_batch shared between >= 2 sessions' steps.
+    uint64_t shared_passes() const { return shared_passes_.load(); }
 
     size_t expire_sessions();
     size_t session_count() const;
@@ -73,6 +80,24 @@ public:
     void linked_end(Lease& l, int seq);
 
 private:
+    struct StepState {
+        wire::FrameView f;
+        std::shared_ptr<Session> sess;
+        std::unique_lock<std::mutex> lock;
+        struct {
+            int seq = 0;
+            std::vector<int32_t> pos;
+        } hc;
+        MaskRuns mr;
+        bool prompt = false;
+        double t0 = 0.0;
+        wire::Dtype out_dt = wire::Dtype::f16;
+        std::vector<uint8_t>* resp = nullptr;
+    };
+    void prepare(const wire::FrameView& f, StepState& st);
+    void run(std::vector<StepState*>& group);
+    static int tc_rows() { return 16; }
+    std::atomic<uint64_t> shared_passes_{0};
     std::shared_ptr<Session> find_session(const std::string& id);
     std::shared_ptr<Session> create_or_reset_session(const std::string& id);
     void handle_frame(const wire::FrameView& f, std::vector<uint8_t>& resp);

@@ -239,11 +239,26 @@ class ServerEngine:
         check(_lib.lib().sfg_server_handle(self.h, buf, len(frame), C.byref(rp), C.byref(rn)))
         return C.string_at(rp, rn.value)
 
+    def handle_batch(self, frames) -> list:
+        """handle() over several queued frames; step frames of distinct sessions
+        share one weight pass (responses identical to handle() one by one)."""
+        n = len(frames)
+        bufs = [(C.c_uint8 * len(f)).from_buffer_copy(f) for f in frames]
+        reqs = (C.c_void_p * n)(*[C.addressof(b) for b in bufs])
+        lens = (C.c_size_t * n)(*[len(f) for f in frames])
+        rps = (C.POINTER(C.c_uint8) * n)()
+        rns = (C.c_size_t * n)()
+        check(_lib.lib().sfg_server_handle_batch(self.h, n, reqs, lens, rps, rns))
+        return [C.string_at(rps[i], rns[i]) for i in range(n)]
+
     @property
     def handler(self):
         """(C function pointer, ctx) usable as a FrameHandler by C clients."""
         fn = C.cast(_lib.lib().sfg_server_handle, C.c_void_p)
         return fn, self.h
+
+    def shared_passes(self) -> int:
+        return int(_lib.lib().sfg_server_shared_passes(self.h))
 
     def expire_sessions(self) -> int:
         return int(_lib.lib().sfg_server_expire_sessions(self.h))

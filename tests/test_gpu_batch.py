@@ -1,0 +1,126 @@
+"""Cross-session batching: ServerEngine.handle_batch runs the
+step frames of several sessions through ONE weight pass of the layer stack
+(each row appends to and attends over its own session's KV cache).
+
+Bar: every response is BITWISE the response ServerEngine.handle gives for
+the same frame one by one on an identical server (batch invariance of the
+FAST kernels), error frames included, and every session ends in the same
+state (server.hpp:49-59 SessionView)."""
+import numpy as np
+import pytest
+
+import paper_2602_16760_b200 as sfg
+import pyoracle as po
+import wirepy
+
+pytestmark = pytest.mark.gpu
+
+
+def scfg(c):
+    return sfg.ModelConfig(**{k: getattr(c, k) for k in po.ModelCfg.__dataclass_fields__})
+
+
+@pytest.fixture(scope="module")
+def desk_fast(port):
+    cfg = po.desk_cfg()
+    m = port.model(cfg, bf16=True)
+    eng = sfg.Engine(scfg(cfg), math=sfg.FAST, params=m.params())
+    return cfg, m, eng
+
+
+def _step(m, sid, prior, ids, keep=None, tree=False):
+    """A lookahead-shaped step: row 0 continues the sequence, the others are
+    draft branches that see the prefix and row 0 but not each other."""
+    n = len(ids)
+    pos = [prior + (1 if (tree and i) else i) for i in range(n)]
+    mask = None
+    if tree and n > 1:
+        mask = np.zeros((n, prior + n), np.float32)
+        for r in range(1, n):
+            for c in range(1, n):
+                if c != r:
+                    mask[r, prior + c] = -np.inf
+    kind = "accept_and_step" if keep is not None else "step"
+    return wirepy.hidden_request(kind, sid, m.embed_at(ids, pos), pos, keep=keep, mask=mask)
+
+
+def _run_pair(cfg, m, eng, rounds):
+    split = 2
+    a = sfg.ServerEngine(eng, sfg.ServerConfig(split, cfg.n_layers - split))
+    b = sfg.ServerEngine(eng, sfg.ServerConfig(split, cfg.n_layers - split))
+    for rnd in rounds:
+        frames = [f(m) for f in rnd]
+        got = a.handle_batch(frames)
+        want = [b.handle(f) for f in frames]
+        assert len(got) == len(want)
+        for i, (g, w) in enumerate(zip(got, want)):
+            assert wirepy.strip_srv_ms(g) == wirepy.strip_srv_ms(w), f"frame {i}"
+    for sid in ("s0", "s1", "s2", "s3", "s4"):
+        assert a.session_view(sid) == b.session_view(sid)
+    return a
+
+
+def _prompt(sid, ids):
+    return lambda m: wirepy.hidden_request("prompt", sid, m.embed_at(ids, list(range(len(ids)))),
+                                           list(range(len(ids))))
+
+
+def test_handle_batch_bitwise_equals_one_by_one(desk_fast):
+    cfg, m, eng = desk_fast
+    rng = np.random.default_rng(7)
+    ids = lambda n: rng.integers(0, cfg.vocab_size, n).tolist()  # noqa: E731
+    p = {f"s{i}": ids(3 + 2 * i) for i in range(5)}
+    lens = {k: len(v) for k, v in p.items()}
+    rounds = [[_prompt(k, v) for k, v in p.items()]]
+    # round 1: one plain step per session (5 sessions x 1 row -> one shared pass)
+    r1 = []
+    for k in p:
+        r1.append((lambda k=k, t=ids(1), L=lens[k]: lambda m: _step(m, k, L, t))())
+        lens[k] += 1
+    rounds.append(r1)
+    # round 2: lookahead trees (1 + 3 drafts) with keep of the provisional row;
+    # 4 x 4 = 16 rows in one pass, the fifth session starts the next group
+    r2 = []
+    for k in p:
+        r2.append((lambda k=k, t=ids(4), L=lens[k]: lambda m: _step(m, k, L, t, keep=[0], tree=True))())
+        lens[k] += 4
+    rounds.append(r2)
+    # round 3: mixed queue — ping, unknown session, a session twice, an
+    # over-wide step (17 rows, handled alone), and valid steps around them
+    r3 = [
+        (lambda k="s0", t=ids(2), L=lens["s0"]: lambda m: _step(m, k, L - 3, t, keep=[0]))(),
+        lambda m: wirepy.encode("ping", "x"),
+        (lambda t=ids(1): lambda m: _step(m, "ghost", 0, t))(),
+        (lambda k="s1", t=ids(3), L=lens["s1"]: lambda m: _step(m, k, L - 2, t, keep=[0, 1], tree=True))(),
+        (lambda k="s1", t=ids(1): lambda m: _step(m, k, 0, t))(),      # same session again: bad positions
+        (lambda k="s2", t=ids(17), L=lens["s2"]: lambda m: _step(m, k, L - 3, t, keep=[0]))(),
+        (lambda k="s3", t=ids(1), L=lens["s3"]: lambda m: _step(m, k, L - 2, t, keep=[0, 2]))(),
+        (lambda k="s4", t=ids(5), L=lens["s4"]: lambda m: _step(m, k, L - 3, t, keep=[0], tree=True))(),
+    ]
+    rounds.append(r3)
+    a = _run_pair(cfg, m, eng, rounds)
+    assert a.shared_passes() >= 3
+
+
+def test_handle_batch_continues_decoding(desk_fast):
+    """Several steps per session through handle_batch, responses equal."""
+    cfg, m, eng = desk_fast
+    rng = np.random.default_rng(11)
+    sids = [f"s{i}" for i in range(5)]
+    lens = {}
+    rounds = [[]]
+    for i, k in enumerate(sids):
+        t = rng.integers(0, cfg.vocab_size, 4 + i).tolist()
+        rounds[0].append(_prompt(k, t))
+        lens[k] = len(t)
+    for step in range(6):
+        rnd = []
+        for k in sids:
+            t = rng.integers(0, cfg.vocab_size, 3).tolist()
+            keep = None if step == 0 else [0]
+            L = lens[k] - (0 if step == 0 else 2)
+            rnd.append((lambda k=k, t=t, L=L, keep=keep: lambda m: _step(m, k, L, t, keep=keep, tree=True))())
+            lens[k] = L + 3
+        rounds.append(rnd)
+    a = _run_pair(cfg, m, eng, rounds)
+    assert a.shared_passes() >= 6
