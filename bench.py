@@ -386,6 +386,13 @@ def run_ours(args, ws, rank, local):
                 L.sfg_decoder_destroy(d)
             del cls
 
+    # ── cross-session batching: the server's queue holds one
+    # lookahead step per session; sfg_server_handle_batch runs them in ONE
+    # weight pass vs ServerEngine.handle one by one (same frames, host buffers)
+    batching = {}
+    if not args.no_sweep:
+        batching = server_batch_sweep(sfg, eng, cfg, nl, rank)
+
     # ── privacy-depth sweep (configs[2]): 2/4/8 local layers each side ─────
     privacy = {}
     if not args.no_sweep:
@@ -447,6 +454,7 @@ def run_ours(args, ws, rank, local):
         "rtt_sweep": sweep,
         "privacy_sweep": privacy,
         "session_sweep": sessions,
+        "server_batching": batching,
         "clocks": clk.summary(),
     }
     if ws == 1 and not args.no_cpu:
@@ -463,6 +471,64 @@ def run_ours(args, ws, rank, local):
             line["cpu_baseline"] = {"value": None, "unit": "tok/s", "cores": 1, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
     print(json.dumps(line), flush=True)
+
+
+def server_batch_sweep(sfg, eng, cfg, nl, rank, rounds=6):
+    """Server-side step time for K sessions' queued lookahead steps (r rows
+    each, row 0 + r-1 draft branches, keep=[0] of the previous step): frames
+    one by one through handle() vs one handle_batch() per round."""
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests"))
+    import wirepy
+    import numpy as np
+    rng = np.random.default_rng(5 + rank)
+    H = cfg.hidden_dim
+    out = {}
+    for k, r in ((1, 4), (4, 4), (8, 2), (16, 1)):
+        res = {}
+        for mode in ("one_by_one", "batched"):
+            srv = sfg.ServerEngine(eng, sfg.ServerConfig(SPLIT, nl - SPLIT, max_sessions=64))
+            sids = [f"b{k}-{i}-{rank}" for i in range(k)]
+            lens = {}
+            for sid in sids:
+                n0 = PROMPT_LEN
+                srv.handle(wirepy.hidden_request("prompt", sid, rng.standard_normal((n0, H), np.float32),
+                                                 list(range(n0)), dtype="f16"))
+                lens[sid] = n0
+            plan = []
+            for rd in range(rounds + 2):
+                frames = []
+                for sid in sids:
+                    L0 = lens[sid] - (0 if rd == 0 else r - 1)
+                    pos = [L0] + [L0 + 1] * (r - 1)
+                    mask = None
+                    if r > 2:
+                        mask = np.zeros((r, L0 + r), np.float32)
+                        for a in range(1, r):
+                            for b in range(1, r):
+                                if a != b:
+                                    mask[a, L0 + b] = -np.inf
+                    rows = (0.5 * rng.standard_normal((r, H))).astype(np.float16).astype(np.float32)
+                    frames.append(wirepy.hidden_request("step" if rd == 0 else "accept_and_step", sid, rows, pos,
+                                                        dtype="f16", keep=None if rd == 0 else [0], mask=mask))
+                    lens[sid] = L0 + r
+                plan.append(frames)
+            for frames in plan[:2]:
+                srv.handle_batch(frames) if mode == "batched" else [srv.handle(f) for f in frames]
+            t0 = time.perf_counter()
+            for frames in plan[2:]:
+                if mode == "batched":
+                    resp = srv.handle_batch(frames)
+                else:
+                    resp = [srv.handle(f) for f in frames]
+            dt = (time.perf_counter() - t0) / rounds
+            assert all(wirepy.decode(x)[0]["kind"] == "response" for x in resp)
+            res[mode + "_ms_per_round"] = dt * 1000.0
+            if mode == "batched":
+                res["shared_passes"] = srv.shared_passes()
+            del srv
+        res["speedup"] = res["one_by_one_ms_per_round"] / res["batched_ms_per_round"]
+        out[f"{k}x{r}"] = {"sessions": k, "rows_per_step": r, **res}
+    return out
 
 
 def main():

@@ -385,7 +385,10 @@ void Server::handle_frame(const wire::FrameView& f, std::vector<uint8_t>& resp) 
 void Server::handle_batch(int n, const uint8_t* const* reqs, const size_t* lens,
                           std::vector<std::vector<uint8_t>>& resps) {
     resps.assign(static_cast<size_t>(n), {});
-    const bool batchable = eng_.fast() && eng_.tp_size() == 1 && rows_attention() && mega_mode() == 1;
+    // the shared pass is the layer-stack megakernel; one-by-one steps take it
+    // too for these shapes, so responses stay bitwise those of handle()
+    const bool batchable = eng_.fast() && eng_.tp_size() == 1 && rows_attention() && mega_mode() == 1 &&
+                           mega_supported(eng_, 1, false) && cfg_.layer_end - cfg_.layer_begin <= 50;
     std::vector<std::unique_ptr<StepState>> pending;
     std::vector<StepState*> group;
     int group_rows = 0;
@@ -409,7 +412,7 @@ void Server::handle_batch(int n, const uint8_t* const* reqs, const size_t* lens,
             continue;
         }
         bool shared = false;
-        if (batchable && f.h.kind == wire::FrameKind::step) {
+        if (batchable && (f.h.kind == wire::FrameKind::step || f.h.kind == wire::FrameKind::accept_and_step)) {
             auto sess = find_session(f.h.session_id);
             bool dup = false;
             for (StepState* st : group) dup = dup || st->sess == sess;
