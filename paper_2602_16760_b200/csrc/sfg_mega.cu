@@ -93,6 +93,7 @@ struct MegaArgs {
     int spin_mma;      // dev knob: MMA issuer spins on test_wait instead of try_wait
     int bpf;           // bubble L2 prefetch depth in units (0: off)
     int G[4];          // per phase: CTAs sharing its stream-K split (phase_ctas)
+    int W[4];          // per phase: whole tiles per CTA after the split part (whole_tiles)
     int fl_base, fl_lay, fl_off[6];  // dataflow flag layout (see fptr)
     long long bpf_cycles;  // ring-full wait (SM cycles) that counts as a bubble
     uint8_t* xim[4];   // per phase: the GEMM's input as [KB][48 x 64] split bf16 images (put_split)
@@ -135,6 +136,8 @@ __device__ __forceinline__ unsigned long long* tslot(const MegaArgs& a, int c, i
 
 struct Geo {
     int tiles, KB, G;  // G: CTAs sharing this GEMM's stream-K split (see split_ctas)
+    int W;             // whole tiles per CTA, processed after its stream-K piece
+    __device__ __forceinline__ int split_units() const { return (tiles - W * G) * KB; }
 };
 // Stream-K split width: at most gridDim.x CTAs, each with at least
 // ceil((KB-1)/(kMaxPieces-1)) k-blocks so a tile never has more than
@@ -155,7 +158,7 @@ __device__ __forceinline__ Geo geom(const MegaArgs& a, int p) {
         case P_GU: t = a.F / 64; kb = a.H / kKB; break;
         default: t = (a.H + kM - 1) / kM; kb = a.F / kKB; break;
     }
-    return {t, kb, a.G[p]};  // CTAs sharing the phase's stream-K split (host: phase_ctas)
+    return {t, kb, a.G[p], a.W[p]};  // host: phase_ctas / whole_tiles
 }
 // CTAs of a phase's split.  A tile-aligned split is used when it keeps at
 // least align_pct % of the grid busy: every CTA then gets exactly one 1/P piece
@@ -184,17 +187,40 @@ inline int phase_ctas(int tiles, int KB, int grid, int align_pct) {
     return split_ctas(tiles, KB, grid);
 }
 
-// this CTA's unit range [st, en) of a phase (empty when c >= g.G)
-// (unit counts are small: tiles x k-blocks < 2^31, 32-bit math throughout)
-__device__ __forceinline__ void unit_range(const Geo& g, int c, int& st, int& en) {
-    const int U = g.tiles * g.KB;
+// Phases with more tiles than CTAs: every CTA also owns W whole tiles, and
+// only the remaining tiles are split stream-K.  A CTA runs its split piece
+// FIRST and its whole tiles last, so the split tiles' fixups (partial
+// stores, arrival counter, reduction) overlap the whole tiles' weight
+// streaming and the phase ends with plain epilogues.  The remainder must
+// keep every split tile within kMaxPieces pieces.
+inline int whole_tiles(int tiles, int KB, int G) {
+    if (G < 1 || tiles < G) return 0;
+    const int W = tiles / G;
+    const int rem = tiles - W * G;
+    if (rem == 0) return W;
+    const int min_units = (rem * KB) / G;  // smallest piece of a split tile
+    if (min_units < 1 || (KB + min_units - 1) / min_units + 1 > kMaxPieces) return 0;
+    return W;
+}
+// this CTA's units of a phase as segments: seg 0 = its piece of the split
+// tiles [0, tiles - W*G), seg 1 = its whole tiles (empty when W == 0; both
+// empty when c >= g.G).  32-bit unit math (tiles x k-blocks < 2^31).
+__device__ __forceinline__ void unit_seg(const Geo& g, int c, int seg, int& st, int& en) {
     if (c >= g.G) {
         st = en = 0;
         return;
     }
-    st = c * U / g.G;
-    en = (c + 1) * U / g.G;
+    if (seg == 0) {
+        const int U = g.split_units();
+        st = c * U / g.G;
+        en = (c + 1) * U / g.G;
+    } else {
+        const int t0 = g.tiles - g.W * g.G + c * g.W;
+        st = t0 * g.KB;
+        en = (t0 + g.W) * g.KB;
+    }
 }
+__device__ __forceinline__ void unit_range(const Geo& g, int c, int& st, int& en) { unit_seg(g, c, 0, st, en); }
 
 // ── grid barrier ──────────────────────────────────────────────────────────
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -1135,9 +1161,10 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                 for (int p = 0; p < 4; ++p) {
                     const Geo g = geom(a, p);
                     const uint8_t* W = a.layers[l].w[p];
-                    int st, en;
-                    unit_range(g, c, st, en);
                     unsigned long long wacc = 0;
+                    for (int sg = 0; sg < 2; ++sg) {
+                    int st, en;
+                    unit_seg(g, c, sg, st, en);
                     for (int u = st; u < en; ++u, ++n_cur) {
                         if (a.bpf > 0) {
                             if (!mbar_test(&empty[stage], ph ^ 1)) {
@@ -1173,6 +1200,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                             ph ^= 1;
                         }
                     }
+                    }
                     if (a.trace) *tslot(a, c, input_barrier(l, p), 5) = wacc;
                 }
         }
@@ -1183,11 +1211,10 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
             for (int l = 0; l < a.nlayers; ++l)
                 for (int p = 0; p < 4; ++p) {
                     const Geo g = geom(a, p);
-                    const int U = g.tiles * g.KB;
-                    int st, en;
-                (void)U;
-                unit_range(g, c, st, en);
                     unsigned long long wacc = 0;
+                    for (int sg = 0; sg < 2; ++sg) {
+                    int st, en;
+                    unit_seg(g, c, sg, st, en);
                     for (int u = st; u < en;) {
                         const int t = static_cast<int>(u / g.KB);
                         const int lo = u - t * g.KB;
@@ -1220,6 +1247,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                             acc_ph ^= 1;
                         }
                         u = t * g.KB + hi;
+                    }
                     }
                     if (a.trace) *tslot(a, c, input_barrier(l, p), 4) = wacc;
                 }
@@ -1254,13 +1282,15 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
             const LayerDesc& L = sh_layers[l];
             for (int p = 0; p < 4; ++p, ++gp) {
                 const Geo g = geom(a, p);
-                const int U = g.tiles * g.KB;
+                const int U = g.split_units();  // stream-K part (seg 0)
                 const int kind = K_QKV + (p == P_QKV ? 0 : p + 1);
                 float* parts = a.partials + (gp & 1) * a.part_stride;
                 int* cnts = a.counters + (gp & 1) * a.cnt_stride;
-                int st, en;
-                unit_range(g, c, st, en);
-                if ((p == P_QKV || p == P_GU) && st < en) {  // per-row 1/rms: needs every producer tile
+                int s0, e0, s1, e1;
+                unit_seg(g, c, 0, s0, e0);
+                unit_seg(g, c, 1, s1, e1);
+                const bool any = s0 < e0 || s1 < e1;
+                if ((p == P_QKV || p == P_GU) && any) {  // per-row 1/rms: needs every producer tile
                     if (et == 0)
                         wait_ge(p == P_QKV ? (l == 0 ? fptr(a, 0, K_STATS, tilesH) : fptr(a, l - 1, K_DOWN, tilesH))
                                            : fptr(a, l, K_O, tilesH),
@@ -1282,7 +1312,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     }
                     named_sync(1, 128);
                 }
-                if ((p == P_O || p == P_DOWN) && st < en) {  // residual rows of this phase are final
+                if ((p == P_O || p == P_DOWN) && any) {  // residual rows of this phase are final
                     if (et == 0) {
                         if (p == P_DOWN) wait_ge(fptr(a, l, K_O, tilesH), static_cast<unsigned>(tilesH));
                         else if (l > 0) wait_ge(fptr(a, l - 1, K_DOWN, tilesH), static_cast<unsigned>(tilesH));
@@ -1290,6 +1320,8 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     named_sync(1, 128);
                 }
                 unsigned long long t_acc = 0;
+                for (int sg = 0; sg < 2; ++sg) {
+                const int st = sg ? s1 : s0, en = sg ? e1 : e0;
                 for (int u = st; u < en;) {
                     const int t = static_cast<int>(u / g.KB);
                     const int lo = u - t * g.KB;
@@ -1385,6 +1417,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     }
                     u = t * g.KB + hi;
                 }
+                }
                 if (a.trace && et == 0) {
                     const int id = 5 * l + (p == P_QKV ? 1 : p + 2);
                     *tslot(a, c, input_barrier(l, p), 7) = gtimer();
@@ -1418,12 +1451,13 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     // input image, as soon as the producer tiles of that block are
                     // published (the 32 lanes poll the next 32 units' flags at once)
                     const Geo g = geom(a, p);
-                    int st, en;
-                    unit_range(g, c, st, en);
                     const uint8_t* X = a.xim[p];
                     unsigned long long xwacc = 0;
-                    int ready = st;
                     bool first = true;
+                    for (int sg = 0; sg < 2; ++sg) {
+                    int st, en;
+                    unit_seg(g, c, sg, st, en);
+                    int ready = st;
                     for (int u = st; u < en; ++u) {
                         if (u >= ready) {
                             unsigned long long spins = 0;
@@ -1452,6 +1486,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                             stage = 0;
                             ph ^= 1;
                         }
+                    }
                     }
                     if (a.trace && lane == 0) {
                         *tslot(a, c, input_barrier(l, p), 1) = gtimer();
@@ -1799,6 +1834,13 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         a.G[P_O] = phase_ctas(tH, dl.qd / tc::kKB, nsm, al_env);
         a.G[P_GU] = phase_ctas(dl.F / 64, dl.H / tc::kKB, nsm, al_env);
         a.G[P_DOWN] = phase_ctas(tH, dl.F / tc::kKB, nsm, al_env);
+        static const int whole_env = [] {
+            const char* v = getenv("SFG_MEGA_WHOLE");  // dev knob: 0 = plain stream-K everywhere
+            return v ? atoi(v) : 1;
+        }();
+        const int tiles_of[4] = {tQ, tH, dl.F / 64, tH};
+        const int kb_of[4] = {dl.H / tc::kKB, dl.qd / tc::kKB, dl.H / tc::kKB, dl.F / tc::kKB};
+        for (int p = 0; p < 4; ++p) a.W[p] = whole_env ? whole_tiles(tiles_of[p], kb_of[p], a.G[p]) : 0;
         // flag layout (must match kind_tiles): statistics tiles + counter, then
         // per layer QKV, attention kv heads, O, gate|up, down tiles + counter each
         const int kt[6] = {tH, tQ, dl.n_kv, tH, dl.F / 64, tH};

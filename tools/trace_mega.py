@@ -102,3 +102,30 @@ for l in range(1, NL - 1):
         d = (en[m] - st[m]) / 1000
         print(f"L{l} attention key walk per CTA: median {np.median(d):.1f} us max {d.max():.1f} us over {m.sum()} CTAs;"
               f" first start {(st[m].min() - t0) / 1000:.1f} last end {(en[m].max() - t0) / 1000:.1f}")
+# per-row attention items (ids 200 + l): entry, flags ok, q staged, walk end
+# per warp (8..15), combine end, published
+for l in range(1, NL - 1):
+    T = tr[:, 200 + l, :]
+    m = T[:, 0] > 0
+    if not m.any():
+        continue
+    T = T[m]
+    qkv_done = (tr[:, 5 * l + 1, 2].max() - t0) / 1000
+    rel = lambda v: (v - t0) / 1000  # noqa: E731
+    walk_end = T[:, 8:16].max(axis=1)
+    walk_first = np.where(T[:, 8:16] > 0, T[:, 8:16], np.iinfo(np.int64).max).min(axis=1)
+    def md(x):
+        return f"{np.median(x) / 1000:5.2f}/{x.max() / 1000:5.2f}"
+    print(f"L{l} attention items ({m.sum()} CTAs), QKV complete at {qkv_done:.1f}: "
+          f"entry med {np.median(rel(T[:, 0])):.1f} max {rel(T[:, 0]).max():.1f}; "
+          f"flag wait {md(T[:, 1] - T[:, 0])}, q stage {md(T[:, 2] - T[:, 1])}, "
+          f"walk first/last warp {md(walk_first - T[:, 2])} / {md(walk_end - T[:, 2])}, "
+          f"combine {md(T[:, 3] - walk_end)}, publish {md(T[:, 4] - T[:, 3])}; "
+          f"last published {rel(T[:, 4]).max():.1f}")
+# per-warp key-walk end (relative to q staged), median over CTAs
+for l in range(1, 3):
+    T = tr[:, 200 + l, :]
+    T = T[T[:, 0] > 0]
+    if T.size:
+        print(f"L{l} walk end per warp (us after q staged):",
+              " ".join(f"{np.median(T[:, 8 + w] - T[:, 2]) / 1000:5.2f}" for w in range(8)))
