@@ -478,7 +478,9 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
             const int tilesH = (a.H + kM - 1) / kM;
             const size_t slot = (static_cast<size_t>(l) * 2 + (p == P_O ? 0 : 1)) * tilesH + tile;
             float* dst = a.peer_inbox + slot * kRows * kM;
-            for (int r = 0; r < a.rows; ++r) dst[r * kM + m] = y[r];
+#pragma unroll
+            for (int r = 0; r < kRows; ++r)  // static bound: y[] stays in registers
+                if (r < a.rows) dst[r * kM + m] = y[r];
             __threadfence_system();
             named_sync(1, 128);
             if (et == 0) {
