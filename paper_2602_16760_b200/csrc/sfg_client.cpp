@@ -283,8 +283,9 @@ void Client::exchange_frames(bool prompt, int seq, const int32_t* pos, const Mas
     const int f32 = cfg_.wire_dtype == SFG_WIRE_F32;
     const size_t wbytes = static_cast<size_t>(n) * (f32 ? 4 : 2);
     prof_.launches += launch_pack_rows(ws.h, f32, n, ws.wire, ws.clamped, s);
-    payload_.resize(wbytes);
-    SFG_CUDA(cudaMemcpyAsync(payload_.data(), ws.wire, wbytes, cudaMemcpyDeviceToHost, s));
+    // the wire rows cross through pinned staging (async DMA, no driver bounce)
+    uint8_t* pin = static_cast<uint8_t*>(ws.wire_pin);
+    SFG_CUDA(cudaMemcpyAsync(pin, ws.wire, wbytes, cudaMemcpyDeviceToHost, s));
     wire::Header h;  // make_request (client.cpp:59-81)
     h.kind = prompt ? wire::FrameKind::prompt : (send_keep ? wire::FrameKind::accept_and_step : wire::FrameKind::step);
     h.session_id = sid_;
@@ -304,7 +305,7 @@ void Client::exchange_frames(bool prompt, int seq, const int32_t* pos, const Mas
     }
     SFG_CUDA(cudaEventRecord(ev_[1], s));
     SFG_CUDA(cudaStreamSynchronize(s));
-    wire::encode(h, payload_.data(), wbytes, reinterpret_cast<const uint8_t*>(mask.data()), mask.size() * 2, req_);
+    wire::encode(h, pin, wbytes, reinterpret_cast<const uint8_t*>(mask.data()), mask.size() * 2, req_);
     sleep_one_way();
     const uint8_t* resp = nullptr;
     size_t rlen = 0;
@@ -313,11 +314,10 @@ void Client::exchange_frames(bool prompt, int seq, const int32_t* pos, const Mas
         dead_ = true;
         throw Error(Kind::transport, "frame handler failed");
     }
-    std::vector<uint8_t> rcopy(resp, resp + rlen);
     sleep_one_way();
-    wire::FrameView r;
+    wire::FrameView r;  // views into the handler's buffer (valid until its next call)
     try {
-        r = wire::decode(rcopy.data(), rcopy.size());
+        r = wire::decode(resp, rlen);
     } catch (...) {
         dead_ = true;
         throw;
@@ -336,10 +336,15 @@ void Client::exchange_frames(bool prompt, int seq, const int32_t* pos, const Mas
         dead_ = true;
         throw Error(Kind::protocol, "response tensor shape mismatch");
     }
-    SFG_CUDA(cudaMemcpyAsync(ws.wire, r.tensor, r.tensor_len, cudaMemcpyHostToDevice, s));
+    if (r.tensor_len > static_cast<size_t>(ws.cap_rows) * c.hidden_dim * 4) {
+        dead_ = true;
+        throw Error(Kind::protocol, "response tensor exceeds the workspace");
+    }
+    std::memcpy(pin, r.tensor, r.tensor_len);
+    SFG_CUDA(cudaMemcpyAsync(ws.wire, pin, r.tensor_len, cudaMemcpyHostToDevice, s));
     prof_.launches += launch_unpack_rows(ws.wire, r.h.dtype == wire::Dtype::f32, n, ws.h, s);
     SFG_CUDA(cudaEventRecord(ev_[2], s));
-    SFG_CUDA(cudaStreamSynchronize(s));  // rcopy must outlive the copy
+    SFG_CUDA(cudaStreamSynchronize(s));  // the staging buffer is reused next step
 }
 
 // SplitClient::prefill (client.cpp:120-167)

@@ -125,7 +125,7 @@ private:
     float* h_logits_ = nullptr;     // pinned [out_rows_ x vocab]
     int out_rows_ = 0;
     std::vector<Graph> graphs_;
-    std::vector<uint8_t> req_, payload_;
+    std::vector<uint8_t> req_;
 };
 
 // decode_sequential / decode_lookahead_with_pool (decoding.cpp:111-355) as a

@@ -134,6 +134,7 @@ void Workspace::release() {
     if (pinned) cudaFreeHost(pinned);
     if (meta_pin) cudaFreeHost(meta_pin);
     if (stage_pin) cudaFreeHost(stage_pin);
+    if (wire_pin) cudaFreeHost(wire_pin);
     *this = Workspace{};
 }
 
@@ -174,6 +175,8 @@ void Engine::ensure_ws(Workspace& ws, int rows, int runs, int logit_rows) {
             ws.fast_bytes = fast_workspace_bytes(c, r);
             grow(&ws.fast, ws.fast_bytes);
         }
+        if (ws.wire_pin) cudaFreeHost(ws.wire_pin);
+        SFG_CUDA(cudaMallocHost(&ws.wire_pin, sizeof(float) * r * H));
         const size_t pin = sizeof(float) * r * std::max<size_t>(H, 64) * 2 + 4096 * 16;
         if (pin > ws.pinned_bytes) {
             if (ws.pinned) cudaFreeHost(ws.pinned);

@@ -85,6 +85,7 @@ struct Workspace {
     size_t fast_bytes = 0;
     void* pinned = nullptr;        // host staging
     size_t pinned_bytes = 0;
+    void* wire_pin = nullptr;      // pinned wire rows [cap_rows x H] (4 B each): frame tensors cross here
     // Per-step scalars read by kernels from device memory, so one captured
     // CUDA graph serves every step of a given batch size:
     //   meta[0] = cache length before the batch (QKV epilogue KV slot base)

@@ -305,7 +305,9 @@ void Server::run(std::vector<StepState*>& group) {
         StepState& st = *group[i];
         const int in_f32 = st.f.h.dtype == wire::Dtype::f32;
         const size_t off = static_cast<size_t>(row0[i]) * c.hidden_dim * 4;
-        SFG_CUDA(cudaMemcpyAsync(wire + off, st.f.tensor, st.f.tensor_len, cudaMemcpyHostToDevice, s));
+        char* pin = static_cast<char*>(ws.wire_pin) + off;  // pinned: an async DMA, no driver staging
+        std::memcpy(pin, st.f.tensor, st.f.tensor_len);
+        SFG_CUDA(cudaMemcpyAsync(wire + off, pin, st.f.tensor_len, cudaMemcpyHostToDevice, s));
         launch_unpack_rows(wire + off, in_f32, st.hc.seq * c.hidden_dim, ws.h + static_cast<size_t>(row0[i]) * c.hidden_dim, s);
     }
     SFG_CUDA(cudaMemsetAsync(ws.status, 0, sizeof(uint32_t), s));
@@ -328,16 +330,16 @@ void Server::run(std::vector<StepState*>& group) {
         mega_forward(eng_, bank0, cfg_.layer_begin, cfg_.layer_end, rows, ws, s, &banks, info.data());
         shared_passes_.fetch_add(1);
     }
-    std::vector<std::vector<uint8_t>> payload(k);
+    std::vector<size_t> out_bytes(k);
     for (int i = 0; i < k; ++i) {
         StepState& st = *group[i];
         const int n = st.hc.seq * c.hidden_dim;
         const size_t off = static_cast<size_t>(row0[i]) * c.hidden_dim * 4;
         launch_pack_rows(ws.h + static_cast<size_t>(row0[i]) * c.hidden_dim, st.out_dt == wire::Dtype::f32, n,
                          wire + off, nullptr, s);
-        const size_t out_bytes = static_cast<size_t>(n) * wire::width(st.out_dt);
-        payload[i].resize(out_bytes + 4);
-        SFG_CUDA(cudaMemcpyAsync(payload[i].data(), wire + off, out_bytes, cudaMemcpyDeviceToHost, s));
+        out_bytes[i] = static_cast<size_t>(n) * wire::width(st.out_dt);
+        SFG_CUDA(cudaMemcpyAsync(static_cast<char*>(ws.wire_pin) + off, wire + off, out_bytes[i],
+                                 cudaMemcpyDeviceToHost, s));
     }
     SFG_CUDA(cudaGetLastError());
     uint32_t* stw = reinterpret_cast<uint32_t*>(static_cast<char*>(ws.pinned) + ws.pinned_bytes - 64);
@@ -356,7 +358,8 @@ void Server::run(std::vector<StepState*>& group) {
         h.shape = {st.hc.seq, c.hidden_dim};
         h.dtype = st.out_dt;
         h.srv_ms = (steady_seconds() - st.t0) * 1000.0;
-        wire::encode(h, payload[i].data(), payload[i].size() - 4, nullptr, 0, *st.resp);
+        wire::encode(h, static_cast<const uint8_t*>(ws.wire_pin) + static_cast<size_t>(row0[i]) * c.hidden_dim * 4,
+                     out_bytes[i], nullptr, 0, *st.resp);
     }
 }
 
