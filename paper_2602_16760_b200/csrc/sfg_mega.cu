@@ -568,19 +568,22 @@ __device__ void attention_row_item(const MegaArgs& a, const LayerDesc& L, int l,
         const int c = ch * 8 + kk;
         const bool live = c < n;
         const int col = !live ? 0 : (c < prior ? c : sh_tail[row][c - prior]);
-        const float4* kr = reinterpret_cast<const float4*>(kb + static_cast<size_t>(col) * HD + sub * (HD / 4));
+        // lane `sub` of a key owns the key's float4 columns sub, sub+4, ...:
+        // the 4 lanes of a key read 64 contiguous bytes per load (not 4
+        // scattered 16-byte pieces), and their query reads hit 4 banks groups
+        const float4* kr = reinterpret_cast<const float4*>(kb + static_cast<size_t>(col) * HD) + sub;
         float4 k4[Q4];
 #pragma unroll
-        for (int t = 0; t < Q4; ++t) k4[t] = __ldcg(kr + t);
+        for (int t = 0; t < Q4; ++t) k4[t] = __ldcg(kr + 4 * t);
         float s[GR];
 #pragma unroll
         for (int g = 0; g < GR; ++g) {
             s[g] = 0.0f;
             if (g >= group) continue;
-            const float4* q4 = reinterpret_cast<const float4*>(qs + g * HD + sub * (HD / 4));
+            const float4* q4 = reinterpret_cast<const float4*>(qs + g * HD) + sub;
 #pragma unroll
             for (int t = 0; t < Q4; ++t) {
-                const float4 qq = q4[t];
+                const float4 qq = q4[4 * t];
                 s[g] += qq.x * k4[t].x + qq.y * k4[t].y + qq.z * k4[t].z + qq.w * k4[t].w;
             }
             s[g] += __shfl_xor_sync(0xffffffffu, s[g], 1);

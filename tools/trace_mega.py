@@ -129,3 +129,14 @@ for l in range(1, 3):
     if T.size:
         print(f"L{l} walk end per warp (us after q staged):",
               " ".join(f"{np.median(T[:, 8 + w] - T[:, 2]) / 1000:5.2f}" for w in range(8)))
+# clock64 breakdown of the per-row attention key walk (debug builds that
+# record ids 200/210/220 + l: scores, value loads, softmax + PV), cycles
+for l in range(1, 3):
+    parts = []
+    for base, name in ((200, "K+scores"), (210, "V loads"), (220, "softmax+PV")):
+        T = tr[:, base + l, :8]
+        v = T[T > 0]
+        if v.size:
+            parts.append(f"{name} med {np.median(v):.0f} max {v.max():.0f}")
+    if parts:
+        print(f"L{l} walk cycles per warp:", "; ".join(parts))
