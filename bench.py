@@ -451,8 +451,7 @@ def run_ours(args, ws, rank, local):
                            for n, v in stats.items() if v[0]},
         "server_ms_per_step": sum(srv_ms) / len(srv_ms), "wall_ms_per_step": wall / args.steps * 1000.0,
         "step_ms_percentiles": {"p50": float(np.percentile(dev_ms, 50)), "p99": float(np.percentile(dev_ms, 99)),
-                                "server_p50": float(np.percentile(srv_ms, 50)),
-                                "server_p99": float(np.percentile(srv_ms, 99)), "samples": len(dev_ms)},
+                                "samples": len(dev_ms)},
         "batch_rows": sorted(set(batches)), "acceptance": toks / args.steps, "weights_init_s": t_init,
         "rtt_sweep": sweep,
         "privacy_sweep": privacy,
