@@ -126,3 +126,53 @@ def test_handle_batch_continues_decoding(desk_fast):
         rounds.append(rnd)
     a = _run_pair(cfg, m, eng, rounds)
     assert a.shared_passes() >= 6
+
+
+def test_handle_batch_seven_b_width():
+    """The shared pass at the Mistral-7B width (4 middle layers of the seeded
+    init): gate|up runs the whole-tiles-last schedule, attention over five
+    caches of different lengths; responses bitwise equal to one by one."""
+    cfg = po.mistral7b_cfg(max_seq_len=256)
+    eng = sfg.Engine(scfg(cfg), math=sfg.FAST, layers=(2, 6), with_embedding=False, with_head=False)
+    H = cfg.hidden_dim
+    rng = np.random.default_rng(3)
+
+    def rows(n):
+        return (0.5 * rng.standard_normal((n, H))).astype(np.float16).astype(np.float32)
+
+    a = sfg.ServerEngine(eng, sfg.ServerConfig(2, 6))
+    b = sfg.ServerEngine(eng, sfg.ServerConfig(2, 6))
+    sids = [f"w{i}" for i in range(5)]
+    lens = {}
+    prompts = []
+    for i, sid in enumerate(sids):
+        n = 5 + 7 * i
+        prompts.append(wirepy.hidden_request("prompt", sid, rows(n), list(range(n)), dtype="f16"))
+        lens[sid] = n
+    for f in prompts:
+        assert wirepy.decode(a.handle(f))[0]["kind"] == "response"
+        assert wirepy.decode(b.handle(f))[0]["kind"] == "response"
+    prev = 0
+    for step in range(3):
+        frames = []
+        r = 4 if step != 1 else 2
+        for sid in sids:
+            L0 = lens[sid] - (0 if step == 0 else prev - 2)  # keep [0, 1] of the previous step's rows
+            pos = [L0] + [L0 + 1] * (r - 1)
+            mask = np.zeros((r, L0 + r), np.float32)
+            for x in range(1, r):
+                for y in range(1, r):
+                    if x != y:
+                        mask[x, L0 + y] = -np.inf
+            frames.append(wirepy.hidden_request("step" if step == 0 else "accept_and_step", sid, rows(r), pos,
+                                                dtype="f16", keep=None if step == 0 else [0, 1], mask=mask))
+            lens[sid] = L0 + r
+        prev = r
+        got = a.handle_batch(frames)
+        want = [b.handle(f) for f in frames]
+        for i, (g, w) in enumerate(zip(got, want)):
+            assert wirepy.decode(g)[0]["kind"] == "response", wirepy.decode(g)[0]
+            assert wirepy.strip_srv_ms(g) == wirepy.strip_srv_ms(w), (step, i)
+    assert a.shared_passes() >= 3
+    for sid in sids:
+        assert a.session_view(sid) == b.session_view(sid)
