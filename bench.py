@@ -554,7 +554,7 @@ def main():
     # attention kernel of the layer-stack: per-(row, kv head) items for short
     # contexts, key-chunked items sharing K/V across rows for long ones (both
     # batch invariant; fixed for the whole run)
-    os.environ.setdefault("SFG_ATTN", "chunked" if PROMPT_LEN >= 512 else "rows")
+    os.environ.setdefault("SFG_ATTN", "chunked" if PROMPT_LEN >= 1024 else "rows")
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     ws, rank, local = dist_setup()
     if args.impl == "reference":
