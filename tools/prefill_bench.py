@@ -1,0 +1,46 @@
+"""Time the prompt (prefill) forward of the 28 middle layers at the 7B shape.
+
+handle_prompt (server.cpp:203-224) runs forward_layers over the whole prompt;
+here: sfg_forward_layers over P rows with the causal mask, FAST math, host
+buffers (sync call).  Prints one JSON line per prompt length.
+    python tools/prefill_bench.py [P ...]
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2602_16760_b200 as sfg  # noqa: E402
+
+H_7B = dict(vocab_size=32768, n_layers=32, hidden_dim=4096, n_heads=32, n_kv_heads=8, head_dim=128, ffn_dim=14336,
+            max_seq_len=4096, rope_base=1e6, rms_eps=1e-5, seed=1234)
+
+
+def main():
+    lens = [int(a) for a in sys.argv[1:]] or [256, 2048]
+    eng = sfg.Engine(sfg.ModelConfig(**H_7B), math=sfg.FAST, layers=(2, 30), with_embedding=False, with_head=False)
+    rng = np.random.default_rng(0)
+    for P in lens:
+        h = (rng.standard_normal((P, 4096)) * 0.5).astype(np.float32)
+        pos = np.arange(P, dtype=np.int32)
+        bank = eng.bank(2, 30)
+        eng.forward_layers(2, 30, h, pos, bank)  # warm-up (workspace growth, graph-free path)
+        ts = []
+        for _ in range(3):
+            bank.reset()
+            t0 = time.perf_counter()
+            out = eng.forward_layers(2, 30, h, pos, bank)
+            ts.append(time.perf_counter() - t0)
+        wbytes = 28 * 436.2e6
+        print(json.dumps({"prompt_len": P, "middle_layers": 28, "ms": min(ts) * 1e3,
+                          "ms_per_token": min(ts) * 1e3 / P,
+                          "weight_bytes_per_16_rows_gb": wbytes / 1e9,
+                          "checksum": float(np.abs(out).astype(np.float64).sum())}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
