@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <initializer_list>
+#include <type_traits>
 
 #include "sfg_engine.h"
 #include "sfg_expf.h"
@@ -45,6 +46,16 @@ constexpr int kThreads = 192;
 constexpr int kAccCols = 64;           // TMEM columns per accumulator (48 used)
 constexpr int kTmemCols = 128;         // two accumulators
 constexpr int kMaxPieces = 16;
+// Prompt passes: one launch feeds each weight stage to NC 16-row chunks (NC
+// accumulators of N = 48 in TMEM), so a prompt streams the weights once per
+// NC chunks instead of once per chunk.  Each chunk's MMAs and k order are
+// those of the one-chunk kernel, so results are bitwise the same.
+constexpr int kPromptChunks = 4;
+template <int NC> constexpr int stage_bytes() { return kABytes + NC * kBBytes; }
+template <int NC> constexpr int n_stages() { return NC == 1 ? kStages : (200 * 1024) / stage_bytes<NC>(); }
+template <int NC> constexpr int acc_cols() { return NC == 1 ? kAccCols : 256; }
+template <int NC> constexpr int tmem_cols() { return 2 * acc_cols<NC>(); }
+static_assert(kPromptChunks * kN <= 256, "prompt chunks must fit one 256-column accumulator");
 
 enum Epi : int { EPI_RESID = 0, EPI_QKV = 1, EPI_GATEUP = 2, EPI_HEAD = 3 };
 
@@ -74,6 +85,12 @@ struct GemmArgs {
     // EPI_HEAD
     float* amax_val;    // [rows_total][tiles]
     int32_t* amax_idx;
+    // multi-chunk launches: chunk j >= 1 reads X2 + (j-1)*KB*kBBytes and keeps its
+    // stream-K partials / counters at partials2 + (j-1)*tiles*kMaxPieces*kRows*kM,
+    // counters2 + (j-1)*tiles
+    const uint8_t* X2;
+    float* partials2;
+    int* counters2;
 };
 
 // ── PTX wrappers ──────────────────────────────────────────────────────────
@@ -263,13 +280,54 @@ __device__ __forceinline__ void final_epilogue(const GemmArgs& a, int tile, int 
 }
 
 // ── the kernel ────────────────────────────────────────────────────────────
+// One accumulated piece [lo, hi) of tile t for one 16-row chunk: a whole tile
+// goes straight to the epilogue; a split tile deposits its partial and the
+// last arriver reduces the pieces in k order.
 template <int EPI>
+__device__ __forceinline__ void finish_piece(const GemmArgs& a, int t, int lo, int hi, const float (&y)[kRows],
+                                             float* xch, int* flag, int G, long long U, int c, int m, int et) {
+    if (lo == 0 && hi == a.KB) {
+        final_epilogue<EPI>(a, t, m, y, xch);
+        return;
+    }
+    const long long first_u = static_cast<long long>(t) * a.KB;
+    const int c_first = static_cast<int>(((first_u + 1) * G - 1) / U);
+    const int piece = c - c_first;
+    const long long last_u = first_u + a.KB - 1;
+    const int n_pieces = static_cast<int>(((last_u + 1) * G - 1) / U) - c_first + 1;
+    float* slot = a.partials + (static_cast<size_t>(t) * kMaxPieces + piece) * kRows * kM;
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) slot[r * kM + m] = y[r];
+    __threadfence();
+    named_sync(1, 128);
+    if (et == 0) {
+        const int old = atomicAdd(&a.counters[t], 1);
+        *flag = (old == n_pieces - 1) ? 1 : 0;
+        if (old == n_pieces - 1) a.counters[t] = 0;  // reset for the next launch
+    }
+    named_sync(1, 128);
+    if (*flag) {
+        __threadfence();
+        float s[kRows];
+        const float* p0 = a.partials + static_cast<size_t>(t) * kMaxPieces * kRows * kM;
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) s[r] = __ldcg(p0 + r * kM + m);
+        for (int p = 1; p < n_pieces; ++p)
+#pragma unroll
+            for (int r = 0; r < kRows; ++r) s[r] = s[r] + __ldcg(p0 + (static_cast<size_t>(p) * kRows + r) * kM + m);
+        final_epilogue<EPI>(a, t, m, s, xch);
+    }
+    named_sync(1, 128);
+}
+
+template <int EPI, int NC = 1>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ GemmArgs a) {
+    constexpr int kSt = n_stages<NC>(), kSB = stage_bytes<NC>(), kAcc = acc_cols<NC>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-    uint64_t* empty = full + kStages;
-    uint64_t* tfull = empty + kStages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kSB);
+    uint64_t* empty = full + kSt;
+    uint64_t* tfull = empty + kSt;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     int* flag = reinterpret_cast<int*>(tmem_slot + 4);
@@ -277,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kSt; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -290,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(kTmemCols)
+                     "r"(tmem_cols<NC>())
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -313,11 +371,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                 const int hi = static_cast<int>(min(end - static_cast<long long>(t) * a.KB, static_cast<long long>(a.KB)));
                 for (int kb = lo; kb < hi; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* sa = smem + stage * kStageBytes;
-                    mbar_expect_tx(&full[stage], kStageBytes);
+                    uint8_t* sa = smem + stage * kSB;
+                    mbar_expect_tx(&full[stage], kSB);
                     bulk_g2s(sa, a.W + (static_cast<size_t>(t) * a.KB + kb) * kABytes, kABytes, &full[stage]);
                     bulk_g2s(sa + kABytes, a.X + static_cast<size_t>(kb) * kBBytes, kBBytes, &full[stage]);
-                    if (++stage == kStages) {
+#pragma unroll
+                    for (int j = 1; j < NC; ++j)
+                        bulk_g2s(sa + kABytes + j * kBBytes,
+                                 a.X2 + (static_cast<size_t>(j - 1) * a.KB + kb) * kBBytes, kBBytes, &full[stage]);
+                    if (++stage == kSt) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -335,17 +397,21 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                 const int hi = static_cast<int>(min(end - static_cast<long long>(t) * a.KB, static_cast<long long>(a.KB)));
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                const uint32_t d = tmem + acc * kAccCols;
+                const uint32_t d = tmem + acc * kAcc;
                 for (int kb = lo; kb < hi; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t sa = smem_u32(smem + stage * kStageBytes);
-                    const uint64_t da = smem_desc(sa), db = smem_desc(sa + kABytes);
+                    const uint32_t sa = smem_u32(smem + stage * kSB);
+                    const uint64_t da = smem_desc(sa);
 #pragma unroll
-                    for (int k = 0; k < kKB / 16; ++k)  // +32 bytes per K=16 step inside the swizzle row
-                        mma_bf16(d, da + 2 * k, db + 2 * k, (kb > lo || k > 0) ? 1u : 0u);
+                    for (int j = 0; j < NC; ++j) {
+                        const uint64_t db = smem_desc(sa + kABytes + j * kBBytes);
+#pragma unroll
+                        for (int k = 0; k < kKB / 16; ++k)  // +32 bytes per K=16 step inside the swizzle row
+                            mma_bf16(d + j * kN, da + 2 * k, db + 2 * k, (kb > lo || k > 0) ? 1u : 0u);
+                    }
                     mma_commit(&empty[stage]);
-                    if (++stage == kStages) {
+                    if (++stage == kSt) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -370,55 +436,53 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             const int hi = static_cast<int>(min(end - static_cast<long long>(t) * a.KB, static_cast<long long>(a.KB)));
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            float v[kN];
-            const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * kAccCols;
-            tmem_ld16(ta, v);
-            tmem_ld16(ta + 16, v + 16);
-            tmem_ld16(ta + 32, v + 32);
-            tmem_wait_ld();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * kAcc;
+            if constexpr (NC == 1) {
+                float v[kN];
+                tmem_ld16(ta, v);
+                tmem_ld16(ta + 16, v + 16);
+                tmem_ld16(ta + 32, v + 32);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                float y[kRows];
+#pragma unroll
+                for (int r = 0; r < kRows; ++r) y[r] = (v[r] + v[kRows + r]) + v[2 * kRows + r];
+                finish_piece<EPI>(a, t, lo, hi, y, xch, flag, G, U, c, m, et);
+            } else {
+                for (int j = 0; j < NC; ++j) {
+                    float v[kN];
+                    tmem_ld16(ta + j * kN, v);
+                    tmem_ld16(ta + j * kN + 16, v + 16);
+                    tmem_ld16(ta + j * kN + 32, v + 32);
+                    tmem_wait_ld();
+                    if (j == NC - 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                    }
+                    if (j * kRows >= a.rows) continue;  // uniform: no valid row in this chunk
+                    float y[kRows];
+#pragma unroll
+                    for (int r = 0; r < kRows; ++r) y[r] = (v[r] + v[kRows + r]) + v[2 * kRows + r];
+                    if (j == 0) {
+                        GemmArgs ac = a;
+                        ac.rows = min(kRows, a.rows);
+                        finish_piece<EPI>(ac, t, lo, hi, y, xch, flag, G, U, c, m, et);
+                    } else {
+                        GemmArgs ac = a;
+                        ac.rows = min(kRows, a.rows - j * kRows);
+                        ac.row0 = a.row0 + j * kRows;
+                        ac.partials = a.partials2 + static_cast<size_t>(j - 1) * a.tiles * kMaxPieces * kRows * kM;
+                        ac.counters = a.counters2 + static_cast<size_t>(j - 1) * a.tiles;
+                        finish_piece<EPI>(ac, t, lo, hi, y, xch, flag, G, U, c, m, et);
+                    }
+                }
+            }
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
-            }
-            float y[kRows];
-#pragma unroll
-            for (int r = 0; r < kRows; ++r) y[r] = (v[r] + v[kRows + r]) + v[2 * kRows + r];
-
-            if (lo == 0 && hi == a.KB) {
-                final_epilogue<EPI>(a, t, m, y, xch);
-            } else {
-                // split tile: deposit this piece, the last arriver reduces in k order
-                const long long first_u = static_cast<long long>(t) * a.KB;
-                const int c_first = static_cast<int>(((first_u + 1) * G - 1) / U);
-                const int piece = c - c_first;
-                const long long last_u = first_u + a.KB - 1;
-                const int n_pieces = static_cast<int>(((last_u + 1) * G - 1) / U) - c_first + 1;
-                float* slot = a.partials + (static_cast<size_t>(t) * kMaxPieces + piece) * kRows * kM;
-#pragma unroll
-                for (int r = 0; r < kRows; ++r) slot[r * kM + m] = y[r];
-                __threadfence();
-                named_sync(1, 128);
-                if (et == 0) {
-                    const int old = atomicAdd(&a.counters[t], 1);
-                    *flag = (old == n_pieces - 1) ? 1 : 0;
-                    if (old == n_pieces - 1) a.counters[t] = 0;  // reset for the next launch
-                }
-                named_sync(1, 128);
-                if (*flag) {
-                    __threadfence();
-                    float s[kRows];
-                    const float* p0 = a.partials + static_cast<size_t>(t) * kMaxPieces * kRows * kM;
-#pragma unroll
-                    for (int r = 0; r < kRows; ++r) s[r] = __ldcg(p0 + r * kM + m);
-                    for (int p = 1; p < n_pieces; ++p)
-#pragma unroll
-                        for (int r = 0; r < kRows; ++r) s[r] = s[r] + __ldcg(p0 + (static_cast<size_t>(p) * kRows + r) * kM + m);
-                    final_epilogue<EPI>(a, t, m, s, xch);
-                }
-                named_sync(1, 128);
             }
             u = static_cast<long long>(t) * a.KB + hi;
         }
@@ -427,7 +491,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols<NC>())
+                     : "memory");
     }
 }
 
@@ -555,20 +620,21 @@ __global__ void relayout_kernel(const __nv_bfloat16* __restrict__ s0, const __nv
     }
 }
 
+template <int NC = 1>
 constexpr size_t smem_bytes() {
-    return 1024 + static_cast<size_t>(kStages) * kStageBytes + 2 * kStages * 8 + 4 * 8 + 16 + 16 +
+    return 1024 + static_cast<size_t>(n_stages<NC>()) * stage_bytes<NC>() + 2 * n_stages<NC>() * 8 + 4 * 8 + 16 + 16 +
            (64 * kRows + 8 * kRows) * 4;
 }
 
-template <int EPI>
+template <int EPI, int NC = 1>
 void launch_gemm(const GemmArgs& a, int grid, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
-        SFG_CUDA(cudaFuncSetAttribute(gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem_bytes())));
+        SFG_CUDA(cudaFuncSetAttribute(gemm_kernel<EPI, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem_bytes<NC>())));
         configured = true;
     }
-    gemm_kernel<EPI><<<grid, kThreads, smem_bytes(), s>>>(a);
+    gemm_kernel<EPI, NC><<<grid, kThreads, smem_bytes<NC>(), s>>>(a);
 }
 
 int num_sms() {
@@ -595,7 +661,15 @@ struct FastWs {
     int* counters;     // [tiles_max]
     float* amax_val;   // [rows][tiles_head]
     int32_t* amax_idx;
+    uint8_t* xs2;      // prompt chunks 1..kPromptChunks-1: [chunk][KBmax][kBBytes]
+    float* partials2;  // [chunk][layer_tiles_max][kMaxPieces][kRows][kM]
+    int* counters2;    // [chunk][layer_tiles_max]
 };
+size_t max_layer_tiles(const ModelCfg& c) {
+    const int qkv = tiles_for(c.q_dim() + 2 * c.kv_dim());
+    const int gu = (c.ffn_dim + 63) / 64;
+    return static_cast<size_t>(std::max({qkv, gu, tiles_for(c.hidden_dim)}));
+}
 size_t max_tiles(const ModelCfg& c) {
     const int qkv = tiles_for(c.q_dim() + 2 * c.kv_dim());
     const int gu = (c.ffn_dim + 63) / 64;
@@ -618,6 +692,10 @@ FastWs carve(const ModelCfg& c, Workspace& ws, int rows) {
     f.counters = reinterpret_cast<int*>(take(max_tiles(c) * sizeof(int)));
     f.amax_val = reinterpret_cast<float*>(take(static_cast<size_t>(rows) * tiles_for(c.vocab_size) * sizeof(float)));
     f.amax_idx = reinterpret_cast<int32_t*>(take(static_cast<size_t>(rows) * tiles_for(c.vocab_size) * sizeof(int32_t)));
+    const size_t extra = kPromptChunks - 1;
+    f.xs2 = take(extra * max_kb(c) * kBBytes);
+    f.partials2 = reinterpret_cast<float*>(take(extra * max_layer_tiles(c) * kMaxPieces * kRows * kM * sizeof(float)));
+    f.counters2 = reinterpret_cast<int*>(take(extra * max_layer_tiles(c) * sizeof(int)));
     return f;
 }
 }  // namespace
@@ -626,8 +704,11 @@ float* fast_partials(const ModelCfg& c, Workspace& ws) { return carve(c, ws, ws.
 int* fast_counters(const ModelCfg& c, Workspace& ws) { return carve(c, ws, ws.cap_rows).counters; }
 
 size_t fast_workspace_bytes(const ModelCfg& c, int rows) {
+    const size_t extra = kPromptChunks - 1;
     return max_kb(c) * kBBytes + max_tiles(c) * kMaxPieces * kRows * kM * sizeof(float) + max_tiles(c) * sizeof(int) +
-           2 * static_cast<size_t>(rows) * tiles_for(c.vocab_size) * sizeof(float) + 8 * 1024;
+           2 * static_cast<size_t>(rows) * tiles_for(c.vocab_size) * sizeof(float) +
+           extra * (max_kb(c) * kBBytes + max_layer_tiles(c) * (kMaxPieces * kRows * kM * sizeof(float) + sizeof(int))) +
+           16 * 1024;
 }
 
 static void check_fast_shape(const ModelCfg& c) {
@@ -695,17 +776,47 @@ int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, i
     float* vc = b.vslab(layer);
     int n = 0;
     const double R = rows;
-    for (int p0 = 0; p0 < rows; p0 += kRows) {
-        const int pr = std::min(kRows, rows - p0);
+    // A pass covers one 16-row chunk, or (prompts: rows > 16) up to
+    // kPromptChunks chunks that share every weight stage.  Each projection runs
+    // GEMM-outer over the passes, so from the second pass on its weights
+    // (QKV 50 MB, O 32 MB at 7B) come from L2.  Passes touch disjoint rows.
+    const int step = rows > kRows ? kRows * kPromptChunks : kRows;
+    auto pass_args = [&](int p0, int pr) {
         GemmArgs a{};
         a.X = f.xs;
         a.partials = f.partials;
         a.counters = f.counters;
+        a.X2 = f.xs2;
+        a.partials2 = f.partials2;
+        a.counters2 = f.counters2;
         a.rows = pr;
         a.row0 = p0;
-        // attention-input RMSNorm + split, fused QKV + RoPE + KV append
-        prep_kernel<<<pr, kPrepThreads, 0, s>>>(ws.h + static_cast<size_t>(p0) * d.H, d.H, d.H, L.attn_norm, d.eps, f.xs);
+        return a;
+    };
+    // [RMSNorm] + 3-way split of the pass's rows into the chunk images
+    auto prep = [&](const float* x, int ld, int K, const float* gain, float eps, int p0, int pr) {
+        for (int j = 0; j * kRows < pr; ++j) {
+            uint8_t* dst = j == 0 ? f.xs : f.xs2 + static_cast<size_t>(j - 1) * (K / kKB) * kBBytes;
+            prep_kernel<<<std::min(kRows, pr - j * kRows), kPrepThreads, 0, s>>>(
+                x + static_cast<size_t>(p0 + j * kRows) * ld, ld, K, gain, eps, dst);
+            ++n;
+        }
+    };
+    auto gemm = [&](auto epi, const GemmArgs& a) {
+        constexpr int EPI = decltype(epi)::value;
+        if (a.rows > kRows)
+            launch_gemm<EPI, kPromptChunks>(a, grid_for(a.tiles, a.KB), s);
+        else
+            launch_gemm<EPI>(a, grid_for(a.tiles, a.KB), s);
         ++n;
+    };
+    using QKV = std::integral_constant<int, EPI_QKV>;
+    using RESID = std::integral_constant<int, EPI_RESID>;
+    using GATEUP = std::integral_constant<int, EPI_GATEUP>;
+    for (int p0 = 0; p0 < rows; p0 += step) {  // attention-input RMSNorm + split, fused QKV + RoPE + KV append
+        const int pr = std::min(step, rows - p0);
+        GemmArgs a = pass_args(p0, pr);
+        prep(ws.h, d.H, d.H, L.attn_norm, d.eps, p0, pr);
         a.W = static_cast<const uint8_t*>(L.f_qkv);
         a.tiles = tiles_for(d.qd + 2 * d.kvd);
         a.KB = d.H / kKB;
@@ -723,33 +834,18 @@ int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, i
         a.vc = vc;
         {
             ProfScope ps(K_QKV, s, 2.0 * d.H * a.n_out + 4.0 * pr * (d.H + a.n_out), 2.0 * pr * d.H * a.n_out);
-            launch_gemm<EPI_QKV>(a, grid_for(a.tiles, a.KB), s);
+            gemm(QKV{}, a);
         }
-        ++n;
     }
     {
         const double kvb = 2.0 * 4.0 * d.kvd * (prior + rows);
         ProfScope ps(K_ATTN, s, kvb + 8.0 * R * d.qd, 4.0 * R * d.qd * (prior + rows));
         n += launch_attention_fast(ws.q, kc, vc, ws.row_off, ws.runs, rows, d, ws.att, ws.status, s);
     }
-    // The remaining GEMMs run GEMM-outer over the 16-row chunks: every chunk of
-    // one projection is launched back to back, so from the second chunk on the
-    // projection's weights (O 32 MB, down 117 MB at 7B) are read from L2
-    // instead of HBM.  Chunks touch disjoint rows and each launch is the same
-    // as in a chunk-outer order, so the results are bitwise unchanged.
-    auto chunk_args = [&](int p0, int pr) {
-        GemmArgs a{};
-        a.X = f.xs;
-        a.partials = f.partials;
-        a.counters = f.counters;
-        a.rows = pr;
-        a.row0 = p0;
-        return a;
-    };
-    for (int p0 = 0; p0 < rows; p0 += kRows) {  // O-proj + residual
-        const int pr = std::min(kRows, rows - p0);
-        GemmArgs a = chunk_args(p0, pr);
-        prep_kernel<<<pr, kPrepThreads, 0, s>>>(ws.att + static_cast<size_t>(p0) * d.qd, d.qd, d.qd, nullptr, 0.f, f.xs);
+    for (int p0 = 0; p0 < rows; p0 += step) {  // O-proj + residual
+        const int pr = std::min(step, rows - p0);
+        GemmArgs a = pass_args(p0, pr);
+        prep(ws.att, d.qd, d.qd, nullptr, 0.f, p0, pr);
         a.W = static_cast<const uint8_t*>(L.f_o);
         a.tiles = tiles_for(d.H);
         a.KB = d.qd / kKB;
@@ -759,15 +855,14 @@ int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, i
         a.store_only = e.tp_rank() > 0;  // rank 0 adds the residual, the others their partial
         {
             ProfScope ps(K_OPROJ, s, 2.0 * d.qd * d.H + 4.0 * pr * (d.qd + 2.0 * d.H), 2.0 * pr * d.qd * d.H);
-            launch_gemm<EPI_RESID>(a, grid_for(a.tiles, a.KB), s);
+            gemm(RESID{}, a);
         }
-        n += 2;
     }
     e.tp_allreduce(ws.h, static_cast<size_t>(rows) * d.H, s);
-    for (int p0 = 0; p0 < rows; p0 += kRows) {  // FFN RMSNorm + split, gate|up + SiLU*up
-        const int pr = std::min(kRows, rows - p0);
-        GemmArgs a = chunk_args(p0, pr);
-        prep_kernel<<<pr, kPrepThreads, 0, s>>>(ws.h + static_cast<size_t>(p0) * d.H, d.H, d.H, L.ffn_norm, d.eps, f.xs);
+    for (int p0 = 0; p0 < rows; p0 += step) {  // FFN RMSNorm + split, gate|up + SiLU*up
+        const int pr = std::min(step, rows - p0);
+        GemmArgs a = pass_args(p0, pr);
+        prep(ws.h, d.H, d.H, L.ffn_norm, d.eps, p0, pr);
         a.W = static_cast<const uint8_t*>(L.f_gu);
         a.tiles = (d.F + 63) / 64;
         a.KB = d.H / kKB;
@@ -776,14 +871,13 @@ int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, i
         a.ld = d.F;
         {
             ProfScope ps(K_GATEUP, s, 4.0 * d.H * d.F + 4.0 * pr * (d.H + d.F), 4.0 * pr * d.H * d.F);
-            launch_gemm<EPI_GATEUP>(a, grid_for(a.tiles, a.KB), s);
+            gemm(GATEUP{}, a);
         }
-        n += 2;
     }
-    for (int p0 = 0; p0 < rows; p0 += kRows) {  // down + residual
-        const int pr = std::min(kRows, rows - p0);
-        GemmArgs a = chunk_args(p0, pr);
-        prep_kernel<<<pr, kPrepThreads, 0, s>>>(ws.act + static_cast<size_t>(p0) * d.F, d.F, d.F, nullptr, 0.f, f.xs);
+    for (int p0 = 0; p0 < rows; p0 += step) {  // down + residual
+        const int pr = std::min(step, rows - p0);
+        GemmArgs a = pass_args(p0, pr);
+        prep(ws.act, d.F, d.F, nullptr, 0.f, p0, pr);
         a.W = static_cast<const uint8_t*>(L.f_down);
         a.tiles = tiles_for(d.H);
         a.KB = d.F / kKB;
@@ -793,9 +887,8 @@ int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, i
         a.store_only = e.tp_rank() > 0;
         {
             ProfScope ps(K_DOWN, s, 2.0 * d.F * d.H + 4.0 * pr * (d.F + 2.0 * d.H), 2.0 * pr * d.F * d.H);
-            launch_gemm<EPI_RESID>(a, grid_for(a.tiles, a.KB), s);
+            gemm(RESID{}, a);
         }
-        n += 2;
     }
     e.tp_allreduce(ws.h, static_cast<size_t>(rows) * d.H, s);
     SFG_CUDA(cudaGetLastError());

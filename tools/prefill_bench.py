@@ -10,6 +10,8 @@ import os
 import sys
 import time
 
+import ctypes as C
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -35,11 +37,23 @@ def main():
             t0 = time.perf_counter()
             out = eng.forward_layers(2, 30, h, pos, bank)
             ts.append(time.perf_counter() - t0)
+        L = sfg.lib()
+        L.sfg_profiler_reset()
+        L.sfg_profiler_enable(1)
+        bank.reset()
+        eng.forward_layers(2, 30, h, pos, bank)
+        L.sfg_profiler_enable(0)
+        classes = {}
+        for ci, name in enumerate(["qkv", "attention", "o_proj", "gate_up", "down"]):
+            cnt, ms, by, fl = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+            L.sfg_profiler_stats(ci, C.byref(cnt), C.byref(ms), C.byref(by), C.byref(fl))
+            classes[name] = {"launches": cnt.value, "ms": round(ms.value, 3)}
         wbytes = 28 * 436.2e6
         print(json.dumps({"prompt_len": P, "middle_layers": 28, "ms": min(ts) * 1e3,
                           "ms_per_token": min(ts) * 1e3 / P,
                           "weight_bytes_per_16_rows_gb": wbytes / 1e9,
-                          "checksum": float(np.abs(out).astype(np.float64).sum())}), flush=True)
+                          "checksum": float(np.abs(out).astype(np.float64).sum()),
+                          "classes": classes}), flush=True)
 
 
 if __name__ == "__main__":
