@@ -11,6 +11,8 @@
 // branch columns sit in the cache (batch invariance, test_metrics.cpp:187).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "sfg_engine.h"
 #include "sfg_expf.h"
 
@@ -26,7 +28,7 @@ __global__ void __launch_bounds__(kThreads) attn_fast_kernel(const float* __rest
                                                              const float* __restrict__ vc,
                                                              const int32_t* __restrict__ row_off,
                                                              const MaskRun* __restrict__ runs, Dims d,
-                                                             float* __restrict__ att, uint32_t* status) {
+                                                             float* __restrict__ att, uint32_t* status, int cap) {
     extern __shared__ float4 smem4[];
     float* smem = reinterpret_cast<float*>(smem4);
     const int group = d.n_heads / d.n_kv;
@@ -34,9 +36,11 @@ __global__ void __launch_bounds__(kThreads) attn_fast_kernel(const float* __rest
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* qs = smem;                                     // [group][HD]
     float* red = qs + kMaxGroup * HD;                     // [kWarps][group][HD]
-    int* cols = reinterpret_cast<int*>(red + kWarps * kMaxGroup * HD);  // [max_len]
-    float* mv = reinterpret_cast<float*>(cols + d.max_len);             // [max_len]
-    float* sc = mv + d.max_len;                                         // [group][max_len]
+    // cap = the launch's bound on a row's visible keys (max_len, or the cache
+    // length after this batch for prompt passes)
+    int* cols = reinterpret_cast<int*>(red + kWarps * kMaxGroup * HD);  // [cap]
+    float* mv = reinterpret_cast<float*>(cols + cap);                   // [cap]
+    float* sc = mv + cap;                                               // [group][cap]
     __shared__ int run_off[65];
     __shared__ int n_s;
     __shared__ float stat[kWarps][kMaxGroup];
@@ -57,6 +61,10 @@ __global__ void __launch_bounds__(kThreads) attn_fast_kernel(const float* __rest
             run_off[64] = off;
         }
         __syncthreads();
+        if (run_off[64] > cap) {  // fail loudly rather than overrun shared memory
+            if (threadIdx.x == 0) atomicOr(status, ST_ATTN_CAP);
+            return;
+        }
         for (int r = 0; r < nr; ++r) {
             const MaskRun rr = runs[base + r];
             for (int j = rr.start + threadIdx.x; j < rr.end; j += kThreads) {
@@ -96,7 +104,7 @@ __global__ void __launch_bounds__(kThreads) attn_fast_kernel(const float* __rest
         for (int g = 0; g < kMaxGroup; ++g) {
             if (g >= group) break;
             const float s = acc[g] * inv_sqrt_hd + mv[c];
-            sc[g * d.max_len + c] = s;
+            sc[g * cap + c] = s;
             mx[g] = fmaxf(mx[g], s);
         }
     }
@@ -127,9 +135,9 @@ __global__ void __launch_bounds__(kThreads) attn_fast_kernel(const float* __rest
 #pragma unroll
         for (int g = 0; g < kMaxGroup; ++g) {
             if (g >= group) break;
-            const float s = sc[g * d.max_len + c];
+            const float s = sc[g * cap + c];
             const float e = s == -INFINITY ? 0.0f : sfg_expf(s - mx_s[g]);
-            sc[g * d.max_len + c] = e;
+            sc[g * cap + c] = e;
             sum[g] += e;
         }
     __syncthreads();
@@ -162,7 +170,7 @@ __global__ void __launch_bounds__(kThreads) attn_fast_kernel(const float* __rest
 #pragma unroll
         for (int g = 0; g < kMaxGroup; ++g) {
             if (g >= group) break;
-            const float p = sc[g * d.max_len + c];
+            const float p = sc[g * cap + c];
 #pragma unroll
             for (int i = 0; i < DPL; ++i) acc[g][i] += p * v[i];
         }
@@ -184,10 +192,10 @@ __global__ void __launch_bounds__(kThreads) attn_fast_kernel(const float* __rest
 
 template <int HD>
 int launch_hd(const float* q, const float* kc, const float* vc, const int32_t* row_off, const MaskRun* runs, int rows,
-              const Dims& d, float* att, uint32_t* status, cudaStream_t s) {
+              const Dims& d, float* att, uint32_t* status, cudaStream_t s, int cap) {
     const size_t smem = sizeof(float) * (kMaxGroup * HD + kWarps * kMaxGroup * HD) +
-                        static_cast<size_t>(d.max_len) * (sizeof(int) + sizeof(float)) +
-                        sizeof(float) * static_cast<size_t>(d.n_heads / d.n_kv) * d.max_len;
+                        static_cast<size_t>(cap) * (sizeof(int) + sizeof(float)) +
+                        sizeof(float) * static_cast<size_t>(d.n_heads / d.n_kv) * cap;
     static size_t configured = 0;
     if (smem > configured) {  // opt in even near 48 KB: static smem counts against the default limit
         if (smem > 220 * 1024) throw Error(Kind::config, "max_seq_len too large for the FAST attention kernel");
@@ -195,20 +203,22 @@ int launch_hd(const float* q, const float* kc, const float* vc, const int32_t* r
                                       static_cast<int>(smem)));
         configured = smem;
     }
-    attn_fast_kernel<HD><<<rows * d.n_kv, kThreads, smem, s>>>(q, kc, vc, row_off, runs, d, att, status);
+    attn_fast_kernel<HD><<<rows * d.n_kv, kThreads, smem, s>>>(q, kc, vc, row_off, runs, d, att, status, cap);
     return 1;
 }
 
 }  // namespace
 
 int launch_attention_fast(const float* q, const float* kcache, const float* vcache, const int32_t* row_off,
-                          const MaskRun* runs, int rows, const Dims& d, float* att, uint32_t* status, cudaStream_t s) {
+                          const MaskRun* runs, int rows, const Dims& d, float* att, uint32_t* status, cudaStream_t s,
+                          int kv_cap) {
+    const int cap = kv_cap > 0 ? std::min(kv_cap, d.max_len) : d.max_len;
     if (d.n_heads / d.n_kv > kMaxGroup) throw Error(Kind::config, "GQA group > 8 not supported by FAST attention");
     switch (d.hd) {
-        case 64: return launch_hd<64>(q, kcache, vcache, row_off, runs, rows, d, att, status, s);
-        case 128: return launch_hd<128>(q, kcache, vcache, row_off, runs, rows, d, att, status, s);
-        case 160: return launch_hd<160>(q, kcache, vcache, row_off, runs, rows, d, att, status, s);
-        case 32: return launch_hd<32>(q, kcache, vcache, row_off, runs, rows, d, att, status, s);
+        case 64: return launch_hd<64>(q, kcache, vcache, row_off, runs, rows, d, att, status, s, cap);
+        case 128: return launch_hd<128>(q, kcache, vcache, row_off, runs, rows, d, att, status, s, cap);
+        case 160: return launch_hd<160>(q, kcache, vcache, row_off, runs, rows, d, att, status, s, cap);
+        case 32: return launch_hd<32>(q, kcache, vcache, row_off, runs, rows, d, att, status, s, cap);
         default:
             return launch_attention_exact(q, kcache, vcache, row_off, runs, rows, 0, d, att, status, s);
     }

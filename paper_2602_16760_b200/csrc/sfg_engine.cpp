@@ -723,6 +723,7 @@ void Engine::forward_host(Bank& b, int lb, int le, int seq, const float* h, cons
     SFG_CUDA(cudaMemcpyAsync(out, ws.h, sizeof(float) * seq * H, cudaMemcpyDeviceToHost, s));
     SFG_CUDA(cudaMemcpyAsync(&st, ws.status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     SFG_CUDA(cudaStreamSynchronize(s));
+    if (st & ST_ATTN_CAP) throw Error(Kind::internal, "attention launch sized below the visible key count");
     if (st & ST_EMPTY_ROW) throw Error(Kind::protocol, "mask row admits no attendable position");
     b.set_len(prior + seq);
 }

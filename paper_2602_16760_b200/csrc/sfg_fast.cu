@@ -840,7 +840,13 @@ int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, i
     {
         const double kvb = 2.0 * 4.0 * d.kvd * (prior + rows);
         ProfScope ps(K_ATTN, s, kvb + 8.0 * R * d.qd, 4.0 * R * d.qd * (prior + rows));
-        n += launch_attention_fast(ws.q, kc, vc, ws.row_off, ws.runs, rows, d, ws.att, ws.status, s);
+        // prompt passes (never graph-captured) size the launch by the cache
+        // length after this batch instead of max_seq_len: more resident CTAs
+        int cap = 0;
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        SFG_CUDA(cudaStreamIsCapturing(s, &cs));
+        if (rows > kRows && cs == cudaStreamCaptureStatusNone) cap = prior + rows;
+        n += launch_attention_fast(ws.q, kc, vc, ws.row_off, ws.runs, rows, d, ws.att, ws.status, s, cap);
     }
     for (int p0 = 0; p0 < rows; p0 += step) {  // O-proj + residual
         const int pr = std::min(step, rows - p0);

@@ -25,6 +25,7 @@ enum WeightType { W_BF16 = 0, W_F32 = 1 };
 enum : uint32_t {
     ST_EMPTY_ROW = 1u,      // mask row admits no attendable position (tinyformer.cpp:467)
     ST_NONFINITE = 2u,      // non-finite hidden state
+    ST_ATTN_CAP = 4u,       // a row saw more keys than the attention launch was sized for
 };
 
 struct LayerPtrs {
@@ -64,7 +65,7 @@ int launch_matvec_store_exact(const float* x, int rows, int K, int wt, const voi
 // ── FAST-mode attention (sfg_attn.cu) ─────────────────────────────────────
 int launch_attention_fast(const float* q, const float* kcache, const float* vcache,
                           const int32_t* row_off, const MaskRun* runs, int rows, const Dims& d,
-                          float* att, uint32_t* status, cudaStream_t s);
+                          float* att, uint32_t* status, cudaStream_t s, int kv_cap = 0);
 
 // ── shared kernels (sfg_common.cu) ────────────────────────────────────────
 int launch_embed(const void* table, int wt, const int32_t* ids, int rows, int H, float* out,

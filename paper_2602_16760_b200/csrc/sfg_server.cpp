@@ -345,6 +345,7 @@ void Server::run(std::vector<StepState*>& group) {
     uint32_t* stw = reinterpret_cast<uint32_t*>(static_cast<char*>(ws.pinned) + ws.pinned_bytes - 64);
     SFG_CUDA(cudaMemcpyAsync(stw, ws.status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     SFG_CUDA(cudaStreamSynchronize(s));
+    if (*stw & ST_ATTN_CAP) throw Error(Kind::internal, "attention launch sized below the visible key count");
     if (*stw & ST_EMPTY_ROW) throw Error(Kind::protocol, "mask row admits no attendable position");
     for (int i = 0; i < k; ++i) {
         StepState& st = *group[i];
