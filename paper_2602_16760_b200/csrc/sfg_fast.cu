@@ -502,9 +502,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 constexpr int kPrepThreads = 256;
 __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const float* __restrict__ x, int ldx, int K,
                                                             const float* __restrict__ gain, float eps,
-                                                            uint8_t* __restrict__ xs) {
-    const int r = blockIdx.x;
-    const float* xr = x + static_cast<size_t>(r) * ldx;
+                                                            uint8_t* __restrict__ xs,
+                                                            uint8_t* __restrict__ xs2 = nullptr,
+                                                            size_t chunk_bytes = 0) {
+    // block b = row b of the pass; rows 16j.. go to chunk j's image (prompt passes)
+    const int b = blockIdx.x, chunk = b / kRows, r = b % kRows;
+    const float* xr = x + static_cast<size_t>(b) * ldx;
+    if (chunk > 0) xs = xs2 + static_cast<size_t>(chunk - 1) * chunk_bytes;
     float scale = 1.0f;
     if (gain) {
         __shared__ float red[kPrepThreads / 32];
@@ -795,12 +799,9 @@ int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, i
     };
     // [RMSNorm] + 3-way split of the pass's rows into the chunk images
     auto prep = [&](const float* x, int ld, int K, const float* gain, float eps, int p0, int pr) {
-        for (int j = 0; j * kRows < pr; ++j) {
-            uint8_t* dst = j == 0 ? f.xs : f.xs2 + static_cast<size_t>(j - 1) * (K / kKB) * kBBytes;
-            prep_kernel<<<std::min(kRows, pr - j * kRows), kPrepThreads, 0, s>>>(
-                x + static_cast<size_t>(p0 + j * kRows) * ld, ld, K, gain, eps, dst);
-            ++n;
-        }
+        prep_kernel<<<pr, kPrepThreads, 0, s>>>(x + static_cast<size_t>(p0) * ld, ld, K, gain, eps, f.xs, f.xs2,
+                                                static_cast<size_t>(K / kKB) * kBBytes);
+        ++n;
     };
     auto gemm = [&](auto epi, const GemmArgs& a) {
         constexpr int EPI = decltype(epi)::value;

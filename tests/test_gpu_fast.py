@@ -36,8 +36,11 @@ def fast_model(request, port):
     return request.param, cfg, m, eng, split
 
 
-@pytest.mark.parametrize("rows", [1, 6, 16, 23])
+@pytest.mark.parametrize("rows", [1, 6, 16, 23, 100, 150])
 def test_fast_forward_within_tolerance(fast_model, rows):
+    """rows > 16 is the prompt path: passes of up to four 16-row chunks per weight
+    stage (100 = 64 + 36 rows, the second pass with an empty fourth chunk;
+    150 = 64 + 64 + 22) and attention sized by the cache length."""
     _, cfg, m, eng, _ = fast_model
     L = cfg.n_layers
     rng = np.random.default_rng(rows)
