@@ -35,10 +35,10 @@ __global__ void __launch_bounds__(kThreads) attn_fast_kernel(const float* __rest
     const int row = blockIdx.x / d.n_kv, kvh = blockIdx.x % d.n_kv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* qs = smem;                                     // [group][HD]
-    float* red = qs + kMaxGroup * HD;                     // [kWarps][group][HD]
+    float* red = qs + group * HD;                         // [kWarps][group][HD]
     // cap = the launch's bound on a row's visible keys (max_len, or the cache
     // length after this batch for prompt passes)
-    int* cols = reinterpret_cast<int*>(red + kWarps * kMaxGroup * HD);  // [cap]
+    int* cols = reinterpret_cast<int*>(red + kWarps * group * HD);      // [cap]
     float* mv = reinterpret_cast<float*>(cols + cap);                   // [cap]
     float* sc = mv + cap;                                               // [group][cap]
     __shared__ int run_off[65];
@@ -179,13 +179,13 @@ __global__ void __launch_bounds__(kThreads) attn_fast_kernel(const float* __rest
     for (int g = 0; g < kMaxGroup; ++g) {
         if (g >= group) break;
 #pragma unroll
-        for (int i = 0; i < DPL; ++i) red[(warp * kMaxGroup + g) * HD + lane + 32 * i] = acc[g][i];
+        for (int i = 0; i < DPL; ++i) red[(warp * group + g) * HD + lane + 32 * i] = acc[g][i];
     }
     __syncthreads();
     for (int t = threadIdx.x; t < group * HD; t += kThreads) {
         const int g = t / HD, dd = t % HD;
         float o = 0.0f;
-        for (int w = 0; w < kWarps; ++w) o += red[(w * kMaxGroup + g) * HD + dd];
+        for (int w = 0; w < kWarps; ++w) o += red[(w * group + g) * HD + dd];
         att[static_cast<size_t>(row) * d.qd + static_cast<size_t>(kvh * group + g) * HD + dd] = o * inv_s[g];
     }
 }
@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(kThreads) attn_fast_kernel(const float* __rest
 template <int HD>
 int launch_hd(const float* q, const float* kc, const float* vc, const int32_t* row_off, const MaskRun* runs, int rows,
               const Dims& d, float* att, uint32_t* status, cudaStream_t s, int cap) {
-    const size_t smem = sizeof(float) * (kMaxGroup * HD + kWarps * kMaxGroup * HD) +
+    const int group = d.n_heads / d.n_kv;  // shared memory sized by the real GQA group
+    const size_t smem = sizeof(float) * (static_cast<size_t>(group) * HD + static_cast<size_t>(kWarps) * group * HD) +
                         static_cast<size_t>(cap) * (sizeof(int) + sizeof(float)) +
                         sizeof(float) * static_cast<size_t>(d.n_heads / d.n_kv) * cap;
     static size_t configured = 0;
