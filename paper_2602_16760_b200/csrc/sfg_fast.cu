@@ -50,7 +50,7 @@ constexpr int kMaxPieces = 16;
 // accumulators of N = 48 in TMEM), so a prompt streams the weights once per
 // NC chunks instead of once per chunk.  Each chunk's MMAs and k order are
 // those of the one-chunk kernel, so results are bitwise the same.
-constexpr int kPromptChunks = 4;
+constexpr int kPromptChunks = 5;
 template <int NC> constexpr int stage_bytes() { return kABytes + NC * kBBytes; }
 template <int NC> constexpr int n_stages() { return NC == 1 ? kStages : (200 * 1024) / stage_bytes<NC>(); }
 template <int NC> constexpr int acc_cols() { return NC == 1 ? kAccCols : 256; }

@@ -38,9 +38,9 @@ def fast_model(request, port):
 
 @pytest.mark.parametrize("rows", [1, 6, 16, 23, 100, 150])
 def test_fast_forward_within_tolerance(fast_model, rows):
-    """rows > 16 is the prompt path: passes of up to four 16-row chunks per weight
-    stage (100 = 64 + 36 rows, the second pass with an empty fourth chunk;
-    150 = 64 + 64 + 22) and attention sized by the cache length."""
+    """rows > 16 is the prompt path: passes of up to five 16-row chunks per weight
+    stage (100 = 80 + 20 rows, the second pass with three empty chunks;
+    150 = 80 + 70, a partial last chunk) and attention sized by the cache length."""
     _, cfg, m, eng, _ = fast_model
     L = cfg.n_layers
     rng = np.random.default_rng(rows)
