@@ -782,8 +782,9 @@ int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, i
     const double R = rows;
     // A pass covers one 16-row chunk, or (prompts: rows > 16) up to
     // kPromptChunks chunks that share every weight stage.  Each projection runs
-    // GEMM-outer over the passes, so from the second pass on its weights
-    // (QKV 50 MB, O 32 MB at 7B) come from L2.  Passes touch disjoint rows.
+    // GEMM-outer over the passes, so its weights (QKV 50 MB, O 32 MB at 7B)
+    // can be re-read from L2 (ncu: little reuse in practice; the L2 is split
+    // over the two dies).  Passes touch disjoint rows.
     const int step = rows > kRows ? kRows * kPromptChunks : kRows;
     auto pass_args = [&](int p0, int pr) {
         GemmArgs a{};
