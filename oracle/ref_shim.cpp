@@ -406,6 +406,9 @@ int ref_verify_greedy(int seq, int vocab, const float* logits, int row_begin, co
 // ── NGramPool (decoding.cpp:61-97) ───────────────────────────────────────
 int ref_pool_new(int n, size_t cap, void** out) { GUARD({ *out = new NGramPool(n, cap); }) }
 void ref_pool_free(void* p) { delete static_cast<NGramPool*>(p); }
+// Copy of a pool (NGramPool is a value type): a junk pool seeded once is
+// handed to several concurrent decodes.
+int ref_pool_clone(void* p, void** out) { GUARD({ *out = new NGramPool(*static_cast<NGramPool*>(p)); }) }
 int ref_pool_update(void* p, const int* prev, const int* cur, int w) {
     GUARD({
         static_cast<NGramPool*>(p)->update(std::span<const int>(prev, w),
@@ -559,6 +562,133 @@ double ref_time_finalize(void* m, int seq, int threads) {
     }
     for (auto& th : ts) th.join();
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+
+// ── 7B-shape golden generation (tests/golden/make_golden_7b.py) ──────────
+// The reference ServerEngine takes its Weights by value and the client keeps a
+// reference, so a full 7B split pipeline would hold 2 x 29 GB fp32.  Here ONE
+// walk of the init_weights stream (tinyformer.cpp:123-152) fills two disjoint
+// Weights objects: the client's (embedding, prefix + suffix layers, final
+// norm, lm_head) and the server's (middle layers only).  Each reference
+// function then touches only the tensors it owns (forward_layers over
+// [begin, end), embed_at, finalize), so results are those of the full model.
+int ref_split_models(const ref_model_cfg* cc, int bf16, int prefix, int suffix, void** client_out,
+                     void** server_out) {
+    GUARD({
+        const ModelConfig c = to_cfg(cc);
+        c.validate();
+        auto cw = std::make_unique<Weights>();
+        auto sw = std::make_unique<Weights>();
+        cw->config = sw->config = c;
+        cw->layers.resize(c.n_layers);
+        sw->layers.resize(c.n_layers);
+        const float a = 1.0f / std::sqrt(static_cast<float>(c.hidden_dim));
+        std::mt19937_64 rng(c.seed);
+        const size_t h = c.hidden_dim, qd = c.q_dim(), kvd = c.kv_dim(), f = c.ffn_dim;
+        fill_or_skip(cw->embedding, c.vocab_size * h, a, rng, true);
+        for (int i = 0; i < c.n_layers; ++i) {
+            const bool local = i < prefix || i >= c.n_layers - suffix;
+            auto& l = local ? cw->layers[i] : sw->layers[i];
+            fill_or_skip(l.attn_norm, h, a, rng, true);
+            fill_or_skip(l.wq, h * qd, a, rng, true);
+            fill_or_skip(l.wk, h * kvd, a, rng, true);
+            fill_or_skip(l.wv, h * kvd, a, rng, true);
+            fill_or_skip(l.wo, qd * h, a, rng, true);
+            fill_or_skip(l.ffn_norm, h, a, rng, true);
+            fill_or_skip(l.w_gate, h * f, a, rng, true);
+            fill_or_skip(l.w_up, h * f, a, rng, true);
+            fill_or_skip(l.w_down, f * h, a, rng, true);
+        }
+        fill_or_skip(cw->final_norm, h, a, rng, true);
+        fill_or_skip(cw->lm_head, h * c.vocab_size, a, rng, true);
+        if (bf16) {
+            round_all(*cw);
+            round_all(*sw);
+        }
+        *client_out = cw.release();
+        *server_out = sw.release();
+    })
+}
+
+// ServerEngine over a Weights object that is MOVED in (server.cpp:27-28);
+// `weights` is consumed (freed) on success.
+int ref_server_new_move(void* weights, int lb, int le, int max_sessions, void** out) {
+    GUARD({
+        ServerConfig sc;
+        sc.layer_begin = lb;
+        sc.layer_end = le;
+        sc.max_sessions = max_sessions;
+        auto* w = static_cast<Weights*>(weights);
+        auto* s = new RefServer;
+        s->engine = std::make_unique<ServerEngine>(std::move(*w), sc);
+        delete w;
+        *out = s;
+    })
+}
+
+// One decode through the reference client + decode loop against a shared
+// reference ServerEngine (thread safe across sessions, server.hpp:53-57).
+// mode 0 = decode_sequential, 2 = decode_lookahead_with_pool(pool) when pool
+// != NULL else decode_lookahead.  The first `rec_frames` exchanges record the
+// boundary rows as the reference saw them: the request rows decoded from the
+// wire (prefix output) and the response rows (middle-layer output), each
+// [rec_frames x max_rows x hidden] fp32, rows per frame in rec_rows.
+int ref_decode_on(void* client_w, void* server, const ref_decode_cfg* dc, void* pool,
+                  const char* session_id, const int* prompt, int n, int max_new, int rec_frames,
+                  int max_rows, float* rec_req, float* rec_resp, int* rec_rows, int* out_tokens,
+                  int* step_batch, int* step_accepted, ref_decode_stats* stats) {
+    GUARD({
+        auto& w = *static_cast<Weights*>(client_w);
+        auto* rs = static_cast<RefServer*>(server);
+        SplitConfig split;
+        split.prefix_layers = dc->prefix_layers;
+        split.suffix_layers = dc->suffix_layers;
+        split.dtype = dc->wire_f32 ? wire::WireDtype::f32 : wire::WireDtype::f16;
+        const int hd = w.config.hidden_dim;
+        int frame_no = 0;
+        FrameHandler fh = [&](const wire::Frame& f) {
+            wire::Frame r = rs->engine->handle(f);
+            if (frame_no < rec_frames && r.header.kind == wire::FrameKind::response) {
+                const int rows = f.header.tensor_shape.empty() ? 0 : f.header.tensor_shape[0];
+                const int take = rows < max_rows ? rows : max_rows;
+                const auto in = wire::decode_values(f.tensor_bytes, f.header.dtype);
+                const auto outv = wire::decode_values(r.tensor_bytes, r.header.dtype);
+                const size_t base = static_cast<size_t>(frame_no) * max_rows * hd;
+                std::memcpy(rec_req + base, in.data(), sizeof(float) * take * hd);
+                std::memcpy(rec_resp + base, outv.data(), sizeof(float) * take * hd);
+                rec_rows[frame_no] = take;
+            }
+            ++frame_no;
+            return r;
+        };
+        LatencyProfile link;
+        auto channel = open_sim_channel(link, fh);
+        SplitClient client(w, split, *channel, session_id ? std::string(session_id) : std::string());
+        LookaheadConfig lc;
+        lc.ngram_n = dc->ngram_n;
+        lc.window_w = dc->window_w;
+        lc.max_candidates_g = dc->max_candidates_g;
+        lc.pool_capacity = static_cast<size_t>(dc->pool_capacity);
+        const std::span<const int> ps(prompt, n);
+        DecodeResult r = dc->mode == 0 ? decode_sequential(client, ps, max_new)
+                         : pool      ? decode_lookahead_with_pool(client, ps, max_new, lc,
+                                                                  *static_cast<NGramPool*>(pool))
+                                     : decode_lookahead(client, ps, max_new, lc);
+        std::memcpy(out_tokens, r.tokens.data(), r.tokens.size() * sizeof(int));
+        for (size_t i = 0; i < r.stats.step_timings.size(); ++i) {
+            if (step_batch) step_batch[i] = r.stats.step_timings[i].batch_len;
+            if (step_accepted) step_accepted[i] = r.stats.step_timings[i].accepted;
+        }
+        if (stats) {
+            stats->steps = r.stats.steps;
+            stats->tokens_committed = r.stats.tokens_committed;
+            stats->wall_seconds = r.stats.wall_seconds;
+            stats->acceptance_rate = r.stats.acceptance_rate;
+            stats->match_rate = r.stats.match_rate;
+            stats->prefill_ms = r.stats.prefill_ms;
+        }
+    })
 }
 
 }  // extern "C"

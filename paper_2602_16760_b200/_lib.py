@@ -13,7 +13,7 @@ import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB_PATH = os.environ.get("SFG_LIB", os.path.join(PKG, "libsfg.so"))  # SFG_LIB: A/B builds (dev tools)
+LIB_PATH = os.path.join(PKG, "libsfg.so")
 HEADER = os.path.join(ROOT, "include", "sfg.h")
 CSRC = os.path.join(PKG, "csrc")
 

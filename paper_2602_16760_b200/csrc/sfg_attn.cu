@@ -197,13 +197,9 @@ int launch_hd(const float* q, const float* kc, const float* vc, const int32_t* r
     const size_t smem = sizeof(float) * (static_cast<size_t>(group) * HD + static_cast<size_t>(kWarps) * group * HD) +
                         static_cast<size_t>(cap) * (sizeof(int) + sizeof(float)) +
                         sizeof(float) * static_cast<size_t>(d.n_heads / d.n_kv) * cap;
-    static size_t configured = 0;
-    if (smem > configured) {  // opt in even near 48 KB: static smem counts against the default limit
-        if (smem > 220 * 1024) throw Error(Kind::config, "max_seq_len too large for the FAST attention kernel");
-        SFG_CUDA(cudaFuncSetAttribute(attn_fast_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-        configured = smem;
-    }
+    // opt in even near 48 KB: static smem counts against the default limit
+    if (smem > 220 * 1024) throw Error(Kind::config, "max_seq_len too large for the FAST attention kernel");
+    ensure_smem_attr(reinterpret_cast<const void*>(attn_fast_kernel<HD>), smem);
     attn_fast_kernel<HD><<<rows * d.n_kv, kThreads, smem, s>>>(q, kc, vc, row_off, runs, d, att, status, cap);
     return 1;
 }

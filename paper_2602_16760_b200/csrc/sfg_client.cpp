@@ -295,13 +295,18 @@ void Client::exchange_frames(bool prompt, int seq, const int32_t* pos, const Mas
     if (send_keep) h.keep = std::vector<int64_t>(keep, keep + n_keep);
     if (crop) h.crop = *crop;
     std::vector<uint16_t> mask;
-    if (runs) {  // encode_values(mask, f16) of the dense {0,-inf} mask
+    if (runs) {  // encode_values(mask, f16) of the dense mask (client.cpp:76-78)
         h.mask_shape = std::vector<int64_t>{1, 1, seq, mask_kv};
-        mask.assign(static_cast<size_t>(seq) * mask_kv, 0xfc00u);
+        mask.assign(static_cast<size_t>(seq) * mask_kv, 0xfc00u);  // -inf
         for (int i = 0; i < seq; ++i)
-            for (int r = runs->row_off[i]; r < runs->row_off[i + 1]; ++r)
+            for (int r = runs->row_off[i]; r < runs->row_off[i + 1]; ++r) {
+                // the visible columns' real additive value: a non-zero one reaches
+                // the server (which rejects it, server.cpp:165-169) as the
+                // reference client would send it
+                const uint16_t v = wire::f32_to_f16_bits(runs->runs[r].mval, nullptr);
                 std::fill(mask.begin() + static_cast<size_t>(i) * mask_kv + runs->runs[r].start,
-                          mask.begin() + static_cast<size_t>(i) * mask_kv + runs->runs[r].end, uint16_t(0));
+                          mask.begin() + static_cast<size_t>(i) * mask_kv + runs->runs[r].end, v);
+            }
     }
     SFG_CUDA(cudaEventRecord(ev_[1], s));
     SFG_CUDA(cudaStreamSynchronize(s));
@@ -407,11 +412,12 @@ int Client::prefill(const int32_t* prompt, int n, float* logits_row) {
     return h_argmax_[0];
 }
 
-Client::Graph* Client::find_graph(int rows, bool logits, bool verify, Bank* server_bank) {
+Client::Graph* Client::find_graph(int rows, bool logits, bool verify, bool additive, const Bank* server_bank) {
     const uint64_t gen = prefix_->ws().generation;
+    const uint64_t bid = server_bank ? server_bank->id() : 0;
     for (auto& g : graphs_)
-        if (g.rows == rows && g.logits == logits && g.verify == verify && g.server_bank == server_bank &&
-            g.generation == gen)
+        if (g.rows == rows && g.logits == logits && g.verify == verify && g.additive == additive &&
+            g.server_bank == bid && g.generation == gen)
             return &g;
     // drop stale entries (workspace reallocated or server session replaced)
     for (auto it = graphs_.begin(); it != graphs_.end();) {
@@ -427,7 +433,8 @@ Client::Graph* Client::find_graph(int rows, bool logits, bool verify, Bank* serv
     g.rows = rows;
     g.logits = logits;
     g.verify = verify;
-    g.server_bank = server_bank;
+    g.additive = additive;
+    g.server_bank = bid;
     g.generation = gen;
     graphs_.push_back(g);
     return &graphs_.back();
@@ -451,12 +458,14 @@ void Client::decode_step(int seq, const int32_t* tokens, const int32_t* position
     const MaskRuns* mr = runs;
     const int committed_before = prefix_->committed_len();
     bool relocate = false;
+    // a keep list longer than the step meta block holds is compacted by
+    // eager kernels ahead of the (graph-captured) step instead
+    const bool big_keep = n_keep > kMetaKeep;
     try {
         if (n_keep > 0 || prefix_->provisional() > 0) {
-            if (n_keep > kMetaKeep) throw Error(Kind::input, "keep list longer than 256 entries");
             prefix_->resolve_meta(keep, n_keep);
             suffix_->resolve_meta(keep, n_keep);
-            relocate = n_keep > 0;
+            relocate = n_keep > 0 && !big_keep;
         }
         if (crop) {
             prefix_->crop(*crop);
@@ -488,6 +497,10 @@ void Client::decode_step(int seq, const int32_t* tokens, const int32_t* position
     ws.meta_pin[1] = committed_before;
     ws.meta_pin[2] = relocate ? n_keep : 0;
     if (relocate) std::memcpy(ws.meta_pin + 3, keep, sizeof(int32_t) * n_keep);
+    if (big_keep) {
+        prefix_->enqueue_compact(keep, n_keep, committed_before, s);
+        suffix_->enqueue_compact(keep, n_keep, committed_before, s);
+    }
     if (vin) std::memcpy(h_vin_, vin, sizeof(VerifyIn));
     const bool send_keep = first_step_done_;
 
@@ -504,15 +517,16 @@ void Client::decode_step(int seq, const int32_t* tokens, const int32_t* position
             throw Error(e.kind(), std::string("server: ") + e.what());
         }
         if (lease.committed_before != committed_before || lease.prior != prefix_->len() ||
-            lease.n_keep != (relocate ? n_keep : lease.n_keep)) {
+            lease.n_keep != (relocate || big_keep ? n_keep : lease.n_keep)) {
             dead_ = true;
             throw Error(Kind::internal, "client and server caches out of lockstep");
         }
+        if (big_keep) lease.bank->enqueue_compact(keep, n_keep, lease.committed_before, s);
         SFG_CUDA(cudaEventRecord(ev_[0], s));
         Graph* gr = nullptr;
         static const bool debug_eager = std::getenv("SFG_DEBUG") != nullptr;
         if (graphs_enabled() && !debug_eager) {
-            gr = find_graph(seq, want_logits, vin != nullptr, lease.bank);
+            gr = find_graph(seq, want_logits, vin != nullptr, ws.additive_mask, lease.bank);
             ++gr->seen;
         }
         if (gr && gr->exec) {

@@ -88,7 +88,10 @@ private:
     struct Graph {
         int rows;
         bool logits, verify;
-        Bank* server_bank;
+        // the mask class fixes the kernel choice baked into the graph
+        // (megakernel vs per-GEMM path, Engine::forward_device)
+        bool additive;
+        uint64_t server_bank;  // Bank::id(), never an address (banks are freed and reallocated)
         uint64_t generation;
         cudaGraphExec_t exec = nullptr;
         std::vector<int> prof_slots;
@@ -104,7 +107,7 @@ private:
     void sleep_one_way() const;
     void stage_inputs(int seq, const int32_t* ids, const int32_t* pos, const MaskRuns& mr);
     void ensure_out(int rows);
-    Graph* find_graph(int rows, bool logits, bool verify, Bank* server_bank);
+    Graph* find_graph(int rows, bool logits, bool verify, bool additive, const Bank* server_bank);
 
     Engine& eng_;
     ClientCfg cfg_;

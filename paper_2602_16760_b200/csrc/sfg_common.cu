@@ -5,9 +5,43 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <map>
+#include <mutex>
+
+#include "sfg_engine.h"
 #include "sfg_kernels.h"
 
 namespace sfg {
+
+namespace {
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void*>, size_t>& attr_sizes() {
+    static std::map<std::pair<int, const void*>, size_t> m;
+    return m;
+}
+}  // namespace
+
+void ensure_smem_attr(const void* fn, size_t smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_attr_mu);
+    size_t& have = attr_sizes()[{dev, fn}];
+    if (smem <= have) return;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) cuda_fail(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)", __FILE__, __LINE__);
+    have = smem;
+}
+
+int device_sm_count() {
+    static int nsm[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!nsm[dev]) cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev);
+    return nsm[dev];
+}
+
 namespace {
 
 // binary16 encode, bit-exact port of wire.cpp:83-135 (RNE, finite overflow
@@ -117,25 +151,40 @@ __global__ void embed_kernel(const void* __restrict__ table, int wt, const int32
 }
 
 // CacheBank::resolve compaction (tinyformer.cpp:291-306), in place on device.
-// One CTA per (layer, kv head, K|V) slab: all kept rows are first gathered
-// into shared memory, then scattered to committed + i — a kept row's
-// destination may be another kept row's source (keep=[1,2]), so a direct
-// per-row copy would race.
+// One CTA per (layer, kv head, K|V) slab.  Kept row i moves from committed +
+// keep[i] to committed + i.  Within a chunk of rows all sources are gathered
+// into shared memory before any destination is written (a kept row's
+// destination may be another kept row's source: keep=[1,2]).  Chunks run in
+// ascending order, which is safe because keep is strictly increasing:
+// keep[j] >= j, so every later source committed + keep[j] (j > i) lies above
+// the destination committed + i — the reference's serial loop relies on the
+// same order.  Any keep length works with kCompactChunk rows of smem.
+constexpr int kCompactChunk = 64;
+
+__device__ __forceinline__ void compact_slab(float* __restrict__ base, int hd, int committed,
+                                             const int32_t* __restrict__ keep, int n_keep, float* buf) {
+    for (int c0 = 0; c0 < n_keep; c0 += kCompactChunk) {
+        const int cn = min(kCompactChunk, n_keep - c0);
+        for (int t = threadIdx.x; t < cn * hd; t += blockDim.x) {
+            const int i = t / hd, dd = t - i * hd;
+            buf[t] = base[(size_t)(committed + keep[c0 + i]) * hd + dd];
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < cn * hd; t += blockDim.x) {
+            const int i = t / hd, dd = t - i * hd;
+            base[(size_t)(committed + c0 + i) * hd + dd] = buf[t];
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void kv_compact_kernel(float* __restrict__ kc, float* __restrict__ vc, int n_kv,
                                   int max_len, int hd, int committed, const int32_t* __restrict__ keep,
                                   int n_keep) {
-    extern __shared__ float buf[];  // [n_keep][hd]
+    extern __shared__ float buf[];  // [min(n_keep, kCompactChunk)][hd]
     const int slab = blockIdx.x;     // (layer * n_kv + head) * 2 + {0:K,1:V}
     float* base = ((slab & 1) ? vc : kc) + (size_t)(slab >> 1) * max_len * hd;
-    for (int t = threadIdx.x; t < n_keep * hd; t += blockDim.x) {
-        const int i = t / hd, dd = t - i * hd;
-        buf[t] = base[(size_t)(committed + keep[i]) * hd + dd];
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < n_keep * hd; t += blockDim.x) {
-        const int i = t / hd, dd = t - i * hd;
-        base[(size_t)(committed + i) * hd + dd] = buf[t];
-    }
+    compact_slab(base, hd, committed, keep, n_keep, buf);
 }
 
 // Same compaction, parameters from the step meta block (meta[1] committed,
@@ -145,18 +194,9 @@ __global__ void kv_compact_meta_kernel(float* __restrict__ kc, float* __restrict
     extern __shared__ float buf[];
     const int committed = meta[1], n_keep = meta[2];
     if (n_keep <= 0) return;
-    const int32_t* keep = meta + 3;
     const int slab = blockIdx.x;
     float* base = ((slab & 1) ? vc : kc) + (size_t)(slab >> 1) * max_len * hd;
-    for (int t = threadIdx.x; t < n_keep * hd; t += blockDim.x) {
-        const int i = t / hd, dd = t - i * hd;
-        buf[t] = base[(size_t)(committed + keep[i]) * hd + dd];
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < n_keep * hd; t += blockDim.x) {
-        const int i = t / hd, dd = t - i * hd;
-        base[(size_t)(committed + i) * hd + dd] = buf[t];
-    }
+    compact_slab(base, hd, committed, meta + 3, n_keep, buf);
 }
 
 // argmax_row (tinyformer.cpp:329-340): first maximum wins == (max value,
@@ -240,7 +280,9 @@ int launch_embed(const void* table, int wt, const int32_t* ids, int rows, int H,
 int launch_kv_compact(float* kcache, float* vcache, int layers, int n_kv, int max_len, int hd,
                       int committed, const int32_t* keep, int n_keep, cudaStream_t s) {
     if (n_keep <= 0 || layers <= 0) return 0;
-    kv_compact_kernel<<<layers * n_kv * 2, 256, sizeof(float) * n_keep * hd, s>>>(
+    const size_t smem = sizeof(float) * (size_t)std::min(n_keep, kCompactChunk) * hd;
+    ensure_smem_attr(reinterpret_cast<const void*>(kv_compact_kernel), smem);
+    kv_compact_kernel<<<layers * n_kv * 2, 256, smem, s>>>(
         kcache, vcache, n_kv, max_len, hd, committed, keep, n_keep);
     return 1;
 }
@@ -248,12 +290,8 @@ int launch_kv_compact(float* kcache, float* vcache, int layers, int n_kv, int ma
 int launch_kv_compact_meta(float* kcache, float* vcache, int layers, int n_kv, int max_len, int hd,
                            const int32_t* meta, int max_keep, cudaStream_t s) {
     if (layers <= 0) return 0;
-    const size_t smem = sizeof(float) * (size_t)max_keep * hd;
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaFuncSetAttribute(kv_compact_meta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
-    }
+    const size_t smem = sizeof(float) * (size_t)std::min(max_keep, kCompactChunk) * hd;
+    ensure_smem_attr(reinterpret_cast<const void*>(kv_compact_meta_kernel), smem);
     kv_compact_meta_kernel<<<layers * n_kv * 2, 256, smem, s>>>(kcache, vcache, max_len, hd, meta);
     return 1;
 }

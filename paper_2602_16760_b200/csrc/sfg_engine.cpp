@@ -4,6 +4,7 @@
 
 #include "sfg_prof.h"
 
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <cstdlib>
@@ -217,7 +218,9 @@ void Engine::set_prior(Workspace& ws, int prior, cudaStream_t s) {
 }
 
 // ── banks ─────────────────────────────────────────────────────────────────
-Bank::Bank(Engine& eng, int lb, int le) : eng_(eng), lb_(lb), le_(le) {
+static std::atomic<uint64_t> g_bank_ids{1};
+
+Bank::Bank(Engine& eng, int lb, int le) : eng_(eng), lb_(lb), le_(le), id_(g_bank_ids.fetch_add(1)) {
     const ModelCfg& c = eng.cfg();
     if (lb < 0 || le > c.n_layers || lb > le) throw Error(Kind::config, "invalid layer range for cache bank");
     DeviceGuard g(eng.device());
@@ -263,20 +266,34 @@ void Bank::resolve(const int32_t* keep, int n, cudaStream_t s) {
         DeviceGuard g(eng_.device());
         const bool own = s == nullptr;
         cudaStream_t st = own ? stream_ : s;
-        eng_.ensure_ws(ws_, std::max(n, 1), 1, 0);
-        if (!keep_pin_) SFG_CUDA(cudaMallocHost(&keep_pin_, sizeof(int32_t) * 1024));
-        if (n > 1024) throw Error(Kind::protocol, "keep list too long");
-        // the previous resolve's copy has completed: every step ends in a sync
-        std::memcpy(keep_pin_, keep, sizeof(int32_t) * n);
-        SFG_CUDA(cudaMemcpyAsync(ws_.keep, keep_pin_, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
-        const ModelCfg& c = eng_.cfg();
-        launch_kv_compact(k_, v_, le_ - lb_, c.n_kv_heads, c.max_seq_len, c.head_dim, committed_, ws_.keep,
-                          n, st);
-        SFG_CUDA(cudaGetLastError());
+        enqueue_compact(keep, n, committed_, st);
         if (own) SFG_CUDA(cudaStreamSynchronize(st));
     }
     committed_ += n;
     len_ = committed_;
+}
+
+// The device half of resolve: kept tail entries committed + keep[i] move to
+// committed + i on stream st (any keep length: sfg_common.cu compacts in
+// chunks).  The keep list crosses through this bank's pinned buffer; the
+// previous resolve's copy has completed (every step ends in a sync).
+void Bank::enqueue_compact(const int32_t* keep, int n, int committed, cudaStream_t st) {
+    if (n <= 0 || le_ == lb_) return;
+    DeviceGuard g(eng_.device());
+    eng_.ensure_ws(ws_, std::max(n, 1), 1, 0);
+    if (n > keep_pin_cap_) {
+        if (keep_pin_) {
+            SFG_CUDA(cudaDeviceSynchronize());
+            cudaFreeHost(keep_pin_);
+        }
+        keep_pin_cap_ = std::max(n, 1024);
+        SFG_CUDA(cudaMallocHost(&keep_pin_, sizeof(int32_t) * keep_pin_cap_));
+    }
+    std::memcpy(keep_pin_, keep, sizeof(int32_t) * n);
+    SFG_CUDA(cudaMemcpyAsync(ws_.keep, keep_pin_, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    const ModelCfg& c = eng_.cfg();
+    launch_kv_compact(k_, v_, le_ - lb_, c.n_kv_heads, c.max_seq_len, c.head_dim, committed, ws_.keep, n, st);
+    SFG_CUDA(cudaGetLastError());
 }
 
 void Bank::resolve_meta(const int32_t* keep, int n) {

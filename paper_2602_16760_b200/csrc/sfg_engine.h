@@ -146,6 +146,8 @@ public:
     // resolve() bookkeeping only (validation + committed/len); the caller
     // enqueues the meta-driven compaction itself (graph-captured steps).
     void resolve_meta(const int32_t* keep, int n);
+    // device compaction of kept tail entries (the device half of resolve)
+    void enqueue_compact(const int32_t* keep, int n, int committed, cudaStream_t st);
     void crop(int pos);                        // tinyformer.cpp:310-316
     float* kslab(int layer) const;
     size_t slab_elems() const { return slab_elems_; }
@@ -156,16 +158,21 @@ public:
     Engine& engine() { return eng_; }
     // per-bank state of the FAST megakernel (layer table, grid barrier)
     std::shared_ptr<void> mega;
+    // process-unique id (never reused, unlike the object's address): keys
+    // the client's captured graphs that bake in this bank's device buffers
+    uint64_t id() const { return id_; }
 
 private:
     Engine& eng_;
     int lb_, le_;
+    uint64_t id_;
     int len_ = 0, committed_ = 0;
     float* k_ = nullptr;
     float* v_ = nullptr;
     size_t slab_elems_ = 0;
     cudaStream_t stream_ = nullptr;
     int32_t* keep_pin_ = nullptr;
+    int keep_pin_cap_ = 0;
     Workspace ws_;
 };
 

@@ -374,12 +374,7 @@ int launch_attention_exact(const float* q, const float* kcache, const float* vca
                            const Dims& d, float* att, uint32_t* status, cudaStream_t s) {
     (void)kv_len;
     const size_t smem = sizeof(float) * (size_t)d.hd + (size_t)d.max_len * (4 * sizeof(float));
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(attention_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-        configured = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(attention_exact_kernel), 200 * 1024);
     attention_exact_kernel<<<rows * d.n_heads, kAttnThreads, smem, s>>>(q, kcache, vcache, row_off,
                                                                         runs, d, att, status);
     return 1;

@@ -632,24 +632,11 @@ constexpr size_t smem_bytes() {
 
 template <int EPI, int NC = 1>
 void launch_gemm(const GemmArgs& a, int grid, cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        SFG_CUDA(cudaFuncSetAttribute(gemm_kernel<EPI, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem_bytes<NC>())));
-        configured = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(gemm_kernel<EPI, NC>), smem_bytes<NC>());
     gemm_kernel<EPI, NC><<<grid, kThreads, smem_bytes<NC>(), s>>>(a);
 }
 
-int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return n;
-}
+int num_sms() { return device_sm_count(); }
 
 int tiles_for(int n) { return (n + kM - 1) / kM; }
 

@@ -21,6 +21,13 @@ struct MaskRun {
 
 enum WeightType { W_BF16 = 0, W_F32 = 1 };
 
+// Opt `fn` in to `smem` bytes of dynamic shared memory on the CURRENT device
+// (function attributes are per device: one process may drive several GPUs).
+// Remembers the largest size configured per (device, function); thread safe.
+void ensure_smem_attr(const void* fn, size_t smem);
+// SM count of the current device (cached per device).
+int device_sm_count();
+
 // status word bits written by kernels (checked by the host after the step)
 enum : uint32_t {
     ST_EMPTY_ROW = 1u,      // mask row admits no attendable position (tinyformer.cpp:467)

@@ -1703,12 +1703,7 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         b.mega = holder;
         stp = holder.get();
     }
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int nsm = device_sm_count();
     const int group = c.n_heads / c.n_kv_heads;
     static const int stages_cap = [] {
         const char* v = getenv("SFG_MEGA_STAGES");  // dev knob: ring depth sensitivity
@@ -1719,10 +1714,8 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     const void* kfn = ra ? reinterpret_cast<const void*>(mega_kernel<true>) : reinterpret_cast<const void*>(mega_kernel<false>);
     while (stages > 4 && smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len) > dyn_smem_budget(ra)) --stages;
     const size_t smem = smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len);
-    static size_t configured[2] = {0, 0};
-    if (smem > configured[ra]) {
-        SFG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured[ra] = smem;
+    {
+        ensure_smem_attr(kfn, smem);
         int nb = 0;
         SFG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kfn, kThreads, smem));
         if (nb < 1) {

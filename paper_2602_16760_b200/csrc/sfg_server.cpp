@@ -226,7 +226,10 @@ void upload_meta(Engine& e, Workspace& ws, const std::vector<int32_t>& pos, cons
 
 // handle_prompt / handle_step (server.cpp:203-265), host part: session state
 // machine, validation, keep/crop, mask -> runs.  Leaves the session locked.
-void Server::prepare(const wire::FrameView& f, StepState& st) {
+// With try_lock, a session whose mutex is held elsewhere is not waited for:
+// returns false before touching any state (handle_batch already holds other
+// sessions' locks, and waiting there could deadlock against another batch).
+bool Server::prepare(const wire::FrameView& f, StepState& st, bool try_lock) {
     const ModelCfg& c = eng_.cfg();
     const auto kind = f.h.kind;
     if (kind == wire::FrameKind::response || kind == wire::FrameKind::error)
@@ -242,7 +245,12 @@ void Server::prepare(const wire::FrameView& f, StepState& st) {
         st.sess = find_session(f.h.session_id);
         if (!st.sess) throw Error(Kind::session, "unknown or expired session: " + f.h.session_id);
     }
-    st.lock = std::unique_lock<std::mutex>(st.sess->mutex);
+    if (try_lock) {
+        st.lock = std::unique_lock<std::mutex>(st.sess->mutex, std::try_to_lock);
+        if (!st.lock.owns_lock()) return false;
+    } else {
+        st.lock = std::unique_lock<std::mutex>(st.sess->mutex);
+    }
     Bank& bank = *st.sess->bank;
     if (st.prompt) {
         bank.reset();
@@ -268,6 +276,7 @@ void Server::prepare(const wire::FrameView& f, StepState& st) {
     forward_checks(bank, st.hc.seq, st.mr, c.max_seq_len);
     st.out_dt = cfg_.response_dtype < 0 ? f.h.dtype
                                         : (cfg_.response_dtype == SFG_WIRE_F32 ? wire::Dtype::f32 : wire::Dtype::f16);
+    return true;
 }
 
 // Device part for one step or for several sessions' steps in ONE weight
@@ -430,7 +439,11 @@ void Server::handle_batch(int n, const uint8_t* const* reqs, const size_t* lens,
         auto st = std::make_unique<StepState>();
         st->resp = &resps[i];
         try {
-            prepare(f, *st);
+            // never block on a session lock while the group holds others
+            if (!prepare(f, *st, !group.empty())) {
+                flush();
+                prepare(f, *st, false);
+            }
         } catch (const Error& e) {
             error_frame(f.h.session_id, e.what(), resps[i]);
             continue;

@@ -94,7 +94,7 @@ private:
         wire::Dtype out_dt = wire::Dtype::f16;
         std::vector<uint8_t>* resp = nullptr;
     };
-    void prepare(const wire::FrameView& f, StepState& st);
+    bool prepare(const wire::FrameView& f, StepState& st, bool try_lock = false);
     void run(std::vector<StepState*>& group);
     static int tc_rows() { return 16; }
     std::atomic<uint64_t> shared_passes_{0};
