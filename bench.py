@@ -62,10 +62,15 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi sampling (B200_PROFILING.md clocks line) over the whole
+    measured run: the value and e2e legs, the sweeps and the profiler passes
+    (the timed value leg alone is ~100 ms, shorter than one sample)."""
 
     def __init__(self, dev):
-        self.dev, self.samples, self.proc = dev, [], None
+        self.dev, self.samples, self.proc, self.marks = dev, [], None, {}
+
+    def mark(self, name):
+        self.marks[name] = len(self.samples)
 
     def __enter__(self):
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -73,7 +78,7 @@ class Clocks:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -98,9 +103,12 @@ class Clocks:
         mx = [float(s[1]) for s in self.samples if len(s) >= 7 and s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples if len(s) >= 7 for i in range(4) if s[3 + i] == "Active"})
+        pw = [float(s[2]) for s in self.samples if len(s) >= 7 and s[2].replace(".", "").isdigit()]
         sm.sort()
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_median": sorted(pw)[len(pw) // 2] if pw else None,
+                "window": "whole measured run (100 ms sampling)"}
 
 
 _GROUP = None
@@ -265,8 +273,12 @@ def run_ours(args, ws, rank, local):
     t_init = time.time() - t0
     nl = cfg.n_layers
     srv = sfg.ServerEngine(eng, sfg.ServerConfig(SPLIT, nl - SPLIT, max_sessions=64))
-    rng = np.random.default_rng(101 + rank)
+    # every rank decodes the SAME prompt from the same seeded pool: identical
+    # per-rank work and acceptance, so N ranks do exactly N x one rank's tokens
+    rng = np.random.default_rng(101)
     prompt = rng.integers(0, cfg.vocab_size, PROMPT_LEN).tolist()
+    # clocks are sampled over the whole measured part of the run (all legs)
+    clk = Clocks(local).__enter__()
     la = _lib.DecodeConfig(2, W, NG, G, 1 << 20)
     total_steps = args.warmup + args.steps
     pools = []
@@ -302,17 +314,18 @@ def run_ours(args, ws, rank, local):
     L.sfg_profiler_reset()
     L.sfg_profiler_enable(1)
     barrier(ws, local)
-    with Clocks(local) as clk:
-        tw = time.perf_counter()
-        for _ in range(args.steps):
-            n, b = step(dec)
-            L.sfg_client_last_profile(client.h, C.byref(prof))
-            dev_ms.append(prof.step_ms)
-            srv_ms.append(prof.server_ms)
-            launches.append(prof.launches)
-            batches.append(b)
-            toks += n
-        wall = time.perf_counter() - tw
+    clk.mark("timed")
+    tw = time.perf_counter()
+    for _ in range(args.steps):
+        n, b = step(dec)
+        L.sfg_client_last_profile(client.h, C.byref(prof))
+        dev_ms.append(prof.step_ms)
+        srv_ms.append(prof.server_ms)
+        launches.append(prof.launches)
+        batches.append(b)
+        toks += n
+    wall = time.perf_counter() - tw
+    clk.mark("timed_end")
     L.sfg_profiler_enable(0)
     barrier(ws, local)
     dev_total = sum(dev_ms) / 1000.0
@@ -333,6 +346,8 @@ def run_ours(args, ws, rank, local):
     for _ in range(args.warmup):
         step(fdec)
     barrier(ws, local)
+    cb0 = (C.c_uint64(), C.c_uint64())
+    L.sfg_copy_bytes(C.byref(cb0[0]), C.byref(cb0[1]))
     te = time.perf_counter()
     etoks, ebatch = 0, []
     for _ in range(args.steps):
@@ -340,6 +355,11 @@ def run_ours(args, ws, rank, local):
         etoks += n
         ebatch.append(b)
     e_wall = time.perf_counter() - te
+    cb1 = (C.c_uint64(), C.c_uint64())
+    L.sfg_copy_bytes(C.byref(cb1[0]), C.byref(cb1[1]))
+    # measured: every host<->device copy the client and server made in the timed steps
+    h2d = (cb1[0].value - cb0[0].value) / args.steps
+    d2h = (cb1[1].value - cb0[1].value) / args.steps
     e_wall_max = barrier_max(ws, local, e_wall)
     etoks_all = dist_sum(ws, local, float(etoks)) / max(1, args.tp)
     L.sfg_decoder_destroy(fdec)
@@ -413,6 +433,7 @@ def run_ours(args, ws, rank, local):
                                   "device_ms_per_step": sum(ms) / len(ms)}
             L.sfg_decoder_destroy(d)
 
+    clk.__exit__(None, None, None)
     if rank != 0:
         return
     hbm, tflops, peak_kind = peaks()
@@ -421,11 +442,6 @@ def run_ours(args, ws, rank, local):
     cnt, ms, by, fl = stats[dom]
     avg_ms = ms / max(cnt, 1)
     achieved = (by / max(cnt, 1)) / (avg_ms / 1000.0) / 1e9 if cnt else 0.0
-    B = batches[-1]
-    H = cfg.hidden_dim
-    mask_kv = PROMPT_LEN + 16 * 8  # order of magnitude; mask is host-side only
-    h2d = 2 * B * H * 2 + 4 * B * 2 + 4700 + 16 * B
-    d2h = 2 * B * H * 2 + 4700
     step_ms = dev_total_max / args.steps * 1000.0
     # whole-step algorithmic bytes (all kernel classes) -> step-level fraction
     step_bytes = sum(v[2] for v in stats.values()) / args.steps
@@ -438,7 +454,8 @@ def run_ours(args, ws, rank, local):
         "config": config_dict(args, ws),
         "e2e": {"value": etoks_all / e_wall_max, "unit": "tok/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e_wall_max / args.steps * 1000.0,
-                "path": "frames through sfg_server_handle (C ABI), host buffers"},
+                "path": "frames through sfg_server_handle (C ABI), host buffers",
+                "bytes": "measured: sum of the library's host<->device copies over the timed steps / steps"},
         "gpu_launches": int(sum(launches)),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "peak_kind": peak_kind, **ncu_traffic(args),

@@ -266,6 +266,9 @@ typedef struct {
     int32_t batch;             /* rows of the last step */
 } sfg_step_profile;
 int32_t sfg_client_last_profile(sfg_client* c, sfg_step_profile* out);
+/* Cumulative host->device / device->host bytes moved by the library's own
+ * copies since process start (bench.py measures e2e bytes per step).      */
+void sfg_copy_bytes(uint64_t* h2d, uint64_t* d2h);
 /* Capture / replay the device part of steps as CUDA graphs (default on). */
 void sfg_set_graphs(int32_t enabled);
 /* Per-kernel-class CUDA-event timing on the launching stream (bench.py's

@@ -148,6 +148,7 @@ def lib() -> C.CDLL:
         "sfg_selftest_wire_roundtrip": (i32, [f32p, f32p, i32, C.POINTER(C.c_uint64)]),
         "sfg_client_last_profile": (i32, [vp, C.POINTER(StepProfile)]),
         "sfg_set_graphs": (None, [i32]),
+        "sfg_copy_bytes": (None, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "sfg_profiler_enable": (None, [i32]),
         "sfg_debug_set_mega": (None, [i32]),
         "sfg_debug_mega_trace": (None, [i32]),

@@ -327,6 +327,11 @@ int32_t sfg_client_last_profile(sfg_client* c, sfg_step_profile* out) {
 
 void sfg_set_graphs(int32_t enabled) { graphs_enabled() = enabled != 0; }
 
+void sfg_copy_bytes(uint64_t* h2d, uint64_t* d2h) {
+    if (h2d) *h2d = copy_counters().h2d.load();
+    if (d2h) *d2h = copy_counters().d2h.load();
+}
+
 void sfg_debug_set_mega(int32_t on) { mega_mode() = on ? 1 : 0; }
 void sfg_debug_mega_trace(int32_t on) { mega_trace_enabled() = on != 0; }
 int32_t sfg_debug_mega_trace_read(sfg_bank* b, uint64_t* out, size_t n) {

@@ -220,12 +220,12 @@ int Client::dev_pre(int rows, Bank* server_bank, bool verify, cudaStream_t s) {
     const StageLayout L = stage_layout(ws.cap_rows, ws.cap_runs);
     const char* p = static_cast<const char*>(ws.stage_pin);
     int n = 0;
-    SFG_CUDA(cudaMemcpyAsync(ws.meta, ws.meta_pin, sizeof(int32_t) * (4 + kMetaKeep), cudaMemcpyHostToDevice, s));
-    SFG_CUDA(cudaMemcpyAsync(ws.ids, p + L.ids, sizeof(int32_t) * ws.cap_rows, cudaMemcpyHostToDevice, s));
-    SFG_CUDA(cudaMemcpyAsync(ws.pos, p + L.pos, sizeof(int32_t) * ws.cap_rows, cudaMemcpyHostToDevice, s));
-    SFG_CUDA(cudaMemcpyAsync(ws.row_off, p + L.roff, sizeof(int32_t) * (ws.cap_rows + 1), cudaMemcpyHostToDevice, s));
-    SFG_CUDA(cudaMemcpyAsync(ws.runs, p + L.runs, sizeof(MaskRun) * ws.cap_runs, cudaMemcpyHostToDevice, s));
-    if (verify) SFG_CUDA(cudaMemcpyAsync(d_vin_, h_vin_, sizeof(VerifyIn), cudaMemcpyHostToDevice, s));
+    SFG_CUDA(copy_async(ws.meta, ws.meta_pin, sizeof(int32_t) * (4 + kMetaKeep), cudaMemcpyHostToDevice, s));
+    SFG_CUDA(copy_async(ws.ids, p + L.ids, sizeof(int32_t) * ws.cap_rows, cudaMemcpyHostToDevice, s));
+    SFG_CUDA(copy_async(ws.pos, p + L.pos, sizeof(int32_t) * ws.cap_rows, cudaMemcpyHostToDevice, s));
+    SFG_CUDA(copy_async(ws.row_off, p + L.roff, sizeof(int32_t) * (ws.cap_rows + 1), cudaMemcpyHostToDevice, s));
+    SFG_CUDA(copy_async(ws.runs, p + L.runs, sizeof(MaskRun) * ws.cap_runs, cudaMemcpyHostToDevice, s));
+    if (verify) SFG_CUDA(copy_async(d_vin_, h_vin_, sizeof(VerifyIn), cudaMemcpyHostToDevice, s));
     SFG_CUDA(cudaMemsetAsync(ws.status, 0, sizeof(uint32_t), s));
     const int mk = std::min(kMetaKeep, ws.cap_rows);
     for (Bank* b : {prefix_.get(), suffix_.get(), server_bank}) {
@@ -247,10 +247,12 @@ int Client::dev_server(int rows, Bank* server_bank, cudaStream_t s) {
     const int f32 = cfg_.wire_dtype == SFG_WIRE_F32;
     int k = launch_wire_roundtrip(ws.h, f32, n, ws.clamped, s);  // encode/decode_values
     k += launch_link_delay(cfg_.one_way_delay_ms, s);             // request leg
-    SFG_CUDA(cudaEventRecord(ev_[1], s));
+    // External records: under stream capture they become event-record nodes of
+    // the step's graph, so the server segment is timed on every replay too
+    SFG_CUDA(cudaEventRecordWithFlags(ev_[1], s, cudaEventRecordExternal));
     k += linked_->engine().forward_device(*server_bank, linked_->config().layer_begin, linked_->config().layer_end,
                                           rows, ws, s);
-    SFG_CUDA(cudaEventRecord(ev_[2], s));
+    SFG_CUDA(cudaEventRecordWithFlags(ev_[2], s, cudaEventRecordExternal));
     const int rd = linked_->config().response_dtype;
     k += launch_wire_roundtrip(ws.h, rd < 0 ? f32 : rd == SFG_WIRE_F32, n, nullptr, s);
     k += launch_link_delay(cfg_.one_way_delay_ms, s);             // response leg
@@ -265,11 +267,11 @@ int Client::dev_post(int rows, bool want_logits, bool verify, cudaStream_t s) {
     n += eng_.head_device(rows, ws, want_logits, true, s);
     if (verify) {
         n += launch_verify(ws.argmax, d_vin_, d_vout_, s);
-        SFG_CUDA(cudaMemcpyAsync(h_vout_, d_vout_, sizeof(VerifyOut), cudaMemcpyDeviceToHost, s));
+        SFG_CUDA(copy_async(h_vout_, d_vout_, sizeof(VerifyOut), cudaMemcpyDeviceToHost, s));
     }
-    SFG_CUDA(cudaMemcpyAsync(h_argmax_, ws.argmax, sizeof(int32_t) * rows, cudaMemcpyDeviceToHost, s));
+    SFG_CUDA(copy_async(h_argmax_, ws.argmax, sizeof(int32_t) * rows, cudaMemcpyDeviceToHost, s));
     if (want_logits)
-        SFG_CUDA(cudaMemcpyAsync(h_logits_, ws.logits, sizeof(float) * rows * c.vocab_size, cudaMemcpyDeviceToHost, s));
+        SFG_CUDA(copy_async(h_logits_, ws.logits, sizeof(float) * rows * c.vocab_size, cudaMemcpyDeviceToHost, s));
     return n;
 }
 
@@ -285,7 +287,7 @@ void Client::exchange_frames(bool prompt, int seq, const int32_t* pos, const Mas
     prof_.launches += launch_pack_rows(ws.h, f32, n, ws.wire, ws.clamped, s);
     // the wire rows cross through pinned staging (async DMA, no driver bounce)
     uint8_t* pin = static_cast<uint8_t*>(ws.wire_pin);
-    SFG_CUDA(cudaMemcpyAsync(pin, ws.wire, wbytes, cudaMemcpyDeviceToHost, s));
+    SFG_CUDA(copy_async(pin, ws.wire, wbytes, cudaMemcpyDeviceToHost, s));
     wire::Header h;  // make_request (client.cpp:59-81)
     h.kind = prompt ? wire::FrameKind::prompt : (send_keep ? wire::FrameKind::accept_and_step : wire::FrameKind::step);
     h.session_id = sid_;
@@ -346,7 +348,7 @@ void Client::exchange_frames(bool prompt, int seq, const int32_t* pos, const Mas
         throw Error(Kind::protocol, "response tensor exceeds the workspace");
     }
     std::memcpy(pin, r.tensor, r.tensor_len);
-    SFG_CUDA(cudaMemcpyAsync(ws.wire, pin, r.tensor_len, cudaMemcpyHostToDevice, s));
+    SFG_CUDA(copy_async(ws.wire, pin, r.tensor_len, cudaMemcpyHostToDevice, s));
     prof_.launches += launch_unpack_rows(ws.wire, r.h.dtype == wire::Dtype::f32, n, ws.h, s);
     SFG_CUDA(cudaEventRecord(ev_[2], s));
     SFG_CUDA(cudaStreamSynchronize(s));  // the staging buffer is reused next step
@@ -398,12 +400,12 @@ int Client::prefill(const int32_t* prompt, int n, float* logits_row) {
     suffix_->mark_committed(n);
     // finalize + argmax of the last row only (rows are independent)
     if (n > 1)
-        SFG_CUDA(cudaMemcpyAsync(ws.h, ws.h + static_cast<size_t>(n - 1) * c.hidden_dim,
+        SFG_CUDA(copy_async(ws.h, ws.h + static_cast<size_t>(n - 1) * c.hidden_dim,
                                  sizeof(float) * c.hidden_dim, cudaMemcpyDeviceToDevice, s));
     prof_.launches += eng_.head_device(1, ws, logits_row != nullptr, true, s);
-    SFG_CUDA(cudaMemcpyAsync(h_argmax_, ws.argmax, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SFG_CUDA(copy_async(h_argmax_, ws.argmax, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     if (logits_row)
-        SFG_CUDA(cudaMemcpyAsync(h_logits_, ws.logits, sizeof(float) * c.vocab_size, cudaMemcpyDeviceToHost, s));
+        SFG_CUDA(copy_async(h_logits_, ws.logits, sizeof(float) * c.vocab_size, cudaMemcpyDeviceToHost, s));
     SFG_CUDA(cudaStreamSynchronize(s));
     SFG_CUDA(cudaGetLastError());
     if (logits_row) std::memcpy(logits_row, h_logits_, sizeof(float) * c.vocab_size);
@@ -596,7 +598,7 @@ void Client::decode_step(int seq, const int32_t* tokens, const int32_t* position
     if (logits_out) std::memcpy(logits_out, h_logits_, sizeof(float) * seq * c.vocab_size);
     float a = 0, b = 0;
     cudaEventElapsedTime(&a, ev_[0], ev_[3]);
-    if (linked_ && !prof_.graph) cudaEventElapsedTime(&b, ev_[1], ev_[2]);
+    if (linked_) SFG_CUDA(cudaEventElapsedTime(&b, ev_[1], ev_[2]));
     prof_.step_ms = a;
     if (linked_) prof_.server_ms = b;
     prof_.local_ms = a - b;

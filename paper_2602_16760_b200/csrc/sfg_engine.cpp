@@ -220,6 +220,11 @@ void Engine::set_prior(Workspace& ws, int prior, cudaStream_t s) {
 // ── banks ─────────────────────────────────────────────────────────────────
 static std::atomic<uint64_t> g_bank_ids{1};
 
+CopyCounters& copy_counters() {
+    static CopyCounters c;
+    return c;
+}
+
 Bank::Bank(Engine& eng, int lb, int le) : eng_(eng), lb_(lb), le_(le), id_(g_bank_ids.fetch_add(1)) {
     const ModelCfg& c = eng.cfg();
     if (lb < 0 || le > c.n_layers || lb > le) throw Error(Kind::config, "invalid layer range for cache bank");

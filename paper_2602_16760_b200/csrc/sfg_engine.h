@@ -6,6 +6,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <memory>
 #include <mutex>
@@ -303,6 +304,19 @@ bool& graphs_enabled();
 // 1: FAST forward uses the layer-stack megakernel when it applies (default;
 // env SFG_MEGA=0 or sfg_debug_set_mega(0) selects the per-GEMM kernels).
 int& mega_mode();
+
+// Host<->device bytes moved by the engine's copies (bench.py's e2e
+// h2d/d2h_bytes_per_step are measured from these, sfg_copy_bytes).
+struct CopyCounters {
+    std::atomic<uint64_t> h2d{0}, d2h{0};
+};
+CopyCounters& copy_counters();
+// cudaMemcpyAsync that also counts host<->device bytes
+inline cudaError_t copy_async(void* dst, const void* src, size_t n, cudaMemcpyKind k, cudaStream_t s) {
+    if (k == cudaMemcpyHostToDevice) copy_counters().h2d.fetch_add(n, std::memory_order_relaxed);
+    if (k == cudaMemcpyDeviceToHost) copy_counters().d2h.fetch_add(n, std::memory_order_relaxed);
+    return cudaMemcpyAsync(dst, src, n, k, s);
+}
 
 // Scoped device selection.
 struct DeviceGuard {

@@ -208,18 +208,18 @@ void upload_meta(Engine& e, Workspace& ws, const std::vector<int32_t>& pos, cons
     const size_t pb = sizeof(int32_t) * pos.size(), rb = sizeof(int32_t) * mr.row_off.size(),
                  ub = sizeof(MaskRun) * mr.runs.size();
     if (pb + rb + ub > ws.pinned_bytes) {
-        SFG_CUDA(cudaMemcpyAsync(ws.pos, pos.data(), pb, cudaMemcpyHostToDevice, s));
-        SFG_CUDA(cudaMemcpyAsync(ws.row_off, mr.row_off.data(), rb, cudaMemcpyHostToDevice, s));
-        SFG_CUDA(cudaMemcpyAsync(ws.runs, mr.runs.data(), ub, cudaMemcpyHostToDevice, s));
+        SFG_CUDA(copy_async(ws.pos, pos.data(), pb, cudaMemcpyHostToDevice, s));
+        SFG_CUDA(copy_async(ws.row_off, mr.row_off.data(), rb, cudaMemcpyHostToDevice, s));
+        SFG_CUDA(copy_async(ws.runs, mr.runs.data(), ub, cudaMemcpyHostToDevice, s));
         SFG_CUDA(cudaStreamSynchronize(s));
         return;
     }
     std::memcpy(pin, pos.data(), pb);
     std::memcpy(pin + pb, mr.row_off.data(), rb);
     std::memcpy(pin + pb + rb, mr.runs.data(), ub);
-    SFG_CUDA(cudaMemcpyAsync(ws.pos, pin, pb, cudaMemcpyHostToDevice, s));
-    SFG_CUDA(cudaMemcpyAsync(ws.row_off, pin + pb, rb, cudaMemcpyHostToDevice, s));
-    SFG_CUDA(cudaMemcpyAsync(ws.runs, pin + pb + rb, ub, cudaMemcpyHostToDevice, s));
+    SFG_CUDA(copy_async(ws.pos, pin, pb, cudaMemcpyHostToDevice, s));
+    SFG_CUDA(copy_async(ws.row_off, pin + pb, rb, cudaMemcpyHostToDevice, s));
+    SFG_CUDA(copy_async(ws.runs, pin + pb + rb, ub, cudaMemcpyHostToDevice, s));
 }
 
 }  // namespace
@@ -316,7 +316,7 @@ void Server::run(std::vector<StepState*>& group) {
         const size_t off = static_cast<size_t>(row0[i]) * c.hidden_dim * 4;
         char* pin = static_cast<char*>(ws.wire_pin) + off;  // pinned: an async DMA, no driver staging
         std::memcpy(pin, st.f.tensor, st.f.tensor_len);
-        SFG_CUDA(cudaMemcpyAsync(wire + off, pin, st.f.tensor_len, cudaMemcpyHostToDevice, s));
+        SFG_CUDA(copy_async(wire + off, pin, st.f.tensor_len, cudaMemcpyHostToDevice, s));
         launch_unpack_rows(wire + off, in_f32, st.hc.seq * c.hidden_dim, ws.h + static_cast<size_t>(row0[i]) * c.hidden_dim, s);
     }
     SFG_CUDA(cudaMemsetAsync(ws.status, 0, sizeof(uint32_t), s));
@@ -347,12 +347,12 @@ void Server::run(std::vector<StepState*>& group) {
         launch_pack_rows(ws.h + static_cast<size_t>(row0[i]) * c.hidden_dim, st.out_dt == wire::Dtype::f32, n,
                          wire + off, nullptr, s);
         out_bytes[i] = static_cast<size_t>(n) * wire::width(st.out_dt);
-        SFG_CUDA(cudaMemcpyAsync(static_cast<char*>(ws.wire_pin) + off, wire + off, out_bytes[i],
+        SFG_CUDA(copy_async(static_cast<char*>(ws.wire_pin) + off, wire + off, out_bytes[i],
                                  cudaMemcpyDeviceToHost, s));
     }
     SFG_CUDA(cudaGetLastError());
     uint32_t* stw = reinterpret_cast<uint32_t*>(static_cast<char*>(ws.pinned) + ws.pinned_bytes - 64);
-    SFG_CUDA(cudaMemcpyAsync(stw, ws.status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    SFG_CUDA(copy_async(stw, ws.status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     SFG_CUDA(cudaStreamSynchronize(s));
     if (*stw & ST_ATTN_CAP) throw Error(Kind::internal, "attention launch sized below the visible key count");
     if (*stw & ST_EMPTY_ROW) throw Error(Kind::protocol, "mask row admits no attendable position");

@@ -58,6 +58,15 @@ def response_rows(b: bytes, hidden: int):
     return h, np.frombuffer(body, dtype=dt).astype(np.float32).reshape(h["shape"])
 
 
+def rows_of(h: dict, body: bytes) -> np.ndarray:
+    """The hidden-row tensor of a decoded request/response frame as fp32
+    (the mask, when present, follows the tensor and is ignored)."""
+    rows, dim = h["shape"]
+    dt = np.float32 if h["dtype"] == "f32" else np.float16
+    n = rows * dim
+    return np.frombuffer(body[:n * np.dtype(dt).itemsize], dtype=dt).astype(np.float32).reshape(rows, dim)
+
+
 def strip_srv_ms(b: bytes) -> bytes:
     h, body = decode(b)
     h.pop("srv_ms", None)
