@@ -247,12 +247,16 @@ int Client::dev_server(int rows, Bank* server_bank, cudaStream_t s) {
     const int f32 = cfg_.wire_dtype == SFG_WIRE_F32;
     int k = launch_wire_roundtrip(ws.h, f32, n, ws.clamped, s);  // encode/decode_values
     k += launch_link_delay(cfg_.one_way_delay_ms, s);             // request leg
-    // External records: under stream capture they become event-record nodes of
-    // the step's graph, so the server segment is timed on every replay too
-    SFG_CUDA(cudaEventRecordWithFlags(ev_[1], s, cudaEventRecordExternal));
+    // under stream capture the records are made External: they become
+    // event-record nodes of the step's graph, so the server segment is timed
+    // on every replay too (the flag is only legal while capturing)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    SFG_CUDA(cudaStreamIsCapturing(s, &cap));
+    const unsigned evf = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+    SFG_CUDA(cudaEventRecordWithFlags(ev_[1], s, evf));
     k += linked_->engine().forward_device(*server_bank, linked_->config().layer_begin, linked_->config().layer_end,
                                           rows, ws, s);
-    SFG_CUDA(cudaEventRecordWithFlags(ev_[2], s, cudaEventRecordExternal));
+    SFG_CUDA(cudaEventRecordWithFlags(ev_[2], s, evf));
     const int rd = linked_->config().response_dtype;
     k += launch_wire_roundtrip(ws.h, rd < 0 ? f32 : rd == SFG_WIRE_F32, n, nullptr, s);
     k += launch_link_delay(cfg_.one_way_delay_ms, s);             // response leg
