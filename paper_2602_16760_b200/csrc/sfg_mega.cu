@@ -92,6 +92,7 @@ struct MegaArgs {
     int evict_first;   // stream weights with an L2 evict-first policy
     int spin_mma;      // dev knob: MMA issuer spins on test_wait instead of try_wait
     int bpf;           // bubble L2 prefetch depth in units (0: off)
+    int noload;        // dev knob (timing experiments only, WRONG results): bit 0 no weight bytes, bit 1 no activation bytes
     int G[4];          // per phase: CTAs sharing its stream-K split (phase_ctas)
     int W[4];          // per phase: whole tiles per CTA after the split part (whole_tiles)
     int fl_base, fl_lay, fl_off[6];  // dataflow flag layout (see fptr)
@@ -126,10 +127,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-constexpr int kTraceW = 16;
+constexpr int kTraceW = 20;
 // slot k of (CTA c, barrier id): 0 X start, 1 X done, 2 arrive, 3/4/5 ns waited by
 // X loader (empty) / MMA (full) / producer (empty), 6 last accumulator ready,
-// 7 epilogue done; last fixup: 8 partials fenced, 9 counter, 10 loads, 11 epi_final
+// 7 epilogue done; last fixup: 8 partials fenced, 9 counter, 10 loads, 11 epi_final;
+// MMA issuer: 16 first MMA issued, 17 last commit, 18 ns waited on a free accumulator
 __device__ __forceinline__ unsigned long long* tslot(const MegaArgs& a, int c, int id, int k) {
     return a.trace + (static_cast<size_t>(c) * 256 + id) * kTraceW + k;
 }
@@ -1194,11 +1196,15 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         } else {
                             mwait_acc(&empty[stage], ph ^ 1, a.trace != nullptr, wacc);
                         }
+                        if (a.noload & 1) {
+                            mbar_arrive(&full[stage]);
+                        } else {
                         mbar_expect_tx(&full[stage], kABytes);
                         if (a.evict_first)
                             bulk_g2s_stream(smem + stage * kStageBytes, W + static_cast<size_t>(u) * kABytes, kABytes, &full[stage], pol);
                         else
                             bulk_g2s(smem + stage * kStageBytes, W + static_cast<size_t>(u) * kABytes, kABytes, &full[stage]);
+                        }
                         if (a.pf) cursor_prefetch_next(a, c, pf);
                         if (++stage == S) {
                             stage = 0;
@@ -1216,7 +1222,8 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
             for (int l = 0; l < a.nlayers; ++l)
                 for (int p = 0; p < 4; ++p) {
                     const Geo g = geom(a, p);
-                    unsigned long long wacc = 0;
+                    unsigned long long wacc = 0, tacc = 0;
+                    bool mfirst = false;
                     for (int sg = 0; sg < 2; ++sg) {
                     int st, en;
                     unit_seg(g, c, sg, st, en);
@@ -1224,7 +1231,11 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         const int t = static_cast<int>(u / g.KB);
                         const int lo = u - t * g.KB;
                         const int hi = min(en - t * g.KB, g.KB);
-                        mwait(&tempty[acc], acc_ph ^ 1);
+                        mwait_acc(&tempty[acc], acc_ph ^ 1, a.trace != nullptr, tacc);
+                        if (a.trace && !mfirst) {
+                            mfirst = true;
+                            *tslot(a, c, input_barrier(l, p), 16) = gtimer();
+                        }
                         tc_fence_after();
                         const uint32_t d = tmem + acc * kAccCols;
                         for (int kb = lo; kb < hi; ++kb) {
@@ -1254,7 +1265,11 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         u = t * g.KB + hi;
                     }
                     }
-                    if (a.trace) *tslot(a, c, input_barrier(l, p), 4) = wacc;
+                    if (a.trace) {
+                        *tslot(a, c, input_barrier(l, p), 4) = wacc;
+                        *tslot(a, c, input_barrier(l, p), 17) = gtimer();
+                        *tslot(a, c, input_barrier(l, p), 18) = tacc;
+                    }
                 }
         }
     } else if (warp < 6) {  // ── epilogue warps 2..5 (+ attention)
@@ -1483,9 +1498,13 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         }
                         if (lane == 0) {
                             mwait_acc(&empty[stage], ph ^ 1, a.trace != nullptr, xwacc);
-                            mbar_expect_tx(&full[stage], kBBytes);
-                            bulk_g2s(smem + stage * kStageBytes + kABytes, X + static_cast<size_t>(u % g.KB) * kBBytes,
-                                     kBBytes, &full[stage]);
+                            if (a.noload & 2) {
+                                mbar_arrive(&full[stage]);
+                            } else {
+                                mbar_expect_tx(&full[stage], kBBytes);
+                                bulk_g2s(smem + stage * kStageBytes + kABytes, X + static_cast<size_t>(u % g.KB) * kBBytes,
+                                         kBBytes, &full[stage]);
+                            }
                         }
                         if (++stage == S) {
                             stage = 0;
@@ -1823,6 +1842,11 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
             return v ? atoll(v) : 2000LL;
         }();
         a.bpf = bpf_env;
+        static const int noload_env = [] {
+            const char* v = getenv("SFG_MEGA_NOLOAD");  // dev knob: latency floor without weight traffic
+            return v ? atoi(v) : 0;
+        }();
+        a.noload = noload_env;
         static const int al_env = [] {
             const char* v = getenv("SFG_MEGA_ALIGN");
             return v ? atoi(v) : 85;

@@ -37,9 +37,10 @@ for it in range(4):
     times.append(time.perf_counter() - t0)
 print("wall per forward (ms):", [round(t * 1000, 3) for t in times])
 G = 148
-tr = np.zeros(G * 256 * 16, dtype=np.uint64)
+TW = 20
+tr = np.zeros(G * 256 * TW, dtype=np.uint64)
 L.sfg_debug_mega_trace_read(bank.h, tr.ctypes.data_as(C.POINTER(C.c_uint64)), tr.size)
-tr = tr.reshape(G, 256, 16).astype(np.int64)
+tr = tr.reshape(G, 256, TW).astype(np.int64)
 t0 = tr[:, 255, 0].min()
 names = {1: "QKV", 2: "ATTN", 3: "O", 4: "GU", 5: "DOWN"}
 print("kernel entry spread (us):", (tr[:, 255, 0].max() - t0) / 1000)
@@ -62,6 +63,19 @@ for bid in range(0, 1 + 5 * NL):
         return f"{np.median(v) / 1000:6.1f}/{v.max() / 1000:6.1f}"
     print(f"{bid:4d} {ph:>5} {col(0):>18} {col(1):>18} {col(2):>18} {dur(3):>14} {dur(4):>14} {dur(5):>14}"
           f" {col(6):>18}")
+# MMA issuer per phase of layer 2: first MMA, last commit (median/max), time
+# waited for a free accumulator, and busy time = last - first - waits
+print("MMA issuer (layer 2): phase  first med/max   last med/max   full-wait   acc-wait   span med")
+for k, ph in enumerate(("QKV", "O", "GU", "DOWN")):
+    in_id = {0: 5 * 2, 1: 5 * 2 + 2, 2: 5 * 2 + 3, 3: 5 * 2 + 4}[k]
+    f, la = tr[:, in_id, 16], tr[:, in_id, 17]
+    m = f > 0
+    if not m.any():
+        continue
+    span = (la[m] - f[m]) / 1000
+    print(f"   {ph:5s} {(np.median(f[m]) - t0) / 1000:7.1f}/{(f[m].max() - t0) / 1000:7.1f} "
+          f"{(np.median(la[m]) - t0) / 1000:7.1f}/{(la[m].max() - t0) / 1000:7.1f} "
+          f"{np.median(tr[m, in_id, 4]) / 1000:8.1f} {np.median(tr[m, in_id, 18]) / 1000:8.1f} {np.median(span):8.1f}")
 # the latest CTAs of each phase of layer 1: last accumulator ready (slot 6 of
 # the phase's input barrier) vs arrival at the phase's output barrier
 phase_in = {1: 5, 3: 7, 4: 8, 5: 9}  # output barrier id -> input barrier id (layer 1)
