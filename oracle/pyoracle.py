@@ -410,6 +410,12 @@ class _Bank:
         getattr(self.lib, f"{self.p}_bank_state")(self.h, C.byref(a), C.byref(b))
         return a.value, b.value
 
+    def load_layer(self, layer, k, v, length):
+        """(_ref only) install a layer's K/V slabs [n_kv x max_len x hd] and its length."""
+        k = np.ascontiguousarray(k, dtype=np.float32)
+        v = np.ascontiguousarray(v, dtype=np.float32)
+        self.o._check(self.lib.ref_bank_load_layer(self.h, layer, _ptr(k, _f32p), _ptr(v, _f32p), length))
+
     def kv(self, layer, head, pos):
         hd = self.m.cfg.head_dim
         k = np.zeros(hd, dtype=np.float32)

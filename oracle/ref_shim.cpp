@@ -360,6 +360,18 @@ int ref_bank_kv(void* bank, int layer, int head, int pos, float* k, float* v) {
     })
 }
 
+// Test hook: install a whole layer's K/V slabs [n_kv_heads x max_len x
+// head_dim] (e.g. read back from the GPU bank) and set its length, so a
+// long-context step can be checked without a CPU prefill of the context.
+int ref_bank_load_layer(void* bank, int layer, const float* k, const float* v, int len) {
+    GUARD({
+        auto& c = static_cast<CacheBank*>(bank)->layer(layer);
+        std::memcpy(c.keys.data(), k, c.keys.size() * sizeof(float));
+        std::memcpy(c.values.data(), v, c.values.size() * sizeof(float));
+        c.len = len;
+    })
+}
+
 int ref_embed_at(void* m, int seq, const int* ids, const int* pos, float* out) {
     GUARD({
         HiddenStates h = embed_at(*static_cast<Weights*>(m), std::span<const int>(ids, seq),
