@@ -42,10 +42,15 @@ H_7B = dict(vocab_size=32768, n_layers=32, hidden_dim=4096, n_heads=32, n_kv_hea
 # Appendix B.3): same d, layers, kv heads, ffn and vocab.
 H_12B = dict(vocab_size=131072, n_layers=40, hidden_dim=5120, n_heads=32, n_kv_heads=8, head_dim=160,
              ffn_dim=14336, max_seq_len=4096, rope_base=1e6, rms_eps=1e-5, seed=1234)
-MODELS = {"7b": H_7B, "12b": H_12B}
+# configs[3] at the TRUE NeMo-12B shape: q_dim 32 x 128 = 4096 != d 5120 (the
+# reference's validate() rejects it; the engine runs it with extended_shapes)
+H_NEMO = dict(vocab_size=131072, n_layers=40, hidden_dim=5120, n_heads=32, n_kv_heads=8, head_dim=128,
+              ffn_dim=14336, max_seq_len=4096, rope_base=1e6, rms_eps=1e-5, seed=1234)
+MODELS = {"7b": H_7B, "12b": H_12B, "nemo12b": H_NEMO}
 MODEL = H_7B
 SHAPE_TEXT = {"7b": "mistral-7b (32L d4096 32q/8kv x128 ffn14336 V32768)",
-              "12b": "nemo-12b width (40L d5120 32q/8kv x160 ffn14336 V131072; head_dim-160 variant)"}
+              "12b": "nemo-12b width (40L d5120 32q/8kv x160 ffn14336 V131072; head_dim-160 variant)",
+              "nemo12b": "mistral-nemo-12b (40L d5120 32q/8kv x128 = q_dim 4096, ffn14336 V131072; true shape)"}
 SPLIT = 2
 W, NG, G = 5, 3, 5
 PROMPT_LEN = 24
@@ -219,7 +224,7 @@ def ncu_traffic(args):
 def config_dict(args, ws):
     nl = MODEL["n_layers"]
     mid = nl - 2 * SPLIT
-    name = "mistral7b" if args.model == "7b" else "nemo12b"
+    name = {"7b": "mistral7b", "12b": "nemo12b-hd160", "nemo12b": "nemo12b"}[args.model]
     return {"workload": f"{name}-shape lookahead step, {SPLIT}+{SPLIT} local split ({mid} middle layers), "
                         "W=5 N=3 G=5, forced B=16 (seeded n-gram pool)",
             "model_shape": SHAPE_TEXT[args.model], "rows_per_step": 16,
@@ -267,9 +272,10 @@ def run_ours(args, ws, rank, local):
         if rank == 0:
             buf.copy_(torch.frombuffer(bytearray(sfg.tp_unique_id()), dtype=torch.uint8))
         dist.broadcast(buf, src=0)
-        eng = sfg.Engine(cfg, math=math, device=local, tp=(args.tp, rank, bytes(buf.cpu().numpy().tobytes())))
+        eng = sfg.Engine(cfg, math=math, device=local, tp=(args.tp, rank, bytes(buf.cpu().numpy().tobytes())),
+                         extended_shapes=args.model == "nemo12b")
     else:
-        eng = sfg.Engine(cfg, math=math, device=local)
+        eng = sfg.Engine(cfg, math=math, device=local, extended_shapes=args.model == "nemo12b")
     t_init = time.time() - t0
     nl = cfg.n_layers
     srv = sfg.ServerEngine(eng, sfg.ServerConfig(SPLIT, nl - SPLIT, max_sessions=64))

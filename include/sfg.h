@@ -88,6 +88,12 @@ typedef struct {
     int32_t layer_end;
     int32_t with_embedding; /* local side: embedding table                        */
     int32_t with_head;      /* local side: final_norm + lm_head                   */
+    int32_t extended_shapes;/* 1: also accept n_heads * head_dim != hidden_dim,
+                               i.e. q_dim != hidden (Mistral NeMo 12B: 32 x 128 =
+                               4096 vs 5120).  The reference's validate() rejects
+                               such configs (tinyformer.cpp:109-111) although its
+                               arithmetic uses q_dim() throughout (:405-406, :444,
+                               :491); 0 keeps the reference's config errors.     */
 } sfg_engine_options;
 
 typedef struct sfg_engine sfg_engine;

@@ -167,14 +167,22 @@ class Port(_Base):
         self._errfn = self.lib.orc_last_error
 
     # model -----------------------------------------------------------------
-    def model(self, cfg: ModelCfg, bf16: bool = True, params: np.ndarray | None = None):
+    def model(self, cfg: ModelCfg, bf16: bool = True, params: np.ndarray | None = None, layers: tuple | None = None):
         h = C.c_void_p()
-        if params is None:
+        if layers is not None:  # decoder layers [lo, hi) of the init stream only
+            self._check(self.lib.orc_model_new_layers(C.byref(_ccfg(cfg)), int(bf16), layers[0], layers[1],
+                                                      C.byref(h)))
+        elif params is None:
             self._check(self.lib.orc_model_new(C.byref(_ccfg(cfg)), int(bf16), C.byref(h)))
         else:
             p = np.ascontiguousarray(params, dtype=np.float32)
             self._check(self.lib.orc_model_from_params(C.byref(_ccfg(cfg)), _ptr(p, _f32p), C.byref(h)))
         return _Model(self, h, cfg, "orc")
+
+    def set_relaxed_validate(self, on: bool):
+        """Accept q_dim != hidden_dim (NeMo-12B); the reference's validate()
+        rejects it while its arithmetic uses q_dim throughout."""
+        self.lib.orc_set_relaxed_validate(int(on))
 
     def param_count(self, cfg: ModelCfg) -> int:
         return int(self.lib.orc_param_count(C.byref(_ccfg(cfg))))
@@ -251,9 +259,16 @@ class Ref(_Base):
         self.lib = Ref._lib
         self._errfn = self.lib.ref_last_error
 
-    def model(self, cfg: ModelCfg, bf16: bool = True, layers: tuple | None = None, with_head=True):
+    def model(self, cfg: ModelCfg, bf16: bool = True, layers: tuple | None = None, with_head=True,
+              unchecked: bool = False):
+        """unchecked: skip ModelConfig::validate (q_dim != hidden, NeMo-12B);
+        needs `layers` (ref_model_new_unchecked)."""
         h = C.c_void_p()
         lo, hi = layers if layers is not None else (-1, -1)
+        if unchecked:
+            self._check(self.lib.ref_model_new_unchecked(C.byref(_ccfg(cfg)), int(bf16), lo, hi, int(with_head),
+                                                         C.byref(h)))
+            return _Model(self, h, cfg, "ref")
         self._check(self.lib.ref_model_new(C.byref(_ccfg(cfg)), int(bf16), lo, hi, int(with_head),
                                            C.byref(h)))
         return _Model(self, h, cfg, "ref")
@@ -499,6 +514,13 @@ def tiny_cfg(seed=1234) -> ModelCfg:
 
 def mistral7b_cfg(seed=1234, max_seq_len=4096) -> ModelCfg:
     return ModelCfg(vocab_size=32768, n_layers=32, hidden_dim=4096, n_heads=32, n_kv_heads=8,
+                    head_dim=128, ffn_dim=14336, max_seq_len=max_seq_len, rope_base=1e6, rms_eps=1e-5,
+                    seed=seed)
+
+
+def nemo12b_cfg(seed=1234, max_seq_len=4096) -> ModelCfg:
+    """Mistral NeMo 12B true shape: d=5120, 32 q heads x 128 = q_dim 4096 (!= d)."""
+    return ModelCfg(vocab_size=131072, n_layers=40, hidden_dim=5120, n_heads=32, n_kv_heads=8,
                     head_dim=128, ffn_dim=14336, max_seq_len=max_seq_len, rope_base=1e6, rms_eps=1e-5,
                     seed=seed)
 

@@ -98,8 +98,10 @@ void fill_or_skip(std::vector<float>& dst, size_t n, float a, std::mt19937_64& r
     }
 }
 
+bool g_unchecked = false;  // skip ModelConfig::validate (q_dim != hidden shapes)
+
 Weights partial_weights(const ModelConfig& c, int lo, int hi, bool head) {
-    c.validate();
+    if (!g_unchecked) c.validate();
     Weights w;
     w.config = c;
     w.layers.resize(c.n_layers);
@@ -190,19 +192,43 @@ int ref_model_new(const ref_model_cfg* c, int bf16, int layer_lo, int layer_hi, 
     })
 }
 
+// The same partial init without ModelConfig::validate: q_dim != hidden_dim
+// (Mistral NeMo 12B, 32 x 128 = 4096 vs 5120).  init_weights / ServerEngine /
+// SplitClient reject that shape (tinyformer.cpp:109-111), but forward_layers
+// and CacheBank never validate and use q_dim() throughout (:405-406, :444,
+// :491), so the reference's own forward_layers runs on it unmodified.
+int ref_model_new_unchecked(const ref_model_cfg* c, int bf16, int layer_lo, int layer_hi, int with_head,
+                            void** out) {
+    GUARD({
+        g_unchecked = true;
+        try {
+            auto* w = new Weights(partial_weights(to_cfg(c), layer_lo, layer_hi, with_head != 0));
+            if (bf16) round_all(*w);
+            *out = w;
+        } catch (...) {
+            g_unchecked = false;
+            throw;
+        }
+        g_unchecked = false;
+    })
+}
+
 // Timing-only model for the CPU baseline: the requested tensors get
 // U[-a, a] values (same distribution, NOT the reference stream positions)
 // without walking the 7.25 G-draw stream; arithmetic cost is identical.
 int ref_model_new_timing(const ref_model_cfg* c, int layer_lo, int layer_hi, int with_head, void** out) {
     GUARD({
         g_timing_only = true;
+        g_unchecked = true;  // timing only: the NeMo-12B true shape (q_dim != hidden) too
         try {
             *out = new Weights(partial_weights(to_cfg(c), layer_lo, layer_hi, with_head != 0));
         } catch (...) {
             g_timing_only = false;
+            g_unchecked = false;
             throw;
         }
         g_timing_only = false;
+        g_unchecked = false;
     })
 }
 

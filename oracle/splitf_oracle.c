@@ -71,6 +71,14 @@ struct orc_model {
     float* lm_head;
 };
 
+/* Relaxed validation (test switch): accept n_heads * head_dim != hidden_dim
+ * (q_dim != hidden, the Mistral NeMo 12B shape).  The reference rejects such
+ * configs (tinyformer.cpp:109-111) but every arithmetic site already uses
+ * q_dim (:405-406 Q/K/V, :444 Q matvec, :491 O matvec), as this restatement
+ * does; so the relaxed oracle is the reference's arithmetic on that shape. */
+static int g_relaxed = 0;
+void orc_set_relaxed_validate(int on) { g_relaxed = on != 0; }
+
 /* ModelConfig::validate, tinyformer.cpp:102-121 */
 static int validate(const orc_cfg* c) {
     if (c->vocab_size < 2) return err(K_CONFIG, "vocab_size must be >= 2");
@@ -78,7 +86,7 @@ static int validate(const orc_cfg* c) {
     if (c->hidden_dim <= 0 || c->n_heads <= 0 || c->n_kv_heads <= 0 || c->head_dim <= 0 ||
         c->ffn_dim <= 0 || c->max_seq_len <= 0)
         return err(K_CONFIG, "all dimensions must be positive");
-    if (c->n_heads * c->head_dim != c->hidden_dim)
+    if (c->n_heads * c->head_dim != c->hidden_dim && !g_relaxed)
         return err(K_CONFIG, "n_heads * head_dim must equal hidden_dim");
     if (c->n_heads % c->n_kv_heads != 0) return err(K_CONFIG, "n_kv_heads must divide n_heads");
     if (c->head_dim % 2 != 0) return err(K_CONFIG, "head_dim must be even for rotary pairs");
@@ -159,6 +167,53 @@ int orc_model_new(const orc_cfg* c, int bf16_round, orc_model** out) {
         m->flat[i] = bf16_round ? bf16_rne(v) : v;
     }
     free(rng);
+    return 0;
+}
+
+/* init_weights restricted to the decoder layers [lo, hi): the same stream,
+ * every other tensor's draws discarded, so a single wide layer (7B / 12B
+ * width) is materialised without the whole model.  The partial model has
+ * no embedding or head: only cache banks / forward_layers inside [lo, hi). */
+int orc_model_new_layers(const orc_cfg* c, int bf16_round, int lo, int hi, orc_model** out) {
+    int rc = validate(c);
+    if (rc) return rc;
+    if (lo < 0 || hi > c->n_layers || lo >= hi) return err(K_CONFIG, "invalid layer range");
+    const int64_t h = c->hidden_dim, q = (int64_t)c->n_heads * c->head_dim,
+                  kv = (int64_t)c->n_kv_heads * c->head_dim, f = c->ffn_dim, v = c->vocab_size;
+    const int64_t per = h + h * q + 2 * h * kv + q * h + h + 3 * h * f;
+    orc_model* m = calloc(1, sizeof *m);
+    m->c = *c;
+    m->n = (hi - lo) * per;
+    m->flat = malloc((size_t)m->n * sizeof(float));
+    m->L = calloc((size_t)c->n_layers, sizeof(orc_layer));
+    if (!m->flat || !m->L) {
+        orc_model_free(m);
+        return err(K_INTERNAL, "out of host memory");
+    }
+    float* p = m->flat;
+    for (int l = lo; l < hi; ++l) {
+        orc_layer* L = &m->L[l];
+        L->attn_norm = p; p += h;
+        L->wq = p; p += h * q;
+        L->wk = p; p += h * kv;
+        L->wv = p; p += h * kv;
+        L->wo = p; p += q * h;
+        L->ffn_norm = p; p += h;
+        L->w_gate = p; p += h * f;
+        L->w_up = p; p += h * f;
+        L->w_down = p; p += f * h;
+    }
+    const float a = 1.0f / sqrtf((float)c->hidden_dim);
+    mt64* rng = malloc(sizeof *rng);
+    mt_seed(rng, c->seed);
+    for (int64_t i = 0; i < v * h + (int64_t)lo * per; ++i) (void)mt_next(rng);
+    for (int64_t i = 0; i < m->n; ++i) {
+        const double u = (double)(mt_next(rng) >> 11) * 0x1.0p-53;
+        const float x = a * (float)(2.0 * u - 1.0);
+        m->flat[i] = bf16_round ? bf16_rne(x) : x;
+    }
+    free(rng);
+    *out = m;
     return 0;
 }
 

@@ -39,6 +39,10 @@ typedef struct orc_pool orc_pool;
 const char* orc_last_error(void);
 
 int orc_model_new(const orc_cfg* c, int bf16_round, orc_model** out);
+/* only decoder layers [lo, hi) of the init stream (no embedding / head) */
+int orc_model_new_layers(const orc_cfg* c, int bf16_round, int lo, int hi, orc_model** out);
+/* test switch: accept q_dim != hidden_dim (NeMo-12B), see splitf_oracle.c */
+void orc_set_relaxed_validate(int on);
 int orc_model_from_params(const orc_cfg* c, const float* params, orc_model** out);
 void orc_model_free(orc_model* m);
 int64_t orc_param_count(const orc_cfg* c);

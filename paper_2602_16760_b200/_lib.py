@@ -44,7 +44,7 @@ class ModelConfig(C.Structure):
 
 class EngineOptions(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("device", "math", "weight_dtype", "layer_begin", "layer_end",
-                                          "with_embedding", "with_head")]
+                                          "with_embedding", "with_head", "extended_shapes")]
 
 
 class ServerConfig(C.Structure):

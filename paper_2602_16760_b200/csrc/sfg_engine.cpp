@@ -49,13 +49,13 @@ DeviceGuard::~DeviceGuard() {
 }
 
 // ModelConfig::validate (tinyformer.cpp:102-121)
-void ModelCfg::validate() const {
+void ModelCfg::validate(bool extended) const {
     if (vocab_size < 2) throw Error(Kind::config, "vocab_size must be >= 2");
     if (n_layers < 4) throw Error(Kind::config, "n_layers must be >= 4");
     if (hidden_dim <= 0 || n_heads <= 0 || n_kv_heads <= 0 || head_dim <= 0 || ffn_dim <= 0 ||
         max_seq_len <= 0)
         throw Error(Kind::config, "all dimensions must be positive");
-    if (n_heads * head_dim != hidden_dim)
+    if (n_heads * head_dim != hidden_dim && !extended)
         throw Error(Kind::config, "n_heads * head_dim must equal hidden_dim");
     if (n_heads % n_kv_heads != 0) throw Error(Kind::config, "n_kv_heads must divide n_heads");
     if (head_dim % 2 != 0) throw Error(Kind::config, "head_dim must be even for rotary pairs");
@@ -352,7 +352,7 @@ static float bf16_rne_host(float v) {
 
 Engine::Engine(const ModelCfg& cfg, const sfg_engine_options& opt, const float* params, const TpConfig& tp)
     : cfg_(cfg), opt_(opt), tp_size_(tp.size), tp_rank_(tp.rank) {
-    cfg_.validate();
+    cfg_.validate(opt_.extended_shapes != 0);
     if (tp_size_ < 1 || tp_rank_ < 0 || tp_rank_ >= tp_size_) throw Error(Kind::config, "invalid tensor-parallel rank");
     if (tp_size_ > 1) {
         if (opt_.math != SFG_MATH_FAST) throw Error(Kind::config, "tensor parallelism runs FAST math");

@@ -49,7 +49,8 @@ struct ModelCfg {
     uint64_t seed;
     int q_dim() const { return n_heads * head_dim; }
     int kv_dim() const { return n_kv_heads * head_dim; }
-    void validate() const;  // ModelConfig::validate, tinyformer.cpp:102-121
+    // ModelConfig::validate, tinyformer.cpp:102-121; extended: q_dim may differ from hidden_dim
+    void validate(bool extended = false) const;
     static ModelCfg from_c(const sfg_model_config& c);
 };
 

@@ -80,14 +80,16 @@ class Engine:
 
     def __init__(self, cfg, math: int = EXACT, weights: str = "bf16", layers: tuple | None = None,
                  with_embedding: bool = True, with_head: bool = True, device: int = 0,
-                 params: np.ndarray | None = None, tp: tuple | None = None):
+                 params: np.ndarray | None = None, tp: tuple | None = None, extended_shapes: bool = False):
         """tp = (size, rank, unique_id bytes): this engine is rank `rank` of a
-        tensor-parallel group (see tp_unique_id; FAST math, seeded weights)."""
+        tensor-parallel group (see tp_unique_id; FAST math, seeded weights).
+        extended_shapes: accept q_dim != hidden_dim (NeMo-12B), which the
+        reference's validate() rejects (sfg.h sfg_engine_options)."""
         self.cfg = ModelConfig.from_any(cfg)
         L = _lib.lib()
         lb, le = layers if layers is not None else (0, self.cfg.n_layers)
         opt = _lib.EngineOptions(device, math, 0 if weights == "bf16" else 1, lb, le, int(with_embedding),
-                                 int(with_head))
+                                 int(with_head), int(extended_shapes))
         h = C.c_void_p()
         cc = self.cfg.to_c()
         if tp is not None and tp[0] > 1:

@@ -253,3 +253,43 @@ def test_expf_port_exhaustive(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "mismatches 0" in r.stdout
+
+
+def test_relaxed_port_equals_reference_forward_q_dim_ne_hidden(port, ref):
+    """NeMo-12B geometry (q_dim != hidden_dim) at a small width: the relaxed C
+    restatement is bit-identical to the reference's OWN forward_layers run on
+    that shape (weights built without ModelConfig::validate, which is the only
+    reference code that rejects it; forward_layers uses q_dim() throughout,
+    tinyformer.cpp:405-406, :444, :491) - prompt pass, branch-masked step,
+    resolve, and the K/V entries."""
+    cfg = po.ModelCfg(vocab_size=256, n_layers=4, hidden_dim=160, n_heads=4, n_kv_heads=2, head_dim=32,
+                      ffn_dim=192, max_seq_len=64, rope_base=1e6, seed=99)  # q_dim 128 != 160
+    port.set_relaxed_validate(True)
+    try:
+        mp = port.model(cfg, bf16=True, layers=(1, 3))
+        with pytest.raises(po.OracleError):
+            port.set_relaxed_validate(False)
+            port.model(cfg, bf16=True, layers=(1, 3))
+        port.set_relaxed_validate(True)
+        mr = ref.model(cfg, bf16=True, layers=(1, 3), with_head=False, unchecked=True)
+        with pytest.raises(po.OracleError, match="n_heads \\* head_dim must equal hidden_dim"):
+            ref.model(cfg, bf16=True, layers=(1, 3), with_head=False)
+        rng = np.random.default_rng(3)
+        bp, br = mp.bank(1, 3), mr.bank(1, 3)
+        h = (rng.standard_normal((9, cfg.hidden_dim)) * 0.5).astype(np.float32)
+        assert np.array_equal(bp.forward(1, 3, h, list(range(9))), br.forward(1, 3, h, list(range(9))))
+        bp.mark_committed(9)
+        br.mark_committed(9)
+        mask = np.zeros((3, 12), np.float32)
+        mask[1, 10] = -np.inf
+        mask[2, 10:] = -np.inf
+        x = (rng.standard_normal((3, cfg.hidden_dim)) * 0.5).astype(np.float32)
+        assert np.array_equal(bp.forward(1, 3, x, [9, 10, 10], mask), br.forward(1, 3, x, [9, 10, 10], mask))
+        bp.resolve([0, 2])
+        br.resolve([0, 2])
+        for l, hh, p in ((1, 0, 3), (2, 1, 9), (2, 1, 10)):
+            kp, vp = bp.kv(l, hh, p)
+            kr, vr = br.kv(l, hh, p)
+            assert np.array_equal(kp, kr) and np.array_equal(vp, vr)
+    finally:
+        port.set_relaxed_validate(False)
