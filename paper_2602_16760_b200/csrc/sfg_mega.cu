@@ -92,7 +92,7 @@ struct MegaArgs {
     int evict_first;   // stream weights with an L2 evict-first policy
     int spin_mma;      // dev knob: MMA issuer spins on test_wait instead of try_wait
     int bpf;           // bubble L2 prefetch depth in units (0: off)
-    int noload;        // dev knob (timing experiments only, WRONG results): bit 0 no weight bytes, bit 1 no activation bytes
+    int noload;        // dev knob (timing experiments only, WRONG results): bit 0 no weight bytes, bit 1 no activation bytes, bit 2 no input flag polls
     int G[4];          // per phase: CTAs sharing its stream-K split (phase_ctas)
     int W[4];          // per phase: whole tiles per CTA after the split part (whole_tiles)
     int fl_base, fl_lay, fl_off[6];  // dataflow flag layout (see fptr)
@@ -1483,7 +1483,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                             unsigned long long spins = 0;
                             while (u >= ready) {
                                 const int uu = ready + lane;
-                                const bool ok = uu >= en || xblock_ready(a, l, p, static_cast<int>(uu % g.KB));
+                                const bool ok = uu >= en || (a.noload & 4) || xblock_ready(a, l, p, static_cast<int>(uu % g.KB));
                                 const unsigned mk = __ballot_sync(0xffffffffu, ok);
                                 const int k = mk == 0xffffffffu ? 32 : __ffs(~mk) - 1;
                                 ready += k;
