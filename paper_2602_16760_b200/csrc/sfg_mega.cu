@@ -1128,8 +1128,13 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
         for (int j = n; j < kRows; ++j) sh_tail[r][j] = prior;
         sh_ncols[r] = r < a.rows ? prior + n : 0;
     }
+    // the ring is walked in PAIRS of stages: one full / empty barrier per pair
+    // (two consecutive units of a phase segment), so the MMA issuer waits and
+    // commits once per 32 KB of weights instead of once per 16 KB (each wait +
+    // commit costs the single issuing thread ~90 ns, tools/mb_issue.cu)
+    const int NP = S / 2;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
+        for (int s = 0; s < NP; ++s) {
             mbar_init(&full[s], 2);   // weight bytes + activation bytes (two expect_tx arrivals)
             mbar_init(&empty[s], 1);
         }
@@ -1172,7 +1177,8 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     for (int sg = 0; sg < 2; ++sg) {
                     int st, en;
                     unit_seg(g, c, sg, st, en);
-                    for (int u = st; u < en; ++u, ++n_cur) {
+                    for (int u = st; u < en; u += 2, n_cur += 2) {
+                        const int n = min(2, en - u);
                         if (a.bpf > 0) {
                             if (!mbar_test(&empty[stage], ph ^ 1)) {
                                 const long long t0 = clock64();
@@ -1199,14 +1205,19 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         if (a.noload & 1) {
                             mbar_arrive(&full[stage]);
                         } else {
-                        mbar_expect_tx(&full[stage], kABytes);
-                        if (a.evict_first)
-                            bulk_g2s_stream(smem + stage * kStageBytes, W + static_cast<size_t>(u) * kABytes, kABytes, &full[stage], pol);
-                        else
-                            bulk_g2s(smem + stage * kStageBytes, W + static_cast<size_t>(u) * kABytes, kABytes, &full[stage]);
+                            mbar_expect_tx(&full[stage], n * kABytes);
+                            for (int h = 0; h < n; ++h) {
+                                uint8_t* dst = smem + (2 * stage + h) * kStageBytes;
+                                const uint8_t* src = W + static_cast<size_t>(u + h) * kABytes;
+                                if (a.evict_first)
+                                    bulk_g2s_stream(dst, src, kABytes, &full[stage], pol);
+                                else
+                                    bulk_g2s(dst, src, kABytes, &full[stage]);
+                            }
                         }
-                        if (a.pf) cursor_prefetch_next(a, c, pf);
-                        if (++stage == S) {
+                        for (int h = 0; h < n; ++h)
+                            if (a.pf) cursor_prefetch_next(a, c, pf);
+                        if (++stage == NP) {
                             stage = 0;
                             ph ^= 1;
                         }
@@ -1219,6 +1230,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
         if (lane == 0) {  // ── MMA issuer
             int stage = 0, acc = 0;
             uint32_t ph = 0, acc_ph = 0;
+            const uint32_t ring0 = smem_u32(smem);
             for (int l = 0; l < a.nlayers; ++l)
                 for (int p = 0; p < 4; ++p) {
                     const Geo g = geom(a, p);
@@ -1227,18 +1239,19 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     for (int sg = 0; sg < 2; ++sg) {
                     int st, en;
                     unit_seg(g, c, sg, st, en);
-                    for (int u = st; u < en;) {
-                        const int t = static_cast<int>(u / g.KB);
-                        const int lo = u - t * g.KB;
-                        const int hi = min(en - t * g.KB, g.KB);
-                        mwait_acc(&tempty[acc], acc_ph ^ 1, a.trace != nullptr, tacc);
-                        if (a.trace && !mfirst) {
-                            mfirst = true;
-                            *tslot(a, c, input_barrier(l, p), 16) = gtimer();
+                    int t = st / max(g.KB, 1), kb = st - t * g.KB;
+                    int lo = kb, hi = min(en - t * g.KB, g.KB);
+                    for (int u = st; u < en; ++u) {
+                        const int half = (u - st) & 1;
+                        if (kb == lo) {  // a new tile: its accumulator must be drained
+                            mwait_acc(&tempty[acc], acc_ph ^ 1, a.trace != nullptr, tacc);
+                            if (a.trace && !mfirst) {
+                                mfirst = true;
+                                *tslot(a, c, input_barrier(l, p), 16) = gtimer();
+                            }
+                            tc_fence_after();
                         }
-                        tc_fence_after();
-                        const uint32_t d = tmem + acc * kAccCols;
-                        for (int kb = lo; kb < hi; ++kb) {
+                        if (half == 0) {  // one wait per pair of units
                             if (a.spin_mma) {
                                 unsigned long long sp = 0;
                                 while (!mbar_test(&full[stage], ph))
@@ -1247,22 +1260,29 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                                 mwait_acc(&full[stage], ph, a.trace != nullptr, wacc);
                             }
                             tc_fence_after();
-                            const uint32_t sa = smem_u32(smem + stage * kStageBytes);
-                            const uint64_t da = smem_desc(sa), db = smem_desc(sa + kABytes);
+                        }
+                        const uint32_t sa = ring0 + static_cast<uint32_t>((2 * stage + half) * kStageBytes);
+                        const uint64_t da = smem_desc(sa), db = smem_desc(sa + kABytes);
+                        const uint32_t d = tmem + acc * kAccCols;
 #pragma unroll
-                            for (int k = 0; k < kKB / 16; ++k) mma_bf16(d, da + 2 * k, db + 2 * k, (kb > lo || k > 0) ? 1u : 0u);
+                        for (int k = 0; k < kKB / 16; ++k) mma_bf16(d, da + 2 * k, db + 2 * k, (kb > lo || k > 0) ? 1u : 0u);
+                        if (half == 1 || u + 1 == en) {  // the pair is consumed: release it
                             mma_commit(&empty[stage]);
-                            if (++stage == S) {
+                            if (++stage == NP) {
                                 stage = 0;
                                 ph ^= 1;
                             }
                         }
-                        mma_commit(&tfull[acc]);
-                        if (++acc == 2) {
-                            acc = 0;
-                            acc_ph ^= 1;
+                        if (++kb == hi) {  // the tile's last unit of this range
+                            mma_commit(&tfull[acc]);
+                            if (++acc == 2) {
+                                acc = 0;
+                                acc_ph ^= 1;
+                            }
+                            ++t;
+                            kb = lo = 0;
+                            hi = min(en - t * g.KB, g.KB);
                         }
-                        u = t * g.KB + hi;
                     }
                     }
                     if (a.trace) {
@@ -1478,10 +1498,11 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     int st, en;
                     unit_seg(g, c, sg, st, en);
                     int ready = st;
-                    for (int u = st; u < en; ++u) {
-                        if (u >= ready) {
+                    for (int u = st; u < en; u += 2) {
+                        const int n = min(2, en - u);
+                        if (u + n > ready) {
                             unsigned long long spins = 0;
-                            while (u >= ready) {
+                            while (u + n > ready) {
                                 const int uu = ready + lane;
                                 const bool ok = uu >= en || (a.noload & 4) || xblock_ready(a, l, p, static_cast<int>(uu % g.KB));
                                 const unsigned mk = __ballot_sync(0xffffffffu, ok);
@@ -1501,12 +1522,13 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                             if (a.noload & 2) {
                                 mbar_arrive(&full[stage]);
                             } else {
-                                mbar_expect_tx(&full[stage], kBBytes);
-                                bulk_g2s(smem + stage * kStageBytes + kABytes, X + static_cast<size_t>(u % g.KB) * kBBytes,
-                                         kBBytes, &full[stage]);
+                                mbar_expect_tx(&full[stage], n * kBBytes);
+                                for (int h = 0; h < n; ++h)
+                                    bulk_g2s(smem + (2 * stage + h) * kStageBytes + kABytes,
+                                             X + static_cast<size_t>((u + h) % g.KB) * kBBytes, kBBytes, &full[stage]);
                             }
                         }
-                        if (++stage == S) {
+                        if (++stage == NP) {
                             stage = 0;
                             ph ^= 1;
                         }
@@ -1728,10 +1750,10 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         const char* v = getenv("SFG_MEGA_STAGES");  // dev knob: ring depth sensitivity
         return v ? std::min(std::max(atoi(v), 2), kMaxStages) : kMaxStages;
     }();
-    int stages = stages_cap;
+    int stages = stages_cap & ~1;  // the ring is walked in pairs of stages
     const bool ra = rows_attention();
     const void* kfn = ra ? reinterpret_cast<const void*>(mega_kernel<true>) : reinterpret_cast<const void*>(mega_kernel<false>);
-    while (stages > 4 && smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len) > dyn_smem_budget(ra)) --stages;
+    while (stages > 4 && smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len) > dyn_smem_budget(ra)) stages -= 2;
     const size_t smem = smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len);
     {
         ensure_smem_attr(kfn, smem);

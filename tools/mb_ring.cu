@@ -35,6 +35,11 @@ __global__ void __launch_bounds__(128, 1) ring_kernel(int units, int mode, int S
     uint64_t* done = empty + 16;
     uint32_t* slot = reinterpret_cast<uint32_t*>(done + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (mode >= 6)  // valid (zero) operands instead of uninitialised shared memory
+        for (int i = threadIdx.x; i < S * stage_bytes / 16; i += blockDim.x)
+            reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    if (mode >= 6) mode -= 6;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -50,7 +55,7 @@ __global__ void __launch_bounds__(128, 1) ring_kernel(int units, int mode, int S
     const uint32_t tmem = *slot;
     unsigned long long t0 = clock64();
     if (warp == 0 && lane == 0) {
-        if (mode != 1) {
+        if (mode != 1 && mode < 3) {
             int stage = 0;
             uint32_t ph = 0;
             for (int u = 0; u < units; ++u) {
@@ -68,13 +73,13 @@ __global__ void __launch_bounds__(128, 1) ring_kernel(int units, int mode, int S
         int stage = 0;
         uint32_t ph = 0;
         for (int u = 0; u < units; ++u) {
-            if (mode != 1) mbar_wait(&full[stage], ph);
-            tc_fence_after();
-            const uint32_t sa = smem_u32(smem + stage * stage_bytes);
+            if (mode != 1 && mode < 3) mbar_wait(&full[stage], ph);
+            if (mode != 3 && mode != 5) tc_fence_after();
+            const uint32_t sa = smem_u32(smem + ((mode == 4 || mode == 5) ? 0 : stage) * stage_bytes);
             const uint64_t da = smem_desc(sa), db = smem_desc(sa + 16384);
 #pragma unroll
             for (int k = 0; k < 4; ++k) mma_n<N_>(tmem, da + 2 * k, db + 2 * k, (u > 0 || k > 0) ? 1u : 0u);
-            if (mode != 1) mma_commit(&empty[stage]);
+            if (mode != 1 && mode < 3) mma_commit(&empty[stage]);
             if (++stage == S) { stage = 0; ph ^= 1; }
         }
         mma_commit(done);
@@ -120,6 +125,7 @@ int main() {
     unsigned long long* d_out;
     cudaMalloc(&d_out, 148 * sizeof(unsigned long long));
     const int U = 4096;
+    for (int mode : {1, 3, 4, 5, 7, 11, 6}) run<48>(mode, 8, U, src, d_out);
     for (int mode : {1, 0, 2}) {
         run<48>(mode, 8, U, src, d_out);
         run<16>(mode, 8, U, src, d_out);
