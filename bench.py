@@ -385,32 +385,16 @@ def run_ours(args, ws, rank, local):
             sweep[f"{int(rtt)}ms"] = {"tok_s": nt / dt, "ms_per_step": dt / k * 1000.0}
             L.sfg_decoder_destroy(d)
 
-    # ── concurrent sessions per GPU (configs[4]): K sessions stepped
-    # round-robin on this GPU (one weight pass per session step: cross-session
-    # batching is the next step); aggregate = all ranks' tokens
+    # ── concurrent sessions per GPU (configs[4]): K client threads (one per
+    # session, like FrameServer's connection threads) decode through the
+    # Router + Batcher front end on this GPU's server; frames cross host
+    # memory; the batcher runs whatever steps are queued in one weight pass.
+    # Natural lookahead (W5 N3 G5, pool from each session's own history) on
+    # distinct random prompts; aggregate = all ranks' committed tokens / max
+    # wall time over ranks.
     sessions = {}
     if not args.no_sweep:
-        for k in (1, 4, 16):
-            cls = [sfg.SplitClient(eng, sfg.SplitConfig(SPLIT, SPLIT, sfg.F16, 0.0), srv,
-                                   session_id=f"bench-s{k}-{i}-{rank}") for i in range(k)]
-            decs = [make_decoder(cl) for cl in cls]
-            for d in decs:
-                step(d)
-                step(d)
-            rounds = 3
-            barrier(ws, local)
-            tr = time.perf_counter()
-            nt = 0
-            for _ in range(rounds):
-                for d in decs:
-                    nt += step(d)[0]
-            dt = barrier_max(ws, local, time.perf_counter() - tr)
-            nt_all = dist_sum(ws, local, float(nt))
-            sessions[str(k * ws)] = {"sessions_per_gpu": k, "gpus": ws, "aggregate_tok_s": nt_all / dt,
-                                     "per_session_step_ms": dt / rounds * 1000.0}
-            for d in decs:
-                L.sfg_decoder_destroy(d)
-            del cls
+        sessions = concurrent_sweep(sfg, eng, cfg, nl, rank, ws, local, args)
 
     # ── cross-session batching: the server's queue holds one
     # lookahead step per session; sfg_server_handle_batch runs them in ONE
@@ -498,6 +482,60 @@ def run_ours(args, ws, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def concurrent_sweep(sfg, eng, cfg, nl, rank, ws, local, args):
+    import numpy as np
+    out = {}
+    la = sfg.LookaheadConfig(ngram_n=NG, window_w=W, max_candidates_g=G)
+    ctxs = [(PROMPT_LEN, (1, 2, 4, 8, 16))]
+    if PROMPT_LEN < 2048 and not args.quick_sweep:
+        ctxs.append((2048, (1, 4)))
+    for ctx, ks in ctxs:
+        for k in ks:
+            srv_k = sfg.ServerEngine(eng, sfg.ServerConfig(SPLIT, nl - SPLIT, max_sessions=64))
+            router = sfg.Router([srv_k])
+            bq = sfg.Batcher(router)
+            prompts = [np.random.default_rng(1000 + i).integers(0, cfg.vocab_size, ctx).tolist() for i in range(k)]
+            new_tokens = 24
+            res, errs = [None] * k, []
+
+            def client(i):
+                try:
+                    cl = sfg.SplitClient(eng, sfg.SplitConfig(SPLIT, SPLIT, sfg.F16, 0.0), bq.handler,
+                                         session_id=f"conc-{ctx}-{k}-{i}-{rank}")
+                    t0 = time.perf_counter()
+                    d = sfg.decode_lookahead(cl, prompts[i], new_tokens, la)  # prefill + decode steps
+                    res[i] = (time.perf_counter() - t0 - d.wall_seconds, d.wall_seconds, d.tokens_committed, d.steps)
+                except Exception as e:  # the sweep must not take the bench line down
+                    errs.append(repr(e))
+
+            barrier(ws, local)
+            t0 = time.perf_counter()
+            ts = [threading.Thread(target=client, args=(i,)) for i in range(k)]
+            for t in ts:
+                t.start()
+            for t in ts:
+                t.join()
+            if errs:
+                out[f"{k}x{ctx}"] = {"error": errs[0]}
+                continue
+            dec_wall = max(r[1] for r in res)  # decode phase (prefill excluded), slowest session
+            dec_wall = barrier_max(ws, local, dec_wall)
+            toks = dist_sum(ws, local, float(sum(r[2] for r in res)))
+            steps = sum(r[3] for r in res)
+            st = bq.stats()
+            out[f"{k * ws}x{ctx}"] = {"sessions": k * ws, "sessions_per_gpu": k, "gpus": ws, "context": ctx,
+                                      "aggregate_tok_s": toks / dec_wall,
+                                      "per_session_step_ms": dec_wall / max(1, steps / k) * 1000.0,
+                                      "frames_per_server_batch": st["frames"] / max(1, st["batches"]),
+                                      "shared_weight_passes": srv_k.shared_passes(),
+                                      "prefill_ms_mean": sum(r[0] for r in res) / k * 1000.0,
+                                      "workload": f"{k} concurrent lookahead sessions (natural pool), "
+                                                  f"{ctx}-token prompts, {new_tokens} tokens each, frames via "
+                                                  "Router + Batcher (host buffers)"}
+            del bq, router, srv_k
+    return out
+
+
 def server_batch_sweep(sfg, eng, cfg, nl, rank, rounds=6):
     """Server-side step time for K sessions' queued lookahead steps (r rows
     each, row 0 + r-1 draft branches, keep=[0] of the previous step): frames
@@ -571,6 +609,7 @@ def main():
                     help="KV context before the first step (configs[4]: 2048)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--quick-sweep", action="store_true", help="concurrent-session sweep at the bench context only")
     args = ap.parse_args()
     MODEL = MODELS[args.model]
     PROMPT_LEN = args.prompt_len

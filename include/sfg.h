@@ -189,6 +189,39 @@ void sfg_server_set_clock(sfg_server* s, double (*now_s)(void* ctx), void* ctx);
 typedef int32_t (*sfg_frame_handler)(void* ctx, const uint8_t* req, size_t req_len,
                                      const uint8_t** resp, size_t* resp_len);
 
+/* ── multi-device serving front end ─────────────────
+ * The reference binds ONE ServerEngine behind a FrameServer that runs a
+ * thread per connection (transport.cpp:531, :565-581).  A router is the
+ * FrameHandler over one server per device (or any frame handlers): a
+ * session is placed on the least-loaded backend when its prompt frame
+ * arrives and stays there (sticky); frames of an unplaced session get the
+ * server's "session: unknown or expired session" error frame.  No
+ * cross-device state, no collective on the data path.                      */
+typedef struct sfg_router sfg_router;
+int32_t sfg_router_create(sfg_server* const* servers, int32_t n, double session_expiry_s, sfg_router** out);
+int32_t sfg_router_create_handlers(const sfg_frame_handler* fns, void* const* ctxs, int32_t n,
+                                   double session_expiry_s, sfg_router** out);
+void sfg_router_destroy(sfg_router* r);
+/* FrameHandler (thread safe); *resp as for sfg_server_handle               */
+int32_t sfg_router_handle(sfg_router* r, const uint8_t* req, size_t req_len, const uint8_t** resp,
+                          size_t* resp_len);
+/* backend index of a session, -1 if not placed                             */
+int32_t sfg_router_session_device(sfg_router* r, const char* session_id);
+/* sessions placed per backend into sessions[0..n); returns n              */
+int32_t sfg_router_load(sfg_router* r, int32_t* sessions);
+void sfg_router_set_clock(sfg_router* r, double (*now_s)(void* ctx), void* ctx);
+/* Cross-session batching queue: a FrameHandler for many concurrent
+ * connection threads.  Frames queue per backend; one worker per backend
+ * drains whatever is queued through sfg_server_handle_batch (steps of
+ * distinct sessions share one weight pass; each response is the one
+ * handle() gives).  A call blocks until its own response is ready.        */
+typedef struct sfg_batcher sfg_batcher;
+int32_t sfg_batcher_create(sfg_router* r, int32_t max_frames /* 0: unlimited */, sfg_batcher** out);
+void sfg_batcher_destroy(sfg_batcher* b);
+int32_t sfg_batcher_handle(sfg_batcher* b, const uint8_t* req, size_t req_len, const uint8_t** resp,
+                           size_t* resp_len);
+void sfg_batcher_stats(sfg_batcher* b, uint64_t* batches, uint64_t* frames, uint64_t* max_batch);
+
 typedef struct {
     int32_t prefix_layers;     /* SplitConfig (client.hpp:14-20) */
     int32_t suffix_layers;

@@ -127,6 +127,19 @@ def lib() -> C.CDLL:
         "sfg_server_session_count": (C.c_size_t, [vp]),
         "sfg_server_session_view": (i32, [vp, C.c_char_p, i32p, i32p, i32p]),
         "sfg_server_set_clock": (None, [vp, C.CFUNCTYPE(C.c_double, C.c_void_p), vp]),
+        "sfg_router_create": (i32, [C.POINTER(vp), i32, C.c_double, C.POINTER(vp)]),
+        "sfg_router_create_handlers": (i32, [C.POINTER(vp), C.POINTER(vp), i32, C.c_double, C.POINTER(vp)]),
+        "sfg_router_destroy": (None, [vp]),
+        "sfg_router_handle": (i32, [vp, C.POINTER(C.c_uint8), C.c_size_t, C.POINTER(C.POINTER(C.c_uint8)),
+                                    C.POINTER(C.c_size_t)]),
+        "sfg_router_session_device": (i32, [vp, C.c_char_p]),
+        "sfg_router_load": (i32, [vp, i32p]),
+        "sfg_router_set_clock": (None, [vp, C.CFUNCTYPE(C.c_double, C.c_void_p), vp]),
+        "sfg_batcher_create": (i32, [vp, i32, C.POINTER(vp)]),
+        "sfg_batcher_destroy": (None, [vp]),
+        "sfg_batcher_handle": (i32, [vp, C.POINTER(C.c_uint8), C.c_size_t, C.POINTER(C.POINTER(C.c_uint8)),
+                                     C.POINTER(C.c_size_t)]),
+        "sfg_batcher_stats": (None, [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "sfg_client_create": (i32, [vp, C.POINTER(ClientConfig), vp, vp, C.c_char_p, C.POINTER(vp)]),
         "sfg_client_create_linked": (i32, [vp, C.POINTER(ClientConfig), vp, C.c_char_p, C.POINTER(vp)]),
         "sfg_client_destroy": (None, [vp]),

@@ -8,6 +8,7 @@
 #include "sfg_client.h"
 #include "sfg_engine.h"
 #include "sfg_prof.h"
+#include "sfg_router.h"
 #include "sfg_server.h"
 #include "sfg_wire.h"
 
@@ -42,6 +43,8 @@ struct sfg_bank { std::unique_ptr<Bank> b; sfg_engine* eng; };
 struct sfg_server { std::unique_ptr<Server> s; double (*clock)(void*) = nullptr; void* clock_ctx = nullptr; };
 struct sfg_client { std::unique_ptr<Client> c; };
 struct sfg_pool { std::unique_ptr<Pool> p; };
+struct sfg_router { std::unique_ptr<Router> r; double (*clock)(void*) = nullptr; void* clock_ctx = nullptr; };
+struct sfg_batcher { std::unique_ptr<Batcher> b; };
 
 extern "C" {
 
@@ -180,6 +183,74 @@ int32_t sfg_server_session_view(sfg_server* s, const char* sid, int32_t* len, in
     *prov = c;
     return 1;
 }
+// ── router / batching queue (sfg_router.h) ─────────────────────────────
+int32_t sfg_router_create(sfg_server* const* servers, int32_t n, double session_expiry_s, sfg_router** out) {
+    SFG_GUARD({
+        if (n < 1 || !servers) throw sfg::Error(sfg::Kind::config, "router needs at least one backend");
+        std::vector<Backend> bs(static_cast<size_t>(n));
+        for (int32_t i = 0; i < n; ++i) {
+            if (!servers[i]) throw sfg::Error(sfg::Kind::config, "null server");
+            bs[i].server = servers[i]->s.get();
+        }
+        auto r = std::make_unique<sfg_router>();
+        r->r = std::make_unique<Router>(std::move(bs), session_expiry_s);
+        *out = r.release();
+    })
+}
+int32_t sfg_router_create_handlers(const sfg_frame_handler* fns, void* const* ctxs, int32_t n, double session_expiry_s,
+                                   sfg_router** out) {
+    SFG_GUARD({
+        if (n < 1 || !fns) throw sfg::Error(sfg::Kind::config, "router needs at least one backend");
+        std::vector<Backend> bs(static_cast<size_t>(n));
+        for (int32_t i = 0; i < n; ++i) {
+            bs[i].fn = fns[i];
+            bs[i].ctx = ctxs ? ctxs[i] : nullptr;
+        }
+        auto r = std::make_unique<sfg_router>();
+        r->r = std::make_unique<Router>(std::move(bs), session_expiry_s);
+        *out = r.release();
+    })
+}
+void sfg_router_destroy(sfg_router* r) { delete r; }
+int32_t sfg_router_handle(sfg_router* r, const uint8_t* req, size_t n, const uint8_t** resp, size_t* resp_len) {
+    SFG_GUARD({
+        r->r->handle(req, n, g_resp);
+        *resp = g_resp.data();
+        *resp_len = g_resp.size();
+    })
+}
+int32_t sfg_router_session_device(sfg_router* r, const char* session_id) { return r->r->device_of(session_id); }
+int32_t sfg_router_load(sfg_router* r, int32_t* sessions) {
+    const std::vector<int> l = r->r->load();
+    for (size_t i = 0; i < l.size(); ++i) sessions[i] = l[i];
+    return static_cast<int32_t>(l.size());
+}
+void sfg_router_set_clock(sfg_router* r, double (*now_s)(void*), void* ctx) {
+    r->clock = now_s;
+    r->clock_ctx = ctx;
+    r->r->set_clock([r] { return r->clock(r->clock_ctx); });
+}
+int32_t sfg_batcher_create(sfg_router* r, int32_t max_frames, sfg_batcher** out) {
+    SFG_GUARD({
+        auto b = std::make_unique<sfg_batcher>();
+        b->b = std::make_unique<Batcher>(*r->r, max_frames);
+        *out = b.release();
+    })
+}
+void sfg_batcher_destroy(sfg_batcher* b) { delete b; }
+int32_t sfg_batcher_handle(sfg_batcher* b, const uint8_t* req, size_t n, const uint8_t** resp, size_t* resp_len) {
+    SFG_GUARD({
+        b->b->handle(req, n, g_resp);
+        *resp = g_resp.data();
+        *resp_len = g_resp.size();
+    })
+}
+void sfg_batcher_stats(sfg_batcher* b, uint64_t* batches, uint64_t* frames, uint64_t* max_batch) {
+    if (batches) *batches = b->b->batches();
+    if (frames) *frames = b->b->frames();
+    if (max_batch) *max_batch = b->b->max_batch();
+}
+
 void sfg_server_set_clock(sfg_server* s, double (*now_s)(void*), void* ctx) {
     s->clock = now_s;
     s->clock_ctx = ctx;

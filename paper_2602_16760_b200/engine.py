@@ -280,6 +280,88 @@ class ServerEngine:
         _lib.lib().sfg_server_set_clock(self.h, cb, None)
 
 
+def _handle_bytes(fn, h, frame: bytes) -> bytes:
+    buf = (C.c_uint8 * len(frame)).from_buffer_copy(frame)
+    rp = C.POINTER(C.c_uint8)()
+    rn = C.c_size_t()
+    check(fn(h, buf, len(frame), C.byref(rp), C.byref(rn)))
+    return C.string_at(rp, rn.value)
+
+
+class Router:
+    """Frame router over one ServerEngine per device (or any frame handlers):
+    sessions are placed on the least-loaded backend at their prompt frame and
+    stay there (sfg.h sfg_router_*).  ``backends`` are ServerEngines or
+    (C function pointer, ctx) handler pairs."""
+
+    def __init__(self, backends, session_expiry_s: float = 300.0):
+        L = _lib.lib()
+        h = C.c_void_p()
+        n = len(backends)
+        if all(isinstance(b, ServerEngine) for b in backends):
+            arr = (C.c_void_p * n)(*[b.h.value for b in backends])
+            check(L.sfg_router_create(arr, n, session_expiry_s, C.byref(h)))
+        else:
+            fns = (C.c_void_p * n)(*[C.cast(b[0], C.c_void_p).value for b in backends])
+            ctxs = (C.c_void_p * n)(*[b[1] for b in backends])
+            check(L.sfg_router_create_handlers(fns, ctxs, n, session_expiry_s, C.byref(h)))
+        self.h, self._backends, self._clock_cb = h, backends, None
+
+    def __del__(self):
+        try:
+            _lib.lib().sfg_router_destroy(self.h)
+        except Exception:
+            pass
+
+    def handle(self, frame: bytes) -> bytes:
+        return _handle_bytes(_lib.lib().sfg_router_handle, self.h, frame)
+
+    @property
+    def handler(self):
+        return C.cast(_lib.lib().sfg_router_handle, C.c_void_p), self.h
+
+    def session_device(self, sid: str) -> int:
+        return int(_lib.lib().sfg_router_session_device(self.h, sid.encode()))
+
+    def load(self) -> list:
+        out = (C.c_int32 * len(self._backends))()
+        n = _lib.lib().sfg_router_load(self.h, out)
+        return list(out[:n])
+
+    def set_clock(self, now_s):
+        cb = C.CFUNCTYPE(C.c_double, C.c_void_p)(lambda _ctx: float(now_s()))
+        self._clock_cb = cb
+        _lib.lib().sfg_router_set_clock(self.h, cb, None)
+
+
+class Batcher:
+    """Cross-session batching queue in front of a Router: a FrameHandler for
+    concurrent connection threads (sfg.h sfg_batcher_*)."""
+
+    def __init__(self, router: Router, max_frames: int = 0):
+        h = C.c_void_p()
+        check(_lib.lib().sfg_batcher_create(router.h, max_frames, C.byref(h)))
+        self.h, self.router = h, router
+
+    def __del__(self):
+        try:
+            _lib.lib().sfg_batcher_destroy(self.h)
+        except Exception:
+            pass
+
+    def handle(self, frame: bytes) -> bytes:
+        return _handle_bytes(_lib.lib().sfg_batcher_handle, self.h, frame)
+
+    @property
+    def handler(self):
+        return C.cast(_lib.lib().sfg_batcher_handle, C.c_void_p), self.h
+
+    def stats(self) -> dict:
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _lib.lib().sfg_batcher_stats(self.h, C.byref(a), C.byref(b), C.byref(c))
+        return {"batches": a.value, "frames": b.value, "max_batch": c.value}
+
+
 @dataclass
 class SplitConfig:
     """splitf::SplitConfig (client.hpp:14-20) + the SimChannel one-way delay."""
