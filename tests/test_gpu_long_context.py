@@ -166,3 +166,43 @@ def test_7b_width_layer_prior_512_chunked_attention(ref):
                         "::test_7b_width_layer_prior_512_chunked_attention"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("math", ["exact", "fast"])
+def test_long_keep_list_compaction_equals_oracle(port, math):
+    """CacheBank::resolve with a keep list longer than one 64-row compaction
+    chunk (tinyformer.cpp:282-308): 150 kept entries of a 200-row provisional
+    tail, each moved down by its own offset.  Every kept K/V entry equals the
+    oracle's (bitwise in EXACT math, where the cached values themselves are
+    bitwise), and the next step over the compacted cache stays in tolerance."""
+    cfg = po.tiny_cfg()
+    m = port.model(cfg, bf16=True)
+    eng = sfg.Engine(sfg.ModelConfig(**{k: getattr(cfg, k) for k in po.ModelCfg.__dataclass_fields__}),
+                     math=sfg.EXACT if math == "exact" else sfg.FAST, params=m.params())
+    lb, le = 1, 3
+    bo, bg = m.bank(lb, le), eng.bank(lb, le)
+    rng = np.random.default_rng(8)
+    h = (rng.standard_normal((40, cfg.hidden_dim)) * 0.5).astype(np.float32)
+    bo.forward(lb, le, h, list(range(40)))
+    eng.forward_layers(lb, le, h, list(range(40)), bg)
+    bo.mark_committed(40)
+    bg.mark_committed(40)
+    t = (rng.standard_normal((200, cfg.hidden_dim)) * 0.5).astype(np.float32)
+    bo.forward(lb, le, t, list(range(40, 240)))
+    eng.forward_layers(lb, le, t, list(range(40, 240)), bg)
+    keep = sorted(rng.choice(200, size=150, replace=False).tolist())
+    bo.resolve(keep)
+    bg.resolve(keep)
+    assert bo.state() == (190, 190) and (bg.len(), bg.committed_len()) == (190, 190)
+    for layer in (lb, le - 1):
+        for pos in list(range(38, 42)) + [100, 150, 188, 189]:
+            kg, vg = bg.kv(layer, cfg.n_kv_heads - 1, pos)
+            ko, vo = bo.kv(layer, cfg.n_kv_heads - 1, pos)
+            if math == "exact":
+                assert np.array_equal(kg, ko) and np.array_equal(vg, vo), (layer, pos)
+            else:
+                assert rel(kg[None], ko[None]) <= TOL and rel(vg[None], vo[None]) <= TOL, (layer, pos)
+    x = (rng.standard_normal((3, cfg.hidden_dim)) * 0.5).astype(np.float32)
+    a = bo.forward(lb, le, x, [190, 191, 192])
+    b = eng.forward_layers(lb, le, x, [190, 191, 192], bg)
+    assert (np.array_equal(a, b) if math == "exact" else rel(b, a) <= TOL)
