@@ -203,7 +203,9 @@ def ncu_traffic(args):
     dominant kernel (profiles/r01_ncu_full_mega_summary.csv: one 28-layer
     server launch of the megakernel), next to that launch's algorithmic bytes."""
     import csv
-    path = os.path.join(ROOT, "profiles", "r01_ncu_full_mega_summary.csv")
+    import glob
+    caps = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_mega_summary.csv")))
+    path = caps[-1] if caps else os.path.join(ROOT, "profiles", "r01_ncu_full_mega_summary.csv")
     try:
         rows = list(csv.reader(open(path)))
         h, u, v = rows[0], rows[1], rows[2]
@@ -215,7 +217,7 @@ def ncu_traffic(args):
         m = MODEL
         H, qd, kvd, F = m["hidden_dim"], m["n_heads"] * m["head_dim"], m["n_kv_heads"] * m["head_dim"], m["ffn_dim"]
         layer = 2 * (H * (qd + 2 * kvd) + qd * H + 3 * H * F)
-        return {"traffic": rd + wr, "traffic_launch": "one 28-layer server launch (ncu --set full)",
+        return {"traffic": rd + wr, "traffic_launch": f"one 28-layer server launch (ncu --set full, {os.path.basename(path)})",
                 "traffic_launch_algorithmic_bytes": 28 * layer}
     except Exception:
         return {"traffic": None}
