@@ -153,6 +153,7 @@ def cpu_sample(threads: int, ctx: int, rows: int = 16):
     if po.ref_available():
         lib, kind = po.Ref(), "reference"
         m = lib.timing_model(cfg, (2, 3), False)
+        lib.lib.ref_time_forward(m.h, 2, 3, 1, ctx, threads)  # page the fresh weights in (first touch)
         t_layer = lib.lib.ref_time_forward(m.h, 2, 3, rows, ctx, threads)
         return {"kind": kind, "t_layer_s": t_layer, "model": m, "lib": lib}
     raise RuntimeError("oracle/_ref not built")
@@ -163,6 +164,7 @@ def cpu_head_time(lib, threads: int) -> float:
     import pyoracle as po
     cfg = po.ModelCfg(**MODEL)
     mh = lib.timing_model(cfg, (0, 0), True)
+    lib.lib.ref_time_finalize(mh.h, 1, threads)  # first touch
     return lib.lib.ref_time_finalize(mh.h, 1, threads)
 
 

@@ -170,8 +170,10 @@ int32_t sfg_server_handle(sfg_server* s, const uint8_t* req, size_t req_len, con
                           size_t* resp_len);
 /* handle() over n frames, in order, with the same responses handle() gives
  * frame by frame.  Step frames of distinct sessions whose rows fit one pass
- * (<= 16 rows total, masks within the layer-stack contract) share ONE weight
- * pass: cross-session batching of concurrent decoders.
+ * (<= 32 rows total, <= 16 per session, masks within the layer-stack
+ * contract) share ONE weight pass: cross-session batching of concurrent
+ * decoders; two sessions' full 16-row lookahead batches
+ * share a pass.
  * resps[i] point into thread-local buffers valid until the next call.
  * Replaces a loop of ServerEngine::handle (server.hpp:49) over the frames a
  * transport has queued.                                                     */

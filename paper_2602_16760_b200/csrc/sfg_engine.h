@@ -338,6 +338,8 @@ float* fast_partials(const ModelCfg& c, Workspace& ws);
 int* fast_counters(const ModelCfg& c, Workspace& ws);
 // FAST layer-stack megakernel (sfg_mega.cu)
 bool mega_supported(const Engine& e, int rows, bool additive_mask);
+// rows of one cross-session layer-stack pass (32, or 16 where unsupported)
+int mega_batch_rows(const Engine& e);
 // banks/rowinfo (optional): rows of several sessions in one pass -- row r
 // appends to (*banks)[rowinfo[3r]] at slot rowinfo[3r+1] and sees
 // rowinfo[3r+2] cached keys; b supplies the launch state (same layer range)

@@ -52,6 +52,12 @@ constexpr int kTmemCols = 128;
 constexpr int kMaxPieces = 16;
 constexpr int kMaxGroup = 8;
 constexpr int kMaxBanks = 16;  // sessions per launch (one row each at least)
+// Rows per launch: R = 16 (one session's lookahead batch) or 32 (several
+// sessions' batches in one weight pass).  The MMA N is 3R (hi | mid | lo bf16
+// pieces of every row) and costs the same for N = 48 and N = 96 (it is issue
+// bound below N = 128, tools/mb_ring.cu), so a 32-row pass streams the same
+// weights with the same tensor-core time; epilogues work in 16-row blocks.
+constexpr int kMaxRows = 32;
 enum Phase : int { P_QKV = 0, P_O = 1, P_GU = 2, P_DOWN = 3 };
 
 struct LayerDesc {
@@ -66,6 +72,12 @@ struct LayerDesc {
 struct MegaArgs {
     const LayerDesc* layers;
     int nlayers, rows, stages;
+    int R;             // row capacity of this launch (16 or 32): image / partial / sum-of-squares row stride
+    int stage_bytes;   // kABytes + xbytes
+    int xbytes;        // one k-block of the activation image: 3R rows x 64 bf16
+    int acc_cols;      // TMEM columns per accumulator (>= 3R)
+    int tmem_cols;     // TMEM columns allocated (2 accumulators)
+    uint32_t idesc;    // kind::f16 instruction descriptor, N = 3R
     int H, qd, kvd, F, hd, n_heads, n_kv, max_len;
     float eps;
     float* h;        // [16][H] residual stream, in/out
@@ -310,6 +322,19 @@ __device__ __forceinline__ bool xblock_ready(const MegaArgs& a, int l, int p, in
     }
 }
 
+// kind::f16 MMA with a runtime instruction descriptor (N = 3R of the launch)
+__device__ __forceinline__ void mma_bf16_id(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+
 // bounded mbarrier wait (traps instead of hanging on a protocol bug)
 __device__ __forceinline__ void mwait(uint64_t* b, uint32_t parity) {
     uint32_t done = 0;
@@ -360,16 +385,16 @@ __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence
 // feature k, row r of a phase's global activation image: [KB][48 x 64] bf16
 // K-major SW128 blocks, the exact smem layout the MMA reads, so a stage's
 // activations arrive with one 6 KB bulk copy.
-__device__ __forceinline__ void put_split(uint8_t* img, int k, int r, float x) {
-    uint8_t* blk = img + static_cast<size_t>(k >> 6) * kBBytes;
+__device__ __forceinline__ void put_split(uint8_t* img, int k, int r, float x, int R) {
+    uint8_t* blk = img + static_cast<size_t>(k >> 6) * (static_cast<size_t>(R) * 384);
     const int kk = k & 63;
     const __nv_bfloat16 hb = __float2bfloat16_rn(x);
     const float r1 = x - __bfloat162float(hb);
     const __nv_bfloat16 mb = __float2bfloat16_rn(r1);
     const __nv_bfloat16 lb = __float2bfloat16_rn(r1 - __bfloat162float(mb));
     *reinterpret_cast<__nv_bfloat16*>(blk + sw128_off(r, kk)) = hb;
-    *reinterpret_cast<__nv_bfloat16*>(blk + sw128_off(kRows + r, kk)) = mb;
-    *reinterpret_cast<__nv_bfloat16*>(blk + sw128_off(2 * kRows + r, kk)) = lb;
+    *reinterpret_cast<__nv_bfloat16*>(blk + sw128_off(R + r, kk)) = mb;
+    *reinterpret_cast<__nv_bfloat16*>(blk + sw128_off(2 * R + r, kk)) = lb;
 }
 
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
@@ -385,14 +410,14 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // per-launch constants staged in shared memory at kernel entry (the layer
 // table too: the epilogue dereferences it on the critical path of every tile)
 constexpr int kMaxMegaLayers = 64;
-__shared__ int sh_pos[kRows];
+__shared__ int sh_pos[kMaxRows];
 __shared__ int sh_prior;
-__shared__ int sh_row_bank[kRows], sh_row_slot[kRows], sh_row_prior[kRows];
+__shared__ int sh_row_bank[kMaxRows], sh_row_slot[kMaxRows], sh_row_prior[kMaxRows];
 __shared__ LayerDesc sh_layers[kMaxMegaLayers];
 // per row: compacted visible-key count and its tail slots (columns >= prior)
-__shared__ int sh_ncols[kRows];
+__shared__ int sh_ncols[kMaxRows];
 __shared__ unsigned sh_epoch;
-__shared__ int sh_tail[kRows][kRows];
+__shared__ int sh_tail[kMaxRows][kRows];  // a row's own tail slots (<= 16 per session)
 
 // ── epilogues (thread = feature m of the tile; y[r] for 16 rows) ─────────
 // RMSNorm is split across the two sides of the GEMM: the producing epilogue
@@ -413,12 +438,13 @@ __device__ __forceinline__ float ld_relaxed_sys(const float* p) {
     return v;
 }
 
+// rows rb .. rb+15 of the launch (one 16-row block of its R rows)
 __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, int tile, int m, int et,
                           const float (&yin)[kRows], float* xch, const float* rs, const float* ropeT,
-                          const float* hpre) {
+                          const float* hpre, int rb) {
     float y[kRows];
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) y[r] = (p == P_QKV || p == P_GU) ? yin[r] * rs[r] : yin[r];
+    for (int r = 0; r < kRows; ++r) y[r] = (p == P_QKV || p == P_GU) ? yin[r] * rs[rb + r] : yin[r];
     if (p == P_QKV) {
         const int f = tile * kM + m;
         const bool valid = f < a.qd + 2 * a.kvd;
@@ -426,17 +452,27 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
         const int fl = seg == 0 ? f : (seg == 1 ? f - a.qd : f - a.qd - a.kvd);
         const int d = fl % a.hd, half = a.hd >> 1, i = d >> 1;
         const bool odd = (m & 1) != 0;
-        // the rows' cos/sin were staged in shared memory at kernel entry
+        // the rows' cos/sin: staged in shared memory at kernel entry for
+        // 16-row launches, read from the (L2-resident) host-libm tables otherwise
         float cs[kRows], sn[kRows];
+        if (a.R == kRows) {
 #pragma unroll
-        for (int r = 0; r < kRows; ++r) {
-            cs[r] = ropeT[r * a.hd + i];
-            sn[r] = ropeT[r * a.hd + half + i];
+            for (int r = 0; r < kRows; ++r) {
+                cs[r] = ropeT[r * a.hd + i];
+                sn[r] = ropeT[r * a.hd + half + i];
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < kRows; ++r) {
+                const size_t o = static_cast<size_t>(rb + r < a.rows ? sh_pos[rb + r] : 0) * half + i;
+                cs[r] = __ldg(a.rope_cos + o);
+                sn[r] = __ldg(a.rope_sin + o);
+            }
         }
 #pragma unroll
         for (int r = 0; r < kRows; ++r) {
             const float partner = __shfl_xor_sync(0xffffffffu, y[r], 1);
-            if (!valid || r >= a.rows) continue;
+            if (!valid || rb + r >= a.rows) continue;
             float v = y[r];
             if (seg != 2) {
                 const float c = cs[r], s = sn[r];
@@ -444,11 +480,11 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
                         : __fsub_rn(__fmul_rn(v, c), __fmul_rn(partner, s));
             }
             if (seg == 0) {
-                a.q[static_cast<size_t>(r) * a.qd + fl] = v;
+                a.q[static_cast<size_t>(rb + r) * a.qd + fl] = v;
             } else {
-                const int b = sh_row_bank[r];
+                const int b = sh_row_bank[rb + r];
                 float* dst = (seg == 1 ? a.kbank[b] : a.vbank[b]) + static_cast<size_t>(l) * a.slab_stride +
-                             (static_cast<size_t>(fl / a.hd) * a.max_len + sh_row_slot[r]) * a.hd + d;
+                             (static_cast<size_t>(fl / a.hd) * a.max_len + sh_row_slot[rb + r]) * a.hd + d;
                 *dst = v;
             }
         }
@@ -463,12 +499,12 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
             if (fg < a.F)
 #pragma unroll
                 for (int r = 0; r < kRows; ++r)
-                    if (r < a.rows) {
+                    if (rb + r < a.rows) {
                         const float g = y[r];
                         const float silu = g / (1.0f + expf(-g));
                         const float v = silu * ub[m * kRows + r];
-                        a.act[static_cast<size_t>(r) * a.F + fg] = v;
-                        put_split(a.xim[P_DOWN], fg, r, v);
+                        a.act[static_cast<size_t>(rb + r) * a.F + fg] = v;
+                        put_split(a.xim[P_DOWN], fg, rb + r, v, a.R);
                     }
         }
         named_sync(1, 128);
@@ -506,23 +542,23 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
         const float* gn = p == P_O ? L.ffn_norm : L.next_attn_norm;
         uint8_t* img = p == P_O ? a.xim[P_GU] : a.xim[P_QKV];
         cp_async_wait_all();
-        const float gf = (gn && f < a.H) ? hpre[kRows * kM + m] : 0.0f;  // prefetched with the residual
+        const float gf = (gn && f < a.H) ? hpre[a.R * kM + m] : 0.0f;  // prefetched with the residual
         // residual rows were prefetched into shared memory (cp.async) while
         // the accumulator was still being produced
         cp_async_wait_all();
         if (a.trace && et == 0) *tslot(a, blockIdx.x, input_barrier(l, p), 12) = gtimer();
         float hn[kRows];
 #pragma unroll
-        for (int r = 0; r < kRows; ++r) hn[r] = (f < a.H && r < a.rows) ? hpre[r * kM + m] : 0.0f;
+        for (int r = 0; r < kRows; ++r) hn[r] = (f < a.H && rb + r < a.rows) ? hpre[(rb + r) * kM + m] : 0.0f;
 #pragma unroll
         for (int r = 0; r < kRows; ++r) {
-            if (f < a.H && r < a.rows) {
+            if (f < a.H && rb + r < a.rows) {
                 hn[r] += y[r];
-                a.h[static_cast<size_t>(r) * a.H + f] = hn[r];
-                if (gn) put_split(img, f, r, hn[r] * gf);
+                a.h[static_cast<size_t>(rb + r) * a.H + f] = hn[r];
+                if (gn) put_split(img, f, rb + r, hn[r] * gf, a.R);
             }
         }
-        float* ss = (p == P_O ? a.ss_o : a.ss_d) + static_cast<size_t>(tile) * kRows;
+        float* ss = (p == P_O ? a.ss_o : a.ss_d) + static_cast<size_t>(tile) * a.R + rb;
         if (a.trace && et == 0) *tslot(a, blockIdx.x, input_barrier(l, p), 13) = gtimer();
         tile_sumsq(hn, xch + 64 * kRows, ss, et);
         if (a.trace && et == 0) *tslot(a, blockIdx.x, input_barrier(l, p), 14) = gtimer();
@@ -650,7 +686,7 @@ __device__ void attention_row_item(const MegaArgs& a, const LayerDesc& L, int l,
         const int f = (kvh * group + g) * HD + dd;
         const float o = acc / l;
         a.att[static_cast<size_t>(row) * a.qd + f] = o;
-        put_split(a.xim[P_O], f, row, o);
+        put_split(a.xim[P_O], f, row, o, a.R);
     }
     fence_proxy_async_global();
     named_sync(3, 256);
@@ -896,7 +932,7 @@ __device__ __noinline__ void attention_chunk(const MegaArgs& a, const LayerDesc&
             const float val = ov[dd] / lsum;
             const int f = (kvh * group + g) * HD + d;
             a.att[static_cast<size_t>(r) * a.qd + f] = val;
-            put_split(a.xim[P_O], f, r, val);
+            put_split(a.xim[P_O], f, r, val, a.R);
         }
     };
     if (a.trace && at == 0) *tslot(a, blockIdx.x, 5 * l + 2, 13) = gtimer();
@@ -1073,30 +1109,31 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = a.stages;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * kStageBytes);
+    const int SB = a.stage_bytes;  // [16 KB weights | 3R x 64 activation image] per stage
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * SB);
     uint64_t* empty = full + kMaxStages;
     uint64_t* tfull = empty + kMaxStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     int* flag = reinterpret_cast<int*>(tmem_slot + 4);
     float* xch = reinterpret_cast<float*>(flag + 4);          // 64*16 gate|up + 4*16 sumsq
-    float* rs = xch + 64 * kRows + 4 * kRows;                  // [16] per-row 1/rms of the phase
+    float* rs = xch + 64 * kRows + 4 * kRows;                  // [kMaxRows] per-row 1/rms of the phase
     // attention scratch, one of two layouts (MegaArgs::attn_rows):
-    float* sq = rs + kRows;                                    // chunked: [32 queries][hd] queries
+    float* sq = rs + kMaxRows;                                 // chunked: [32 queries][hd] queries
     float* sp = sq + 32 * a.hd;                                //   [8 warps][4][kKeyBlock] probabilities
     float* skv = sp + 8 * 4 * kKeyBlock;                       //   2 staged K | V blocks + tail slots
-    float* qs = rs + kRows;                                    // per-row: [group][hd] queries
+    float* qs = rs + kMaxRows;                                 // per-row: [group][hd] queries
     float* wst = qs + kMaxGroup * a.hd;                        //   [8][kMaxGroup][2] warp stats
     float* ocomb = wst + 8 * kMaxGroup * 2;                    //   [8][group][hd] warp partials
     int* cols = reinterpret_cast<int*>(ocomb + 8 * (a.n_heads / a.n_kv) * a.hd);  //   [max_len]
-    float* ropeT = rs + kRows + attn_scratch_floats(kRowsAttn, a.hd, a.n_heads / a.n_kv, a.max_len);  // [16][hd] cos | sin
-    float* hpre = ropeT + kRows * a.hd;                         // [16][128] residual prefetch
+    float* ropeT = rs + kMaxRows + attn_scratch_floats(kRowsAttn, a.hd, a.n_heads / a.n_kv, a.max_len);  // [16][hd] cos | sin (R = 16)
+    float* hpre = ropeT + (a.R == kRows ? kRows * a.hd : 0);    // [R][128] residual prefetch + gain row
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = gridDim.x, c = blockIdx.x;
     if (threadIdx.x == 0 && a.trace) *tslot(a, c, kBarSlots - 1, 0) = gtimer();
-    if (threadIdx.x < kRows) sh_pos[threadIdx.x] = static_cast<int>(threadIdx.x) < a.rows ? a.pos[threadIdx.x] : 0;
-    for (int i = threadIdx.x; i < kRows * a.hd; i += blockDim.x) {  // RoPE table rows (host-libm values)
+    if (threadIdx.x < kMaxRows) sh_pos[threadIdx.x] = static_cast<int>(threadIdx.x) < a.rows ? a.pos[threadIdx.x] : 0;
+    for (int i = threadIdx.x; a.R == kRows && i < kRows * a.hd; i += blockDim.x) {  // RoPE table rows (host-libm values)
         const int r = i / a.hd, j = i % a.hd, half = a.hd >> 1;
         float v = j < half ? 1.0f : 0.0f;
         if (r < a.rows) {
@@ -1108,7 +1145,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
     if (threadIdx.x == 0) sh_prior = *a.prior;
     if (threadIdx.x == 0) sh_epoch = a.tp > 1 ? *a.epoch_ptr + 1u : 0u;
     for (int i = threadIdx.x; i < a.nlayers; i += blockDim.x) sh_layers[i] = a.layers[i];
-    if (threadIdx.x < kRows) {  // per-row cache, slot and compacted key list (mega_mask_ok)
+    if (threadIdx.x < kMaxRows) {  // per-row cache, slot and compacted key list (mega_mask_ok)
         const int r = threadIdx.x;
         int prior = *a.prior, bank = 0, slot = prior + r;
         if (a.rowinfo && r < a.rows) {
@@ -1145,7 +1182,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+    if (warp == 1) tmem_alloc(tmem_slot, a.tmem_cols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -1207,7 +1244,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         } else {
                             mbar_expect_tx(&full[stage], n * kABytes);
                             for (int h = 0; h < n; ++h) {
-                                uint8_t* dst = smem + (2 * stage + h) * kStageBytes;
+                                uint8_t* dst = smem + (2 * stage + h) * SB;
                                 const uint8_t* src = W + static_cast<size_t>(u + h) * kABytes;
                                 if (a.evict_first)
                                     bulk_g2s_stream(dst, src, kABytes, &full[stage], pol);
@@ -1261,11 +1298,11 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                             }
                             tc_fence_after();
                         }
-                        const uint32_t sa = ring0 + static_cast<uint32_t>((2 * stage + half) * kStageBytes);
+                        const uint32_t sa = ring0 + static_cast<uint32_t>((2 * stage + half) * SB);
                         const uint64_t da = smem_desc(sa), db = smem_desc(sa + kABytes);
-                        const uint32_t d = tmem + acc * kAccCols;
+                        const uint32_t d = tmem + acc * a.acc_cols;
 #pragma unroll
-                        for (int k = 0; k < kKB / 16; ++k) mma_bf16(d, da + 2 * k, db + 2 * k, (kb > lo || k > 0) ? 1u : 0u);
+                        for (int k = 0; k < kKB / 16; ++k) mma_bf16_id(d, da + 2 * k, db + 2 * k, a.idesc, (kb > lo || k > 0) ? 1u : 0u);
                         if (half == 1 || u + 1 == en) {  // the pair is consumed: release it
                             mma_commit(&empty[stage]);
                             if (++stage == NP) {
@@ -1299,13 +1336,16 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
         for (int t = c; t < tilesH; t += G) {
             const int f = t * kM + m;
             const float gf = f < a.H ? __ldg(sh_layers[0].attn_norm + f) : 0.0f;
-            float hv[kRows];
+            for (int rb = 0; rb < a.R; rb += kRows) {  // 16-row blocks (every block: the ss rows of padding are 0)
+                float hv[kRows];
 #pragma unroll
-            for (int r = 0; r < kRows; ++r) {
-                hv[r] = (f < a.H && r < a.rows) ? __ldcg(a.h + static_cast<size_t>(r) * a.H + f) : 0.0f;
-                if (f < a.H && r < a.rows) put_split(a.xim[P_QKV], f, r, hv[r] * gf);
+                for (int r = 0; r < kRows; ++r) {
+                    const bool ok = f < a.H && rb + r < a.rows;
+                    hv[r] = ok ? __ldcg(a.h + static_cast<size_t>(rb + r) * a.H + f) : 0.0f;
+                    if (ok) put_split(a.xim[P_QKV], f, rb + r, hv[r] * gf, a.R);
+                }
+                tile_sumsq(hv, xch + 64 * kRows, a.ss_d + static_cast<size_t>(t) * a.R + rb, et);
             }
-            tile_sumsq(hv, xch + 64 * kRows, a.ss_d + static_cast<size_t>(t) * kRows, et);
             fence_proxy_async_global();
             named_sync(1, 128);
             if (et == 0) {
@@ -1336,21 +1376,23 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                                            : fptr(a, l, K_O, tilesH),
                                 static_cast<unsigned>(tilesH));
                     named_sync(1, 128);
-                    {  // 8 threads per row, loads in flight together, fixed-order combine
-                        const float* ssb = p == P_QKV ? a.ss_d : a.ss_o;
-                        const int r = et & 15, j = et >> 4;
-                        float part = 0.0f;
-                        for (int t = j; t < tilesH; t += 8) part += __ldcg(ssb + t * kRows + r);
-                        xch[j * kRows + r] = part;
-                    }
-                    named_sync(1, 128);
-                    if (et < kRows) {
-                        float ss = 0.0f;
+                    for (int rb = 0; rb < a.R; rb += kRows) {  // 8 threads per row, fixed-order combine
+                        {
+                            const float* ssb = p == P_QKV ? a.ss_d : a.ss_o;
+                            const int r = et & 15, j = et >> 4;
+                            float part = 0.0f;
+                            for (int t = j; t < tilesH; t += 8) part += __ldcg(ssb + t * a.R + rb + r);
+                            xch[j * kRows + r] = part;
+                        }
+                        named_sync(1, 128);
+                        if (et < kRows) {
+                            float ss = 0.0f;
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) ss += xch[j * kRows + et];
-                        rs[et] = 1.0f / sqrtf(ss / static_cast<float>(a.H) + a.eps);
+                            for (int j = 0; j < 8; ++j) ss += xch[j * kRows + et];
+                            rs[rb + et] = 1.0f / sqrtf(ss / static_cast<float>(a.H) + a.eps);
+                        }
+                        named_sync(1, 128);
                     }
-                    named_sync(1, 128);
                 }
                 if ((p == P_O || p == P_DOWN) && any) {  // residual rows of this phase are final
                     if (et == 0) {
@@ -1372,41 +1414,56 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         const float* gn = p == P_O ? L.ffn_norm : L.next_attn_norm;
                         if (f < a.H) {
                             for (int r = 0; r < a.rows; ++r) cp_async4(hpre + r * kM + m, a.h + static_cast<size_t>(r) * a.H + f);
-                            if (gn) cp_async4(hpre + kRows * kM + m, gn + f);
+                            if (gn) cp_async4(hpre + a.R * kM + m, gn + f);
                         }
                         cp_async_commit();
                     }
                     mwait(&tfull[acc], acc_ph);
                     if (a.trace && et == 0) t_acc = gtimer();
                     tc_fence_after();
-                    float v[kN];
-                    const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * kAccCols;
-                    tmem_ld16(ta, v);
-                    tmem_ld16(ta + 16, v + 16);
-                    tmem_ld16(ta + 32, v + 32);
-                    tmem_wait_ld();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[acc]);
-                    if (++acc == 2) {
-                        acc = 0;
-                        acc_ph ^= 1;
-                    }
-                    float y[kRows];
+                    const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * a.acc_cols;
+                    const int nblk = (a.rows + kRows - 1) / kRows;  // 16-row blocks that hold rows
+                    // block rb of feature m: (hi + mid) + lo, the accumulator columns rb, R + rb, 2R + rb
+                    auto load_block = [&](int rb, float (&y)[kRows]) {
+                        float v[kN];
+                        tmem_ld16(ta + rb, v);
+                        tmem_ld16(ta + a.R + rb, v + 16);
+                        tmem_ld16(ta + 2 * a.R + rb, v + 32);
+                        tmem_wait_ld();
 #pragma unroll
-                    for (int r = 0; r < kRows; ++r) y[r] = (v[r] + v[kRows + r]) + v[2 * kRows + r];
+                        for (int r = 0; r < kRows; ++r) y[r] = (v[r] + v[kRows + r]) + v[2 * kRows + r];
+                    };
+                    auto release = [&]() {  // the accumulator is read: the MMA may reuse it
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                        if (++acc == 2) {
+                            acc = 0;
+                            acc_ph ^= 1;
+                        }
+                    };
                     bool done_tile = false;
                     if (lo == 0 && hi == g.KB) {
-                        epi_final(a, L, l, p, t, m, et, y, xch, rs, ropeT, hpre);
+                        for (int bk = 0; bk < nblk; ++bk) {
+                            float y[kRows];
+                            load_block(bk * kRows, y);
+                            if (bk == nblk - 1) release();
+                            epi_final(a, L, l, p, t, m, et, y, xch, rs, ropeT, hpre, bk * kRows);
+                        }
                         done_tile = true;
                     } else {  // stream-K fixup: last arriver sums the pieces in k order
                         const int first_u = t * g.KB;
                         const int c_first = static_cast<int>(((first_u + 1) * g.G - 1) / U);
                         const int piece = c - c_first;
                         const int n_pieces = static_cast<int>(((first_u + g.KB) * g.G - 1) / U) - c_first + 1;
-                        float* slot = parts + (static_cast<size_t>(t) * kMaxPieces + piece) * kRows * kM;
+                        float* slot = parts + (static_cast<size_t>(t) * kMaxPieces + piece) * a.R * kM;
+                        for (int bk = 0; bk < nblk; ++bk) {
+                            float y[kRows];
+                            load_block(bk * kRows, y);
 #pragma unroll
-                        for (int r = 0; r < kRows; ++r) slot[r * kM + m] = y[r];
+                            for (int r = 0; r < kRows; ++r) slot[(bk * kRows + r) * kM + m] = y[r];
+                        }
+                        release();
                         __threadfence();
                         if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 8) = gtimer();
                         named_sync(1, 128);
@@ -1419,27 +1476,30 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         if (*flag) {
                             if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 9) = gtimer();
                             __threadfence();
-                            float sacc[kRows];
-                            const float* p0 = parts + static_cast<size_t>(t) * kMaxPieces * kRows * kM;
-                            // pieces in k order; the loads of 4 pieces are in flight together
-                            for (int pc0 = 0; pc0 < n_pieces; pc0 += 4) {
-                                float t4[4][kRows];
+                            const float* p0 = parts + static_cast<size_t>(t) * kMaxPieces * a.R * kM;
+                            for (int bk = 0; bk < nblk; ++bk) {
+                                const int rb = bk * kRows;
+                                float sacc[kRows];
+                                // pieces in k order; the loads of 4 pieces are in flight together
+                                for (int pc0 = 0; pc0 < n_pieces; pc0 += 4) {
+                                    float t4[4][kRows];
 #pragma unroll
-                                for (int j = 0; j < 4; ++j)
+                                    for (int j = 0; j < 4; ++j)
 #pragma unroll
-                                    for (int r = 0; r < kRows; ++r)
-                                        t4[j][r] = pc0 + j < n_pieces
-                                                       ? __ldcg(p0 + (static_cast<size_t>(pc0 + j) * kRows + r) * kM + m)
-                                                       : 0.0f;
+                                        for (int r = 0; r < kRows; ++r)
+                                            t4[j][r] = pc0 + j < n_pieces
+                                                           ? __ldcg(p0 + (static_cast<size_t>(pc0 + j) * a.R + rb + r) * kM + m)
+                                                           : 0.0f;
 #pragma unroll
-                                for (int j = 0; j < 4; ++j) {
-                                    if (pc0 + j >= n_pieces) break;
+                                    for (int j = 0; j < 4; ++j) {
+                                        if (pc0 + j >= n_pieces) break;
 #pragma unroll
-                                    for (int r = 0; r < kRows; ++r) sacc[r] = (pc0 + j == 0) ? t4[j][r] : sacc[r] + t4[j][r];
+                                        for (int r = 0; r < kRows; ++r) sacc[r] = (pc0 + j == 0) ? t4[j][r] : sacc[r] + t4[j][r];
+                                    }
                                 }
+                                if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 10) = gtimer();
+                                epi_final(a, L, l, p, t, m, et, sacc, xch, rs, ropeT, hpre, rb);
                             }
-                            if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 10) = gtimer();
-                            epi_final(a, L, l, p, t, m, et, sacc, xch, rs, ropeT, hpre);
                             if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 11) = gtimer();
                             done_tile = true;
                         }
@@ -1522,10 +1582,10 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                             if (a.noload & 2) {
                                 mbar_arrive(&full[stage]);
                             } else {
-                                mbar_expect_tx(&full[stage], n * kBBytes);
+                                mbar_expect_tx(&full[stage], n * a.xbytes);
                                 for (int h = 0; h < n; ++h)
-                                    bulk_g2s(smem + (2 * stage + h) * kStageBytes + kABytes,
-                                             X + static_cast<size_t>((u + h) % g.KB) * kBBytes, kBBytes, &full[stage]);
+                                    bulk_g2s(smem + (2 * stage + h) * SB + kABytes,
+                                             X + static_cast<size_t>((u + h) % g.KB) * a.xbytes, a.xbytes, &full[stage]);
                             }
                         }
                         if (++stage == NP) {
@@ -1560,7 +1620,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_free(tmem, kTmemCols);
+        tmem_free(tmem, a.tmem_cols);
     }
     // last CTA out resets the dataflow flags and the exit counter for the next launch
     if (threadIdx.x == 0) {
@@ -1594,10 +1654,12 @@ size_t dyn_smem_budget(bool rows_attn) {
     return budget[rows_attn];
 }
 
-size_t smem_bytes(bool rows_attn, int stages, int hd, int group, int max_len) {
-    return 1024 + static_cast<size_t>(stages) * kStageBytes + (2 * kMaxStages + 4) * 8 + 32 +
-           sizeof(float) * (64 * kRows + 5 * kRows + attn_scratch_floats(rows_attn, hd, group, max_len) + kRows * hd +
-                            kRows * kM + kM) + 16;
+// dynamic shared memory of a launch with row capacity R (must match the
+// kernel's carve-up: ring | barriers | xch | rs | attention | ropeT | hpre)
+size_t smem_bytes(bool rows_attn, int stages, int hd, int group, int max_len, int R = kRows) {
+    return 1024 + static_cast<size_t>(stages) * (kABytes + 384 * R) + (2 * kMaxStages + 4) * 8 + 32 +
+           sizeof(float) * (64 * kRows + 4 * kRows + kMaxRows + attn_scratch_floats(rows_attn, hd, group, max_len) +
+                            (R == kRows ? kRows * hd : 0) + R * kM + kM) + 16;
 }
 
 }  // namespace mega
@@ -1627,6 +1689,16 @@ bool mega_supported(const Engine& e, int rows, bool additive_mask) {
     return sm <= dyn_smem_budget(ra);
 }
 
+// Rows one cross-session weight pass can carry: 32 (two 16-row blocks, MMA
+// N = 96) with the per-row attention design when its shared memory fits,
+// else 16.
+int mega_batch_rows(const Engine& e) {
+    if (!mega_supported(e, 1, false) || !rows_attention() || e.tp_size() > 1) return tc::kRows;
+    const ModelCfg& c = e.cfg();
+    const size_t sm = smem_bytes(true, 4, c.head_dim, c.n_heads / c.n_kv_heads, c.max_seq_len, kMaxRows);
+    return sm <= dyn_smem_budget(true) ? kMaxRows : tc::kRows;
+}
+
 namespace {
 struct MegaState {
     LayerDesc* d_layers = nullptr;
@@ -1636,6 +1708,7 @@ struct MegaState {
     unsigned long long* trace = nullptr;
     uint8_t* xim = nullptr;  // the four phases' input images, back to back
     float* partials = nullptr;  // 2 parity buffers of stream-K partials
+    int rcap = 0;               // row capacity the ss / image / partial buffers are sized for
     int* counters = nullptr;    // 2 parity arrays of per-tile arrival counters
     unsigned* flags = nullptr;  // dataflow completion flags
     float* apart = nullptr;     // attention chunk partials
@@ -1679,7 +1752,7 @@ int mega_trace_read(Bank& b, unsigned long long* out, size_t n) {
 float* mega_ss(Bank& b, int which, int tilesH) {
     MegaState* st = static_cast<MegaState*>(b.mega.get());
     if (!st) return nullptr;
-    return st->ss + (which ? tilesH * tc::kRows : 0);
+    return st->ss + (which ? tilesH * st->rcap : 0);
 }
 
 int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cudaStream_t s,
@@ -1717,15 +1790,10 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         SFG_CUDA(cudaMalloc(&st.bar, sizeof(unsigned) * (kBarSlots + 1)));
         SFG_CUDA(cudaMemset(st.bar, 0, sizeof(unsigned) * (kBarSlots + 1)));
         const int tilesH = (c.hidden_dim + tc::kM - 1) / tc::kM;
-        SFG_CUDA(cudaMalloc(&st.ss, sizeof(float) * 2 * tilesH * tc::kRows));
-        const size_t xblocks = static_cast<size_t>(2 * c.hidden_dim + c.q_dim() + c.ffn_dim) / tc::kKB;
-        SFG_CUDA(cudaMalloc(&st.xim, xblocks * tc::kBBytes));
         {
             const int tQ = (c.q_dim() + 2 * c.kv_dim() + tc::kM - 1) / tc::kM, tG = c.ffn_dim / 64;
             const int tiles_max = std::max(std::max(tQ, tG), tilesH);
-            st.part_stride = static_cast<size_t>(tiles_max) * kMaxPieces * tc::kRows * tc::kM;
             st.cnt_stride = tiles_max;
-            SFG_CUDA(cudaMalloc(&st.partials, sizeof(float) * 2 * st.part_stride));
             SFG_CUDA(cudaMalloc(&st.counters, sizeof(int) * 2 * st.cnt_stride));
             SFG_CUDA(cudaMemset(st.counters, 0, sizeof(int) * 2 * st.cnt_stride));
             // must match fptr(): stats tiles + counter, then per layer
@@ -1739,10 +1807,30 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
             SFG_CUDA(cudaMemset(st.acnt, 0, sizeof(unsigned) * c.n_kv_heads * 16));
             SFG_CUDA(cudaMemset(st.flags, 0, sizeof(unsigned) * st.nflags));
         }
-        SFG_CUDA(cudaMemset(st.xim, 0, xblocks * tc::kBBytes));
         SFG_CUDA(cudaDeviceSynchronize());
         b.mega = holder;
         stp = holder.get();
+    }
+    // row capacity of this launch: one 16-row block, or two for a
+    // cross-session pass of more than 16 rows
+    const int R = rows > tc::kRows ? kMaxRows : tc::kRows;
+    if (R > tc::kRows && (!rows_attention() || e.tp_size() > 1 || rows > kMaxRows))
+        throw Error(Kind::internal, "a wide (> 16-row) pass needs <= 32 rows, the per-row attention and no tensor parallelism");
+    if (stp->rcap < R) {  // (re)size the row-strided buffers
+        SFG_CUDA(cudaDeviceSynchronize());
+        if (stp->ss) cudaFree(stp->ss);
+        if (stp->xim) cudaFree(stp->xim);
+        if (stp->partials) cudaFree(stp->partials);
+        const int tilesH = (c.hidden_dim + tc::kM - 1) / tc::kM;
+        SFG_CUDA(cudaMalloc(&stp->ss, sizeof(float) * 2 * tilesH * R));
+        SFG_CUDA(cudaMemset(stp->ss, 0, sizeof(float) * 2 * tilesH * R));
+        const size_t xblocks = static_cast<size_t>(2 * c.hidden_dim + c.q_dim() + c.ffn_dim) / tc::kKB;
+        SFG_CUDA(cudaMalloc(&stp->xim, xblocks * 384 * R));
+        SFG_CUDA(cudaMemset(stp->xim, 0, xblocks * 384 * R));
+        stp->part_stride = static_cast<size_t>(stp->cnt_stride) * kMaxPieces * R * tc::kM;
+        SFG_CUDA(cudaMalloc(&stp->partials, sizeof(float) * 2 * stp->part_stride));
+        stp->rcap = R;
+        SFG_CUDA(cudaDeviceSynchronize());
     }
     const int nsm = device_sm_count();
     const int group = c.n_heads / c.n_kv_heads;
@@ -1751,10 +1839,11 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         return v ? std::min(std::max(atoi(v), 2), kMaxStages) : kMaxStages;
     }();
     int stages = stages_cap & ~1;  // the ring is walked in pairs of stages
+    const int RS = stp->rcap;      // the buffers' row stride (>= R)
     const bool ra = rows_attention();
     const void* kfn = ra ? reinterpret_cast<const void*>(mega_kernel<true>) : reinterpret_cast<const void*>(mega_kernel<false>);
-    while (stages > 4 && smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len) > dyn_smem_budget(ra)) stages -= 2;
-    const size_t smem = smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len);
+    while (stages > 4 && smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len, RS) > dyn_smem_budget(ra)) stages -= 2;
+    const size_t smem = smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len, RS);
     {
         ensure_smem_attr(kfn, smem);
         int nb = 0;
@@ -1773,6 +1862,13 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     a.nlayers = le - lb;
     a.rows = rows;
     a.stages = stages;
+    a.R = RS;
+    a.xbytes = 384 * RS;
+    a.stage_bytes = tc::kABytes + a.xbytes;
+    a.acc_cols = RS == tc::kRows ? kAccCols : 128;
+    a.tmem_cols = 2 * a.acc_cols > kTmemCols ? 2 * a.acc_cols : kTmemCols;
+    a.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>((3 * RS) >> 3) << 17) |
+              (static_cast<uint32_t>(tc::kM >> 4) << 24);
     const Dims dl = e.dims();  // this engine's shard (tensor parallelism: local heads / FFN columns)
     a.H = dl.H;
     a.qd = dl.qd;
@@ -1810,8 +1906,8 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
             a.vbank[i] = bi->vslab(lb);
         }
         if (!stp->rowinfo) {
-            SFG_CUDA(cudaMalloc(&stp->rowinfo, sizeof(int32_t) * 3 * tc::kRows));
-            SFG_CUDA(cudaMallocHost(&stp->rowinfo_pin, sizeof(int32_t) * 3 * tc::kRows));
+            SFG_CUDA(cudaMalloc(&stp->rowinfo, sizeof(int32_t) * 3 * kMaxRows));
+            SFG_CUDA(cudaMallocHost(&stp->rowinfo_pin, sizeof(int32_t) * 3 * kMaxRows));
         }
         std::memcpy(stp->rowinfo_pin, rowinfo, sizeof(int32_t) * 3 * rows);
         SFG_CUDA(cudaMemcpyAsync(stp->rowinfo, stp->rowinfo_pin, sizeof(int32_t) * 3 * rows, cudaMemcpyHostToDevice, s));
@@ -1822,7 +1918,7 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     a.att = ws.att;
     a.act = ws.act;
     a.ss_d = stp->ss;
-    a.ss_o = stp->ss + tilesH * tc::kRows;
+    a.ss_o = stp->ss + tilesH * RS;
     a.pos = ws.pos;
     a.rope_cos = e.rope_cos();
     a.rope_sin = e.rope_sin();
@@ -1903,9 +1999,9 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     {
         const size_t kbH = c.hidden_dim / tc::kKB, kbQ = c.q_dim() / tc::kKB;
         a.xim[P_QKV] = stp->xim;
-        a.xim[P_O] = a.xim[P_QKV] + kbH * tc::kBBytes;
-        a.xim[P_GU] = a.xim[P_O] + kbQ * tc::kBBytes;
-        a.xim[P_DOWN] = a.xim[P_GU] + kbH * tc::kBBytes;
+        a.xim[P_O] = a.xim[P_QKV] + kbH * a.xbytes;
+        a.xim[P_GU] = a.xim[P_O] + kbQ * a.xbytes;
+        a.xim[P_DOWN] = a.xim[P_GU] + kbH * a.xbytes;
     }
     if (mega_trace_enabled() && !stp->trace) {
         const size_t bytes = sizeof(unsigned long long) * static_cast<size_t>(nsm) * kBarSlots * kTraceW;

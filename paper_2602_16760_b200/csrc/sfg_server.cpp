@@ -392,8 +392,8 @@ void Server::handle_frame(const wire::FrameView& f, std::vector<uint8_t>& resp) 
 }
 
 // handle() over several frames: step frames of distinct sessions whose rows
-// fit one pass (<= 16 rows, masks inside the layer-stack contract) share ONE
-// weight pass; everything else is handled frame by frame.  Responses (and
+// fit one pass (<= 32 rows, each session <= 16, masks inside the layer-stack
+// contract) share ONE weight pass; everything else is handled frame by frame.  Responses (and
 // error frames) are exactly what handle() returns for each frame.
 void Server::handle_batch(int n, const uint8_t* const* reqs, const size_t* lens,
                           std::vector<std::vector<uint8_t>>& resps) {
@@ -402,6 +402,9 @@ void Server::handle_batch(int n, const uint8_t* const* reqs, const size_t* lens,
     // too for these shapes, so responses stay bitwise those of handle()
     const bool batchable = eng_.fast() && eng_.tp_size() == 1 && rows_attention() && mega_mode() == 1 &&
                            mega_supported(eng_, 1, false) && cfg_.layer_end - cfg_.layer_begin <= 50;
+    // rows one shared weight pass carries: two sessions' 16-row lookahead
+    // batches (32) when the layer stack supports it
+    const int pass_rows = batchable ? mega_batch_rows(eng_) : tc_rows();
     std::vector<std::unique_ptr<StepState>> pending;
     std::vector<StepState*> group;
     int group_rows = 0;
@@ -463,7 +466,7 @@ void Server::handle_batch(int n, const uint8_t* const* reqs, const size_t* lens,
             }
             continue;
         }
-        if (group_rows + st->hc.seq > tc_rows() || static_cast<int>(group.size()) >= 16) flush();
+        if (group_rows + st->hc.seq > pass_rows || static_cast<int>(group.size()) >= 16) flush();
         group_rows += st->hc.seq;
         group.push_back(st.get());
         pending.push_back(std::move(st));

@@ -176,3 +176,26 @@ def test_handle_batch_seven_b_width():
     assert a.shared_passes() >= 3
     for sid in sids:
         assert a.session_view(sid) == b.session_view(sid)
+
+
+def test_handle_batch_two_full_lookahead_batches(desk_fast):
+    """Two sessions' full 16-row lookahead batches (anchor + 15 draft rows) in
+    ONE 32-row weight pass (two 16-row blocks, MMA N = 96): every response
+    bitwise equal to one by one, over rounds that keep and relocate rows."""
+    cfg, m, eng = desk_fast
+    rng = np.random.default_rng(11)
+    rounds = [[_prompt("s0", rng.integers(0, cfg.vocab_size, 9).tolist()),
+               _prompt("s1", rng.integers(0, cfg.vocab_size, 14).tolist())]]
+    lens = {"s0": 9, "s1": 14}
+    for rnd_i in range(4):
+        rnd = []
+        for sid in ("s0", "s1"):
+            keep = None if rnd_i == 0 else [0, 3]
+            prior = lens[sid] - (0 if rnd_i == 0 else 16 - 2)
+            ids = rng.integers(0, cfg.vocab_size, 16).tolist()
+            rnd.append(lambda mm, sid=sid, prior=prior, ids=ids, keep=keep: _step(mm, sid, prior, ids, keep=keep,
+                                                                                   tree=True))
+            lens[sid] = prior + 16
+        rounds.append(rnd)
+    a = _run_pair(cfg, m, eng, rounds)
+    assert a.shared_passes() >= 4

@@ -40,8 +40,10 @@ def main():
     cfg = po.mistral7b_cfg()
     # 1) the bench's extrapolation (bench.py cpu_sample / cpu_head_time), same host, 1 thread
     tm = ref.timing_model(cfg, (2, 3), False)
+    lib.ref_time_forward(tm.h, 2, 3, 1, 24, 1)  # first touch of the fresh weights (bench.py does the same)
     t_layer = lib.ref_time_forward(tm.h, 2, 3, 16, 24, 1)
     th = ref.timing_model(cfg, (0, 0), True)
+    lib.ref_time_finalize(th.h, 1, 1)
     t_head = lib.ref_time_finalize(th.h, 1, 1)
     extrapolated = t_layer * cfg.n_layers + t_head * 16
     del tm, th
