@@ -550,7 +550,7 @@ def server_batch_sweep(sfg, eng, cfg, nl, rank, rounds=6):
     rng = np.random.default_rng(5 + rank)
     H = cfg.hidden_dim
     out = {}
-    for k, r in ((1, 4), (4, 4), (8, 2), (16, 1)):
+    for k, r in ((1, 16), (2, 16), (4, 8), (4, 4), (8, 4), (16, 2)):
         res = {}
         for mode in ("one_by_one", "batched"):
             srv = sfg.ServerEngine(eng, sfg.ServerConfig(SPLIT, nl - SPLIT, max_sessions=64))

@@ -385,7 +385,8 @@ __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence
 // feature k, row r of a phase's global activation image: [KB][48 x 64] bf16
 // K-major SW128 blocks, the exact smem layout the MMA reads, so a stage's
 // activations arrive with one 6 KB bulk copy.
-__device__ __forceinline__ void put_split(uint8_t* img, int k, int r, float x, int R) {
+template <int R>  // rows per launch (image row stride)
+__device__ __forceinline__ void put_split(uint8_t* img, int k, int r, float x) {
     uint8_t* blk = img + static_cast<size_t>(k >> 6) * (static_cast<size_t>(R) * 384);
     const int kk = k & 63;
     const __nv_bfloat16 hb = __float2bfloat16_rn(x);
@@ -439,6 +440,7 @@ __device__ __forceinline__ float ld_relaxed_sys(const float* p) {
 }
 
 // rows rb .. rb+15 of the launch (one 16-row block of its R rows)
+template <int R>
 __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, int tile, int m, int et,
                           const float (&yin)[kRows], float* xch, const float* rs, const float* ropeT,
                           const float* hpre, int rb) {
@@ -455,7 +457,7 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
         // the rows' cos/sin: staged in shared memory at kernel entry for
         // 16-row launches, read from the (L2-resident) host-libm tables otherwise
         float cs[kRows], sn[kRows];
-        if (a.R == kRows) {
+        if constexpr (R == kRows) {
 #pragma unroll
             for (int r = 0; r < kRows; ++r) {
                 cs[r] = ropeT[r * a.hd + i];
@@ -504,7 +506,7 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
                         const float silu = g / (1.0f + expf(-g));
                         const float v = silu * ub[m * kRows + r];
                         a.act[static_cast<size_t>(rb + r) * a.F + fg] = v;
-                        put_split(a.xim[P_DOWN], fg, rb + r, v, a.R);
+                        put_split<R>(a.xim[P_DOWN], fg, rb + r, v);
                     }
         }
         named_sync(1, 128);
@@ -542,7 +544,7 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
         const float* gn = p == P_O ? L.ffn_norm : L.next_attn_norm;
         uint8_t* img = p == P_O ? a.xim[P_GU] : a.xim[P_QKV];
         cp_async_wait_all();
-        const float gf = (gn && f < a.H) ? hpre[a.R * kM + m] : 0.0f;  // prefetched with the residual
+        const float gf = (gn && f < a.H) ? hpre[R * kM + m] : 0.0f;  // prefetched with the residual
         // residual rows were prefetched into shared memory (cp.async) while
         // the accumulator was still being produced
         cp_async_wait_all();
@@ -555,10 +557,10 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
             if (f < a.H && rb + r < a.rows) {
                 hn[r] += y[r];
                 a.h[static_cast<size_t>(rb + r) * a.H + f] = hn[r];
-                if (gn) put_split(img, f, rb + r, hn[r] * gf, a.R);
+                if (gn) put_split<R>(img, f, rb + r, hn[r] * gf);
             }
         }
-        float* ss = (p == P_O ? a.ss_o : a.ss_d) + static_cast<size_t>(tile) * a.R + rb;
+        float* ss = (p == P_O ? a.ss_o : a.ss_d) + static_cast<size_t>(tile) * R + rb;
         if (a.trace && et == 0) *tslot(a, blockIdx.x, input_barrier(l, p), 13) = gtimer();
         tile_sumsq(hn, xch + 64 * kRows, ss, et);
         if (a.trace && et == 0) *tslot(a, blockIdx.x, input_barrier(l, p), 14) = gtimer();
@@ -567,7 +569,7 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
 
 // ── attention for one (row, kv head): flash-decode over the row's visible
 // keys with a fixed key partition (chunk i of 32 keys -> warp i % 8).
-template <int HD, int GR>  // GR: compile-time bound on the GQA group (register arrays)
+template <int HD, int GR, int R>  // GR: compile-time bound on the GQA group (register arrays); R: rows per launch
 __device__ void attention_row_item(const MegaArgs& a, const LayerDesc& L, int l, int row, int kvh, int at, float* qs,
                                float* wst, float* ocomb, int* cols) {
     const int group = a.n_heads / a.n_kv;
@@ -686,12 +688,13 @@ __device__ void attention_row_item(const MegaArgs& a, const LayerDesc& L, int l,
         const int f = (kvh * group + g) * HD + dd;
         const float o = acc / l;
         a.att[static_cast<size_t>(row) * a.qd + f] = o;
-        put_split(a.xim[P_O], f, row, o, a.R);
+        put_split<R>(a.xim[P_O], f, row, o);
     }
     fence_proxy_async_global();
     named_sync(3, 256);
 }
 
+template <int R>
 __device__ __forceinline__ void attention_rows_dispatch(const MegaArgs& a, const LayerDesc& L, int l, int row, int kvh,
                                                    int at, float* qs, float* wst, float* ocomb, int* cols) {
     const int group = a.n_heads / a.n_kv;
@@ -708,15 +711,15 @@ __device__ __forceinline__ void attention_rows_dispatch(const MegaArgs& a, const
     }
     if (group <= 4) {
         switch (a.hd) {
-            case 64: attention_row_item<64, 4>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
-            case 128: attention_row_item<128, 4>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
-            case 160: attention_row_item<160, 4>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
-            default: attention_row_item<32, 4>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
+            case 64: attention_row_item<64, 4, R>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
+            case 128: attention_row_item<128, 4, R>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
+            case 160: attention_row_item<160, 4, R>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
+            default: attention_row_item<32, 4, R>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
         }
     } else {
         switch (a.hd) {
-            case 64: attention_row_item<64, 8>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
-            default: attention_row_item<32, 8>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
+            case 64: attention_row_item<64, 8, R>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
+            default: attention_row_item<32, 8, R>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
         }
     }
     if (at == 0) signal_add(fptr(a, l, K_ATT, kvh), 1u);  // item's att rows + image are published
@@ -932,7 +935,7 @@ __device__ __noinline__ void attention_chunk(const MegaArgs& a, const LayerDesc&
             const float val = ov[dd] / lsum;
             const int f = (kvh * group + g) * HD + d;
             a.att[static_cast<size_t>(r) * a.qd + f] = val;
-            put_split(a.xim[P_O], f, r, val, a.R);
+            put_split<kRows>(a.xim[P_O], f, r, val);
         }
     };
     if (a.trace && at == 0) *tslot(a, blockIdx.x, 5 * l + 2, 13) = gtimer();
@@ -1104,7 +1107,9 @@ __host__ __device__ __forceinline__ int attn_scratch_floats(bool rows_attn, int 
 // 10 warps, one CTA per SM: 3 warps share an SM sub-partition's 16K
 // registers, so 168 registers per thread is the ceiling
 // kRowsAttn: which attention design this instantiation carries (MegaArgs::attn_rows)
-template <bool kRowsAttn>
+// RR: rows per launch (16, or 32 for cross-session passes; compile time so the
+// 16-row path keeps its constant-folded addressing)
+template <bool kRowsAttn, int RR>
 __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant__ MegaArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1127,13 +1132,13 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
     float* ocomb = wst + 8 * kMaxGroup * 2;                    //   [8][group][hd] warp partials
     int* cols = reinterpret_cast<int*>(ocomb + 8 * (a.n_heads / a.n_kv) * a.hd);  //   [max_len]
     float* ropeT = rs + kMaxRows + attn_scratch_floats(kRowsAttn, a.hd, a.n_heads / a.n_kv, a.max_len);  // [16][hd] cos | sin (R = 16)
-    float* hpre = ropeT + (a.R == kRows ? kRows * a.hd : 0);    // [R][128] residual prefetch + gain row
+    float* hpre = ropeT + (RR == kRows ? kRows * a.hd : 0);     // [R][128] residual prefetch + gain row
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = gridDim.x, c = blockIdx.x;
     if (threadIdx.x == 0 && a.trace) *tslot(a, c, kBarSlots - 1, 0) = gtimer();
     if (threadIdx.x < kMaxRows) sh_pos[threadIdx.x] = static_cast<int>(threadIdx.x) < a.rows ? a.pos[threadIdx.x] : 0;
-    for (int i = threadIdx.x; a.R == kRows && i < kRows * a.hd; i += blockDim.x) {  // RoPE table rows (host-libm values)
+    for (int i = threadIdx.x; RR == kRows && i < kRows * a.hd; i += blockDim.x) {  // RoPE table rows (host-libm values)
         const int r = i / a.hd, j = i % a.hd, half = a.hd >> 1;
         float v = j < half ? 1.0f : 0.0f;
         if (r < a.rows) {
@@ -1336,15 +1341,15 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
         for (int t = c; t < tilesH; t += G) {
             const int f = t * kM + m;
             const float gf = f < a.H ? __ldg(sh_layers[0].attn_norm + f) : 0.0f;
-            for (int rb = 0; rb < a.R; rb += kRows) {  // 16-row blocks (every block: the ss rows of padding are 0)
+            for (int rb = 0; rb < RR; rb += kRows) {  // 16-row blocks (every block: the ss rows of padding are 0)
                 float hv[kRows];
 #pragma unroll
                 for (int r = 0; r < kRows; ++r) {
                     const bool ok = f < a.H && rb + r < a.rows;
                     hv[r] = ok ? __ldcg(a.h + static_cast<size_t>(rb + r) * a.H + f) : 0.0f;
-                    if (ok) put_split(a.xim[P_QKV], f, rb + r, hv[r] * gf, a.R);
+                    if (ok) put_split<RR>(a.xim[P_QKV], f, rb + r, hv[r] * gf);
                 }
-                tile_sumsq(hv, xch + 64 * kRows, a.ss_d + static_cast<size_t>(t) * a.R + rb, et);
+                tile_sumsq(hv, xch + 64 * kRows, a.ss_d + static_cast<size_t>(t) * RR + rb, et);
             }
             fence_proxy_async_global();
             named_sync(1, 128);
@@ -1376,12 +1381,12 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                                            : fptr(a, l, K_O, tilesH),
                                 static_cast<unsigned>(tilesH));
                     named_sync(1, 128);
-                    for (int rb = 0; rb < a.R; rb += kRows) {  // 8 threads per row, fixed-order combine
+                    for (int rb = 0; rb < RR; rb += kRows) {  // 8 threads per row, fixed-order combine
                         {
                             const float* ssb = p == P_QKV ? a.ss_d : a.ss_o;
                             const int r = et & 15, j = et >> 4;
                             float part = 0.0f;
-                            for (int t = j; t < tilesH; t += 8) part += __ldcg(ssb + t * a.R + rb + r);
+                            for (int t = j; t < tilesH; t += 8) part += __ldcg(ssb + t * RR + rb + r);
                             xch[j * kRows + r] = part;
                         }
                         named_sync(1, 128);
@@ -1414,7 +1419,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         const float* gn = p == P_O ? L.ffn_norm : L.next_attn_norm;
                         if (f < a.H) {
                             for (int r = 0; r < a.rows; ++r) cp_async4(hpre + r * kM + m, a.h + static_cast<size_t>(r) * a.H + f);
-                            if (gn) cp_async4(hpre + a.R * kM + m, gn + f);
+                            if (gn) cp_async4(hpre + RR * kM + m, gn + f);
                         }
                         cp_async_commit();
                     }
@@ -1422,13 +1427,13 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     if (a.trace && et == 0) t_acc = gtimer();
                     tc_fence_after();
                     const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * a.acc_cols;
-                    const int nblk = (a.rows + kRows - 1) / kRows;  // 16-row blocks that hold rows
+                    const int nblk = RR == kRows ? 1 : (a.rows + kRows - 1) / kRows;  // 16-row blocks that hold rows
                     // block rb of feature m: (hi + mid) + lo, the accumulator columns rb, R + rb, 2R + rb
                     auto load_block = [&](int rb, float (&y)[kRows]) {
                         float v[kN];
                         tmem_ld16(ta + rb, v);
-                        tmem_ld16(ta + a.R + rb, v + 16);
-                        tmem_ld16(ta + 2 * a.R + rb, v + 32);
+                        tmem_ld16(ta + RR + rb, v + 16);
+                        tmem_ld16(ta + 2 * RR + rb, v + 32);
                         tmem_wait_ld();
 #pragma unroll
                         for (int r = 0; r < kRows; ++r) y[r] = (v[r] + v[kRows + r]) + v[2 * kRows + r];
@@ -1448,7 +1453,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                             float y[kRows];
                             load_block(bk * kRows, y);
                             if (bk == nblk - 1) release();
-                            epi_final(a, L, l, p, t, m, et, y, xch, rs, ropeT, hpre, bk * kRows);
+                            epi_final<RR>(a, L, l, p, t, m, et, y, xch, rs, ropeT, hpre, bk * kRows);
                         }
                         done_tile = true;
                     } else {  // stream-K fixup: last arriver sums the pieces in k order
@@ -1456,7 +1461,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         const int c_first = static_cast<int>(((first_u + 1) * g.G - 1) / U);
                         const int piece = c - c_first;
                         const int n_pieces = static_cast<int>(((first_u + g.KB) * g.G - 1) / U) - c_first + 1;
-                        float* slot = parts + (static_cast<size_t>(t) * kMaxPieces + piece) * a.R * kM;
+                        float* slot = parts + (static_cast<size_t>(t) * kMaxPieces + piece) * RR * kM;
                         for (int bk = 0; bk < nblk; ++bk) {
                             float y[kRows];
                             load_block(bk * kRows, y);
@@ -1476,7 +1481,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         if (*flag) {
                             if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 9) = gtimer();
                             __threadfence();
-                            const float* p0 = parts + static_cast<size_t>(t) * kMaxPieces * a.R * kM;
+                            const float* p0 = parts + static_cast<size_t>(t) * kMaxPieces * RR * kM;
                             for (int bk = 0; bk < nblk; ++bk) {
                                 const int rb = bk * kRows;
                                 float sacc[kRows];
@@ -1488,7 +1493,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
 #pragma unroll
                                         for (int r = 0; r < kRows; ++r)
                                             t4[j][r] = pc0 + j < n_pieces
-                                                           ? __ldcg(p0 + (static_cast<size_t>(pc0 + j) * a.R + rb + r) * kM + m)
+                                                           ? __ldcg(p0 + (static_cast<size_t>(pc0 + j) * RR + rb + r) * kM + m)
                                                            : 0.0f;
 #pragma unroll
                                     for (int j = 0; j < 4; ++j) {
@@ -1498,7 +1503,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                                     }
                                 }
                                 if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 10) = gtimer();
-                                epi_final(a, L, l, p, t, m, et, sacc, xch, rs, ropeT, hpre, rb);
+                                epi_final<RR>(a, L, l, p, t, m, et, sacc, xch, rs, ropeT, hpre, rb);
                             }
                             if (a.trace && et == 0) *tslot(a, c, input_barrier(l, p), 11) = gtimer();
                             done_tile = true;
@@ -1527,7 +1532,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                 if (p == P_QKV) {  // attention, shared with the activation warps
                     if constexpr (kRowsAttn) {
                         for (int it = c; it < a.rows * a.n_kv; it += G)
-                            attention_rows_dispatch(a, L, l, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst,
+                            attention_rows_dispatch<RR>(a, L, l, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst,
                                                     ocomb, cols);
                     } else {
                         const int nchunks = (sh_prior + a.rows + kKeyChunk - 1) / kKeyChunk;
@@ -1603,7 +1608,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                 if (p == P_QKV) {  // join the attention phase
                     if constexpr (kRowsAttn) {
                         for (int it = c; it < a.rows * a.n_kv; it += G)
-                            attention_rows_dispatch(a, L, l, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst,
+                            attention_rows_dispatch<RR>(a, L, l, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst,
                                                     ocomb, cols);
                     } else {
                         const int nchunks = (sh_prior + a.rows + kKeyChunk - 1) / kKeyChunk;
@@ -1646,9 +1651,9 @@ size_t dyn_smem_budget(bool rows_attn) {
     if (!budget[rows_attn]) {
         cudaFuncAttributes fa{};
         if (rows_attn)
-            cudaFuncGetAttributes(&fa, mega_kernel<true>);
+            cudaFuncGetAttributes(&fa, mega_kernel<true, kMaxRows>);
         else
-            cudaFuncGetAttributes(&fa, mega_kernel<false>);
+            cudaFuncGetAttributes(&fa, mega_kernel<false, kRows>);
         budget[rows_attn] = 227 * 1024 - fa.sharedSizeBytes;
     }
     return budget[rows_attn];
@@ -1841,7 +1846,9 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     int stages = stages_cap & ~1;  // the ring is walked in pairs of stages
     const int RS = stp->rcap;      // the buffers' row stride (>= R)
     const bool ra = rows_attention();
-    const void* kfn = ra ? reinterpret_cast<const void*>(mega_kernel<true>) : reinterpret_cast<const void*>(mega_kernel<false>);
+    const void* kfn = !ra ? reinterpret_cast<const void*>(mega_kernel<false, kRows>)
+                      : RS == kRows ? reinterpret_cast<const void*>(mega_kernel<true, kRows>)
+                                    : reinterpret_cast<const void*>(mega_kernel<true, kMaxRows>);
     while (stages > 4 && smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len, RS) > dyn_smem_budget(ra)) stages -= 2;
     const size_t smem = smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len, RS);
     {
