@@ -24,7 +24,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <initializer_list>
+#include <string>
 #include <type_traits>
 
 #include "sfg_engine.h"
@@ -496,6 +498,193 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
 }
 
+// ── prompt GEMM: (weight tile x 128-token tile) items, whole K, no split-K ──
+// A prompt of P tokens has P/128 token tiles; every (weight tile t, token tile
+// j) item is one CTA that streams the tile's weights (16 KB per k-block, L2
+// hits for all but the first of the tile's P/128 items, which run side by
+// side) against the token tile's activation image and accumulates D[128
+// features x 128 tokens] in TMEM: per k-block and K=16 step, the hi, mid and
+// lo bf16 pieces of the activations are three N = 128 MMAs into the SAME
+// accumulator (fixed order hi, mid, lo) — so a 2048-token prompt reads each
+// weight byte from HBM once instead of 26 times, runs N = 128 MMAs instead of
+// N = 48 ones, and needs no stream-K fixups.  Results differ from the decode
+// kernels only in summation order (deterministic; FAST tolerance vs the
+// reference, tests/test_gpu_fast.py, test_gpu_long_context.py).
+constexpr int kPT = 128;                     // tokens per tile (MMA N)
+constexpr int kPBBytes = kPT * kKB * 2;      // one piece of a k-block: 16 KB
+constexpr int kPStage = kABytes + 3 * kPBBytes;  // 64 KB
+constexpr int kPStages = 3;
+constexpr uint32_t kPIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kPT >> 3) << 17) |
+                             (static_cast<uint32_t>(kM >> 4) << 24);
+constexpr size_t pgemm_smem_bytes() { return 1024 + static_cast<size_t>(kPStages) * kPStage + 2 * kPStages * 8 + 8 + 16 + (64 * kRows + 8 * kRows) * 4; }
+
+struct PgArgs {
+    GemmArgs g;           // weights, tiles, KB, n_out and the epilogue operands (row0/rows set per block)
+    const uint8_t* X;     // [TT][KB][3][kPT x 64] bf16 SW128 (hi | mid | lo)
+    int TT;               // token tiles
+    int total_rows;       // prompt rows of this pass
+};
+
+__device__ __forceinline__ void mma_bf16_n128(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(kPIdesc), "r"(accum)
+        : "memory");
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1) pgemm_kernel(const __grid_constant__ PgArgs pa) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPStages * kPStage);
+    uint64_t* empty = full + kPStages;
+    uint64_t* tfull = empty + kPStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+    float* xch = reinterpret_cast<float*>(tmem_slot + 4);
+    const GemmArgs& a = pa.g;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // item -> (weight tile, token tile): consecutive CTAs share a weight tile
+    const int t = blockIdx.x / pa.TT, j = blockIdx.x % pa.TT;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kPStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kPT)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp == 0) {
+        if (lane == 0) {  // ── producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int kb = 0; kb < a.KB; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* sa = smem + stage * kPStage;
+                mbar_expect_tx(&full[stage], kPStage);
+                bulk_g2s(sa, a.W + (static_cast<size_t>(t) * a.KB + kb) * kABytes, kABytes, &full[stage]);
+                bulk_g2s(sa + kABytes, pa.X + (static_cast<size_t>(j) * a.KB + kb) * 3 * kPBBytes, 3 * kPBBytes,
+                         &full[stage]);
+                if (++stage == kPStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ── MMA issuer: hi, mid, lo into one accumulator per K=16 step
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int kb = 0; kb < a.KB; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                const uint32_t sa = smem_u32(smem + stage * kPStage);
+                const uint64_t da = smem_desc(sa);
+#pragma unroll
+                for (int k = 0; k < kKB / 16; ++k)
+#pragma unroll
+                    for (int pc = 0; pc < 3; ++pc)
+                        mma_bf16_n128(tmem, da + 2 * k, smem_desc(sa + kABytes + pc * kPBBytes) + 2 * k,
+                                      (kb > 0 || k > 0 || pc > 0) ? 1u : 0u);
+                mma_commit(&empty[stage]);
+                if (++stage == kPStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            mma_commit(tfull);
+        }
+    } else {  // ── epilogue: 16-token blocks of the tile through the decode epilogues
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        mbar_wait(tfull, 0);
+        tc_fence_after();
+        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        for (int b = 0; b < kPT / kRows; ++b) {
+            const int row0 = j * kPT + b * kRows;
+            if (row0 >= pa.total_rows) break;  // uniform over the epilogue warps
+            float y[kRows];
+            tmem_ld16(ta + b * kRows, y);
+            tmem_wait_ld();
+            GemmArgs ab = a;
+            ab.row0 = a.row0 + row0;
+            ab.rows = min(kRows, pa.total_rows - row0);
+            final_epilogue<EPI>(ab, t, m, y, xch);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kPT) : "memory");
+    }
+}
+
+// [RMSNorm] + 3-way split of prompt rows into the token-tiled image: one CTA
+// per row (rows beyond `rows` of the last tile are written as zeros).
+__global__ void __launch_bounds__(256) pprep_kernel(const float* __restrict__ x, int ldx, int K, int rows,
+                                                    const float* __restrict__ gain, float eps,
+                                                    uint8_t* __restrict__ xs) {
+    const int row = blockIdx.x, j = row / kPT, r = row % kPT, KB = K / kKB;
+    const bool live = row < rows;
+    const float* xr = x + static_cast<size_t>(live ? row : 0) * ldx;
+    float scale = 1.0f;
+    if (gain && live) {
+        __shared__ float red[8];
+        float ss = 0.0f;
+        for (int i = threadIdx.x; i < K; i += 256) ss += xr[i] * xr[i];
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float tt = 0.0f;
+            for (int w = 0; w < 8; ++w) tt += red[w];
+            red[0] = 1.0f / sqrtf(tt / static_cast<float>(K) + eps);
+        }
+        __syncthreads();
+        scale = red[0];
+    }
+    for (int k8 = threadIdx.x * 8; k8 < K; k8 += 256 * 8) {
+        __align__(16) __nv_bfloat16 hi[8], mid[8], lo[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            float v = live ? xr[k8 + e] : 0.0f;
+            if (gain) v = (v * scale) * gain[k8 + e];
+            const __nv_bfloat16 h = __float2bfloat16_rn(v);
+            const float r1 = v - __bfloat162float(h);
+            const __nv_bfloat16 mm = __float2bfloat16_rn(r1);
+            hi[e] = h;
+            mid[e] = mm;
+            lo[e] = __float2bfloat16_rn(r1 - __bfloat162float(mm));
+        }
+        const int kb = k8 / kKB, kk = k8 % kKB;
+        uint8_t* base = xs + (static_cast<size_t>(j) * KB + kb) * 3 * kPBBytes;
+        *reinterpret_cast<uint4*>(base + sw128_off(r, kk)) = *reinterpret_cast<uint4*>(hi);
+        *reinterpret_cast<uint4*>(base + kPBBytes + sw128_off(r, kk)) = *reinterpret_cast<uint4*>(mid);
+        *reinterpret_cast<uint4*>(base + 2 * kPBBytes + sw128_off(r, kk)) = *reinterpret_cast<uint4*>(lo);
+    }
+}
+
+template <int EPI>
+void launch_pgemm(const PgArgs& pa, cudaStream_t s) {
+    ensure_smem_attr(reinterpret_cast<const void*>(pgemm_kernel<EPI>), pgemm_smem_bytes());
+    pgemm_kernel<EPI><<<pa.g.tiles * pa.TT, kThreads, pgemm_smem_bytes(), s>>>(pa);
+}
+
 // ── activation prologue: [RMSNorm] + 3-way bf16 split into the swizzled B image
 // One CTA per row of the pass; rows beyond `rows` keep stale values, which
 // only feed their own (ignored) MMA columns.
@@ -757,8 +946,133 @@ static int grid_for(int tiles, int KB) {
     return static_cast<int>(std::max<long long>(g, 1));
 }
 
+// Prompt passes (rows > 16): the (weight tile x 128-token tile) GEMMs.
+// SFG_PROMPT=chunks selects the older five-chunk stream-K passes (A/B).
+static bool prompt_tiles() {
+    static const bool on = [] {
+        const char* v = getenv("SFG_PROMPT");
+        return !(v && std::string(v) == "chunks");
+    }();
+    return on;
+}
+
+static int fast_forward_layer_prompt(Engine& e, Bank& b, int layer, int rows, Workspace& ws, int prior,
+                                     cudaStream_t s) {
+    const ModelCfg& c = e.cfg();
+    const Dims d = e.dims();
+    const LayerWeights& L = e.layer(layer);
+    float* kc = b.kslab(layer);
+    float* vc = b.vslab(layer);
+    const int TT = (rows + kPT - 1) / kPT;
+    const size_t img = static_cast<size_t>(TT) * max_kb(c) * 3 * kPBBytes;
+    if (img > ws.pimg_bytes) {
+        SFG_CUDA(cudaDeviceSynchronize());
+        if (ws.pimg) cudaFree(ws.pimg);
+        ws.pimg = nullptr;
+        SFG_CUDA(cudaMalloc(&ws.pimg, img));
+        ws.pimg_bytes = img;
+    }
+    uint8_t* X = static_cast<uint8_t*>(ws.pimg);
+    int n = 0;
+    const double R = rows;
+    auto pprep = [&](const float* x, int ld, int K, const float* gain, float eps) {
+        pprep_kernel<<<TT * kPT, 256, 0, s>>>(x, ld, K, rows, gain, eps, X);
+        ++n;
+    };
+    auto args = [&]() {
+        PgArgs pa{};
+        pa.X = X;
+        pa.TT = TT;
+        pa.total_rows = rows;
+        pa.g.row0 = 0;
+        pa.g.rows = rows;
+        return pa;
+    };
+    {  // attention-input RMSNorm + split, fused QKV + RoPE + KV append
+        pprep(ws.h, d.H, d.H, L.attn_norm, d.eps);
+        PgArgs pa = args();
+        GemmArgs& a = pa.g;
+        a.W = static_cast<const uint8_t*>(L.f_qkv);
+        a.tiles = tiles_for(d.qd + 2 * d.kvd);
+        a.KB = d.H / kKB;
+        a.n_out = d.qd + 2 * d.kvd;
+        a.out = ws.q;
+        a.qd = d.qd;
+        a.kvd = d.kvd;
+        a.hd = d.hd;
+        a.max_len = d.max_len;
+        a.prior = ws.meta;
+        a.pos = ws.pos;
+        a.rope_cos = e.rope_cos();
+        a.rope_sin = e.rope_sin();
+        a.kc = kc;
+        a.vc = vc;
+        ProfScope ps(K_QKV, s, 2.0 * d.H * a.n_out + 4.0 * R * (d.H + a.n_out), 2.0 * R * d.H * a.n_out);
+        launch_pgemm<EPI_QKV>(pa, s);
+        ++n;
+    }
+    {
+        const double kvb = 2.0 * 4.0 * d.kvd * (prior + rows);
+        ProfScope ps(K_ATTN, s, kvb + 8.0 * R * d.qd, 4.0 * R * d.qd * (prior + rows));
+        int cap = 0;  // prompt passes are never graph-captured: size by the cache length
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        SFG_CUDA(cudaStreamIsCapturing(s, &cs));
+        if (cs == cudaStreamCaptureStatusNone) cap = prior + rows;
+        n += launch_attention_fast(ws.q, kc, vc, ws.row_off, ws.runs, rows, d, ws.att, ws.status, s, cap);
+    }
+    {  // O-proj + residual
+        pprep(ws.att, d.qd, d.qd, nullptr, 0.f);
+        PgArgs pa = args();
+        GemmArgs& a = pa.g;
+        a.W = static_cast<const uint8_t*>(L.f_o);
+        a.tiles = tiles_for(d.H);
+        a.KB = d.qd / kKB;
+        a.n_out = d.H;
+        a.out = ws.h;
+        a.ld = d.H;
+        a.store_only = e.tp_rank() > 0;
+        ProfScope ps(K_OPROJ, s, 2.0 * d.qd * d.H + 4.0 * R * (d.qd + 2.0 * d.H), 2.0 * R * d.qd * d.H);
+        launch_pgemm<EPI_RESID>(pa, s);
+        ++n;
+    }
+    e.tp_allreduce(ws.h, static_cast<size_t>(rows) * d.H, s);
+    {  // FFN RMSNorm + split, gate|up + SiLU*up
+        pprep(ws.h, d.H, d.H, L.ffn_norm, d.eps);
+        PgArgs pa = args();
+        GemmArgs& a = pa.g;
+        a.W = static_cast<const uint8_t*>(L.f_gu);
+        a.tiles = (d.F + 63) / 64;
+        a.KB = d.H / kKB;
+        a.n_out = d.F;
+        a.out = ws.act;
+        a.ld = d.F;
+        ProfScope ps(K_GATEUP, s, 4.0 * d.H * d.F + 4.0 * R * (d.H + d.F), 4.0 * R * d.H * d.F);
+        launch_pgemm<EPI_GATEUP>(pa, s);
+        ++n;
+    }
+    {  // down + residual
+        pprep(ws.act, d.F, d.F, nullptr, 0.f);
+        PgArgs pa = args();
+        GemmArgs& a = pa.g;
+        a.W = static_cast<const uint8_t*>(L.f_down);
+        a.tiles = tiles_for(d.H);
+        a.KB = d.F / kKB;
+        a.n_out = d.H;
+        a.out = ws.h;
+        a.ld = d.H;
+        a.store_only = e.tp_rank() > 0;
+        ProfScope ps(K_DOWN, s, 2.0 * d.F * d.H + 4.0 * R * (d.F + 2.0 * d.H), 2.0 * R * d.F * d.H);
+        launch_pgemm<EPI_RESID>(pa, s);
+        ++n;
+    }
+    e.tp_allreduce(ws.h, static_cast<size_t>(rows) * d.H, s);
+    SFG_CUDA(cudaGetLastError());
+    return n;
+}
+
 // One layer of forward_layers (tinyformer.cpp:412-504) in FAST math.
 int fast_forward_layer(Engine& e, Bank& b, int layer, int rows, Workspace& ws, int prior, cudaStream_t s) {
+    if (rows > kRows && prompt_tiles()) return fast_forward_layer_prompt(e, b, layer, rows, ws, prior, s);
     const ModelCfg& c = e.cfg();
     const Dims d = e.dims();
     const LayerWeights& L = e.layer(layer);
