@@ -204,7 +204,183 @@ int launch_hd(const float* q, const float* kc, const float* vc, const int32_t* r
     return 1;
 }
 
+// ── prompt (prefill) attention: tiled, K/V shared by a block of queries ──
+// attn_fast_kernel reads every visible K/V row once per (query row, kv head):
+// a 2048-token prompt moves ~16 GB per layer through L2.  Here a CTA takes 64
+// queries (64 / G consecutive rows x the G q-heads of one kv head) and walks
+// the keys in blocks of 64 at ABSOLUTE positions, staged in shared memory once
+// for all 64 queries: S = Q K^T by a 4 x 4 register tile per thread, an online
+// softmax per query in ascending block order, O += P V by a 4 x HD/16 tile.
+// Only the prefix mask law applies (every row sees keys [0, lim): causal
+// prompts, tinyformer.cpp:229-241); a row's result depends on its own query
+// and keys only, never on the rows it is tiled with.
+constexpr int kPQ = 64;   // queries per CTA
+constexpr int kPK = 64;   // keys per block
+
+template <int HD>
+__global__ void __launch_bounds__(256) attn_prompt_kernel(const float* __restrict__ q, const float* __restrict__ kc,
+                                                          const float* __restrict__ vc,
+                                                          const int32_t* __restrict__ row_off,
+                                                          const MaskRun* __restrict__ runs, Dims d, int rows,
+                                                          float* __restrict__ att, uint32_t* status) {
+    constexpr int DPT = HD / 16;  // value dims per thread
+    extern __shared__ float4 smem4[];
+    float* QT = reinterpret_cast<float*>(smem4);  // [HD][kPQ]
+    float* KT = QT + HD * kPQ;                     // [HD][kPK]
+    float* Vs = KT + HD * kPK;                     // [kPK][HD]
+    float* P = Vs + kPK * HD;                      // [kPQ][kPK + 4]
+    __shared__ int lim_s[kPQ];
+    const int G = d.n_heads / d.n_kv, RPB = kPQ / G;
+    const int rb0 = blockIdx.x * RPB, kvh = blockIdx.y;
+    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+    // query qi = g * RPB + r: row rb0 + r, head kvh * G + g
+    for (int idx = tid; idx < kPQ * HD; idx += 256) {
+        const int qi = idx % kPQ, dd = idx / kPQ, r = qi % RPB, g = qi / RPB, row = rb0 + r;
+        QT[dd * kPQ + qi] = row < rows ? q[static_cast<size_t>(row) * d.qd + static_cast<size_t>(kvh * G + g) * HD + dd]
+                                       : 0.0f;
+    }
+    if (tid < kPQ) {
+        const int row = rb0 + tid % RPB;
+        lim_s[tid] = row < rows ? runs[row_off[row]].end : 0;
+    }
+    __syncthreads();
+    int kmax = 0;
+    for (int i = 0; i < kPQ; ++i) kmax = max(kmax, lim_s[i]);
+    int lim[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) lim[i] = lim_s[4 * ty + i];
+    const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(HD));
+    const float* kb = kc + static_cast<size_t>(kvh) * d.max_len * HD;
+    const float* vb = vc + static_cast<size_t>(kvh) * d.max_len * HD;
+    float m[4], l[4], o[4][DPT];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        m[i] = -INFINITY;
+        l[i] = 0.0f;
+#pragma unroll
+        for (int c = 0; c < DPT; ++c) o[i][c] = 0.0f;
+    }
+    for (int k0 = 0; k0 < kmax; k0 += kPK) {
+        __syncthreads();  // the previous block's K / V / P are consumed
+        for (int idx = tid; idx < kPK * (HD / 4); idx += 256) {
+            const int kk = idx % kPK, d4 = idx / kPK, key = k0 + kk;
+            float4 kv = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (key < kmax) kv = __ldg(reinterpret_cast<const float4*>(kb + static_cast<size_t>(key) * HD) + d4);
+            KT[(4 * d4 + 0) * kPK + kk] = kv.x;
+            KT[(4 * d4 + 1) * kPK + kk] = kv.y;
+            KT[(4 * d4 + 2) * kPK + kk] = kv.z;
+            KT[(4 * d4 + 3) * kPK + kk] = kv.w;
+        }
+        for (int idx = tid; idx < kPK * (HD / 4); idx += 256) {
+            const int d4 = idx % (HD / 4), kk = idx / (HD / 4), key = k0 + kk;
+            reinterpret_cast<float4*>(Vs)[kk * (HD / 4) + d4] =
+                key < kmax ? __ldg(reinterpret_cast<const float4*>(vb + static_cast<size_t>(key) * HD) + d4)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncthreads();
+        float sc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) sc[i][j] = 0.0f;
+#pragma unroll 8
+        for (int dd = 0; dd < HD; ++dd) {
+            const float4 q4 = reinterpret_cast<const float4*>(QT + dd * kPQ)[ty];
+            const float4 k4 = reinterpret_cast<const float4*>(KT + dd * kPK)[tx];
+            const float qv[4] = {q4.x, q4.y, q4.z, q4.w}, kv[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) sc[i][j] += qv[i] * kv[j];
+        }
+        // online softmax per query (its 64 keys sit on the 16 tx lanes of its group)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            float bm = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int key = k0 + 4 * tx + j;
+                sc[i][j] = key < lim[i] ? sc[i][j] * inv_sqrt_hd : -INFINITY;
+                bm = fmaxf(bm, sc[i][j]);
+            }
+            for (int off = 8; off > 0; off >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, off));
+            const float mn = fmaxf(m[i], bm);
+            const float alpha = m[i] == -INFINITY ? 0.0f : sfg_expf(m[i] - mn);
+            float rs = 0.0f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float pj = sc[i][j] == -INFINITY ? 0.0f : sfg_expf(sc[i][j] - mn);
+                P[(4 * ty + i) * (kPK + 4) + 4 * tx + j] = pj;
+                rs += pj;
+            }
+            for (int off = 8; off > 0; off >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, off);
+            l[i] = l[i] * alpha + rs;
+            m[i] = mn;
+#pragma unroll
+            for (int c = 0; c < DPT; ++c) o[i][c] *= alpha;
+        }
+        __syncthreads();
+        // O += P V: rows 4ty..4ty+3, dims tx*DPT ..
+        for (int kk = 0; kk < kPK; ++kk) {
+            float pv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) pv[i] = P[(4 * ty + i) * (kPK + 4) + kk];
+            const float2* vr = reinterpret_cast<const float2*>(Vs + kk * HD + tx * DPT);
+#pragma unroll
+            for (int c2 = 0; c2 < DPT / 2; ++c2) {
+                const float2 v2 = vr[c2];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    o[i][2 * c2] += pv[i] * v2.x;
+                    o[i][2 * c2 + 1] += pv[i] * v2.y;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int qi = 4 * ty + i, r = qi % RPB, g = qi / RPB, row = rb0 + r;
+        if (row >= rows) continue;
+        if (!(l[i] > 0.0f)) {  // tinyformer.cpp:467-469
+            if (tx == 0) atomicOr(status, ST_EMPTY_ROW);
+            continue;
+        }
+        float* dst = att + static_cast<size_t>(row) * d.qd + static_cast<size_t>(kvh * G + g) * HD + tx * DPT;
+        const float inv = 1.0f / l[i];
+#pragma unroll
+        for (int c = 0; c < DPT; ++c) dst[c] = o[i][c] * inv;
+    }
+}
+
+template <int HD>
+int launch_prompt_hd(const float* q, const float* kc, const float* vc, const int32_t* row_off, const MaskRun* runs,
+                     int rows, const Dims& d, float* att, uint32_t* status, cudaStream_t s) {
+    const size_t smem = sizeof(float) * (static_cast<size_t>(HD) * kPQ + HD * kPK + kPK * HD + kPQ * (kPK + 4));
+    ensure_smem_attr(reinterpret_cast<const void*>(attn_prompt_kernel<HD>), smem);
+    const int rpb = kPQ / (d.n_heads / d.n_kv);
+    const dim3 grid((rows + rpb - 1) / rpb, d.n_kv);
+    attn_prompt_kernel<HD><<<grid, 256, smem, s>>>(q, kc, vc, row_off, runs, d, rows, att, status);
+    return 1;
+}
+
 }  // namespace
+
+// Prompt attention for masks of the prefix law (host-checked: every row one
+// run [0, lim) with value 0); other shapes take launch_attention_fast.
+bool attention_prompt_supported(const Dims& d) {
+    const int G = d.n_heads / d.n_kv;
+    return (d.hd == 64 || d.hd == 128 || d.hd == 160) && (G == 1 || G == 2 || G == 4 || G == 8);
+}
+
+int launch_attention_prompt(const float* q, const float* kcache, const float* vcache, const int32_t* row_off,
+                            const MaskRun* runs, int rows, const Dims& d, float* att, uint32_t* status,
+                            cudaStream_t s) {
+    switch (d.hd) {
+        case 64: return launch_prompt_hd<64>(q, kcache, vcache, row_off, runs, rows, d, att, status, s);
+        case 128: return launch_prompt_hd<128>(q, kcache, vcache, row_off, runs, rows, d, att, status, s);
+        default: return launch_prompt_hd<160>(q, kcache, vcache, row_off, runs, rows, d, att, status, s);
+    }
+}
 
 int launch_attention_fast(const float* q, const float* kcache, const float* vcache, const int32_t* row_off,
                           const MaskRun* runs, int rows, const Dims& d, float* att, uint32_t* status, cudaStream_t s,

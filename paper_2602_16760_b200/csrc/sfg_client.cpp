@@ -211,6 +211,7 @@ void Client::stage_inputs(int seq, const int32_t* ids, const int32_t* pos, const
     std::memcpy(p + L.roff, mr.row_off.data(), sizeof(int32_t) * mr.row_off.size());
     std::memcpy(p + L.runs, mr.runs.data(), sizeof(MaskRun) * mr.runs.size());
     ws.additive_mask = !mega_mask_ok(mr, prefix_->len());
+    ws.prefix_mask = prefix_law(mr);
 }
 
 // [inputs H2D] -> compaction -> embed -> prefix layers

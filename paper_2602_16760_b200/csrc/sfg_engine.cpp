@@ -69,6 +69,16 @@ ModelCfg ModelCfg::from_c(const sfg_model_config& c) {
 }
 
 // ── masks → runs ──────────────────────────────────────────────────────────
+bool prefix_law(const MaskRuns& mr) {
+    const int rows = static_cast<int>(mr.row_off.size()) - 1;
+    for (int i = 0; i < rows; ++i) {
+        if (mr.row_off[i + 1] - mr.row_off[i] != 1) return false;
+        const MaskRun& r = mr.runs[mr.row_off[i]];
+        if (r.start != 0 || r.end <= 0 || r.mval != 0.0f) return false;
+    }
+    return true;
+}
+
 bool mega_mask_ok(const MaskRuns& mr, int prior) {
     for (const MaskRun& r : mr.runs)
         if (r.mval != 0.0f) return false;
@@ -733,6 +743,7 @@ void Engine::forward_host(Bank& b, int lb, int le, int seq, const float* h, cons
     cudaStream_t s = b.stream();
     ensure_ws(ws, seq, static_cast<int>(mr.runs.size()), 0);
     ws.additive_mask = !mega_mask_ok(mr, prior);
+    ws.prefix_mask = prefix_law(mr);
     SFG_CUDA(cudaMemcpyAsync(ws.h, h, sizeof(float) * seq * H, cudaMemcpyHostToDevice, s));
     SFG_CUDA(cudaMemcpyAsync(ws.pos, pos, sizeof(int32_t) * seq, cudaMemcpyHostToDevice, s));
     SFG_CUDA(cudaMemcpyAsync(ws.row_off, mr.row_off.data(), sizeof(int32_t) * (seq + 1), cudaMemcpyHostToDevice, s));

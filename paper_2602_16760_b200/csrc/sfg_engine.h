@@ -104,6 +104,9 @@ struct Workspace {
     // column carries a non-zero (additive) value, or some row does not see the
     // whole cached prefix [0, prior) (see mega_mask_ok)
     bool additive_mask = false;
+    // every row sees exactly [0, lim) with mask value 0 (the causal prefix law
+    // of prompt passes): the tiled prompt attention applies
+    bool prefix_mask = false;
     void release();
 };
 
@@ -194,6 +197,8 @@ MaskRuns runs_from_dense(const float* mask, int rows, int kv);
 // and shares the cached prefix between rows: every row must see all of
 // [0, prior) with mask value 0 (causal, lookahead and branch masks do).
 bool mega_mask_ok(const MaskRuns& mr, int prior);
+// every row: one run [0, end) with value 0
+bool prefix_law(const MaskRuns& mr);
 
 // Tensor parallelism over NCCL (sfg_tp.cpp): a group of `size` engines, one
 // per GPU, each holding 1/size of every layer's heads and FFN columns.

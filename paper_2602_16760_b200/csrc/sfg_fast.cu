@@ -1014,11 +1014,15 @@ static int fast_forward_layer_prompt(Engine& e, Bank& b, int layer, int rows, Wo
     {
         const double kvb = 2.0 * 4.0 * d.kvd * (prior + rows);
         ProfScope ps(K_ATTN, s, kvb + 8.0 * R * d.qd, 4.0 * R * d.qd * (prior + rows));
-        int cap = 0;  // prompt passes are never graph-captured: size by the cache length
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        SFG_CUDA(cudaStreamIsCapturing(s, &cs));
-        if (cs == cudaStreamCaptureStatusNone) cap = prior + rows;
-        n += launch_attention_fast(ws.q, kc, vc, ws.row_off, ws.runs, rows, d, ws.att, ws.status, s, cap);
+        if (ws.prefix_mask && attention_prompt_supported(d)) {
+            n += launch_attention_prompt(ws.q, kc, vc, ws.row_off, ws.runs, rows, d, ws.att, ws.status, s);
+        } else {
+            int cap = 0;  // prompt passes are never graph-captured: size by the cache length
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            SFG_CUDA(cudaStreamIsCapturing(s, &cs));
+            if (cs == cudaStreamCaptureStatusNone) cap = prior + rows;
+            n += launch_attention_fast(ws.q, kc, vc, ws.row_off, ws.runs, rows, d, ws.att, ws.status, s, cap);
+        }
     }
     {  // O-proj + residual
         pprep(ws.att, d.qd, d.qd, nullptr, 0.f);

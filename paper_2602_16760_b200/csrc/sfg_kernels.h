@@ -73,6 +73,12 @@ int launch_matvec_store_exact(const float* x, int rows, int K, int wt, const voi
 int launch_attention_fast(const float* q, const float* kcache, const float* vcache,
                           const int32_t* row_off, const MaskRun* runs, int rows, const Dims& d,
                           float* att, uint32_t* status, cudaStream_t s, int kv_cap = 0);
+// prompt passes whose mask follows the prefix law (every row one run [0, lim),
+// value 0): K/V blocks staged once per 64 queries
+bool attention_prompt_supported(const Dims& d);
+int launch_attention_prompt(const float* q, const float* kcache, const float* vcache, const int32_t* row_off,
+                            const MaskRun* runs, int rows, const Dims& d, float* att, uint32_t* status,
+                            cudaStream_t s);
 
 // ── shared kernels (sfg_common.cu) ────────────────────────────────────────
 int launch_embed(const void* table, int wt, const int32_t* ids, int rows, int H, float* out,

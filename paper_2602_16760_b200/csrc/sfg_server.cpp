@@ -309,6 +309,7 @@ void Server::run(std::vector<StepState*>& group) {
     mr.row_off.push_back(static_cast<int32_t>(mr.runs.size()));
     upload_meta(eng_, ws, pos, mr, s);
     ws.additive_mask = k > 1 ? false : !mega_mask_ok(s0.mr, bank0.len());
+    ws.prefix_mask = k == 1 && prefix_law(s0.mr);
     char* wire = static_cast<char*>(ws.wire);
     for (int i = 0; i < k; ++i) {
         StepState& st = *group[i];
