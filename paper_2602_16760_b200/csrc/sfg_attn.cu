@@ -231,7 +231,8 @@ __global__ void __launch_bounds__(256) attn_prompt_kernel(const float* __restric
     float* P = Vs + kPK * HD;                      // [kPQ][kPK + 4]
     __shared__ int lim_s[kPQ];
     const int G = d.n_heads / d.n_kv, RPB = kPQ / G;
-    const int rb0 = blockIdx.x * RPB, kvh = blockIdx.y;
+    // the heaviest (latest, longest causal) row blocks are scheduled first
+    const int rb0 = (gridDim.x - 1 - blockIdx.x) * RPB, kvh = blockIdx.y;
     const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
     // query qi = g * RPB + r: row rb0 + r, head kvh * G + g
     for (int idx = tid; idx < kPQ * HD; idx += 256) {
@@ -305,11 +306,11 @@ __global__ void __launch_bounds__(256) attn_prompt_kernel(const float* __restric
             }
             for (int off = 8; off > 0; off >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, off));
             const float mn = fmaxf(m[i], bm);
-            const float alpha = m[i] == -INFINITY ? 0.0f : sfg_expf(m[i] - mn);
+            const float alpha = m[i] == -INFINITY ? 0.0f : expf(m[i] - mn);
             float rs = 0.0f;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const float pj = sc[i][j] == -INFINITY ? 0.0f : sfg_expf(sc[i][j] - mn);
+                const float pj = sc[i][j] == -INFINITY ? 0.0f : expf(sc[i][j] - mn);
                 P[(4 * ty + i) * (kPK + 4) + 4 * tx + j] = pj;
                 rs += pj;
             }

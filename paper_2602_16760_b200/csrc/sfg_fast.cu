@@ -512,11 +512,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 // reference, tests/test_gpu_fast.py, test_gpu_long_context.py).
 constexpr int kPT = 128;                     // tokens per tile (MMA N)
 constexpr int kPBBytes = kPT * kKB * 2;      // one piece of a k-block: 16 KB
-constexpr int kPStage = kABytes + 3 * kPBBytes;  // 64 KB
-constexpr int kPStages = 3;
+constexpr int kPTiles = 2;                   // weight tiles per item: they share every activation stage
+constexpr int kPStage = kPTiles * kABytes + 3 * kPBBytes;  // 80 KB
+constexpr int kPStages = 2;
 constexpr uint32_t kPIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kPT >> 3) << 17) |
                              (static_cast<uint32_t>(kM >> 4) << 24);
-constexpr size_t pgemm_smem_bytes() { return 1024 + static_cast<size_t>(kPStages) * kPStage + 2 * kPStages * 8 + 8 + 16 + (64 * kRows + 8 * kRows) * 4; }
+constexpr size_t pgemm_smem_bytes() { return 1024 + static_cast<size_t>(kPStages) * kPStage + 2 * kPStages * 8 + 4 * 8 + 16 + (64 * kRows + 8 * kRows) * 4; }
 
 struct PgArgs {
     GemmArgs g;           // weights, tiles, KB, n_out and the epilogue operands (row0/rows set per block)
@@ -542,25 +543,32 @@ __global__ void __launch_bounds__(kThreads, 1) pgemm_kernel(const __grid_constan
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kPStages * kPStage);
     uint64_t* empty = full + kPStages;
-    uint64_t* tfull = empty + kPStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+    uint64_t* tfull = empty + kPStages;   // [2] accumulator ready
+    uint64_t* tempty = tfull + 2;         // [2] accumulator drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     float* xch = reinterpret_cast<float*>(tmem_slot + 4);
     const GemmArgs& a = pa.g;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // item -> (weight tile, token tile): consecutive CTAs share a weight tile
-    const int t = blockIdx.x / pa.TT, j = blockIdx.x % pa.TT;
+    // persistent: item i = (weight tile pair i / TT, token tile i % TT); items
+    // of one CTA alternate between two TMEM accumulators so one item's
+    // epilogue overlaps the next item's MMAs
+    const int items = ((a.tiles + kPTiles - 1) / kPTiles) * pa.TT;
+    constexpr uint32_t kAccW = kPTiles * kPT;  // TMEM columns per accumulator
     if (threadIdx.x == 0) {
         for (int s = 0; s < kPStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tfull, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(kPT)
+                     "r"(2 * kAccW)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -572,65 +580,99 @@ __global__ void __launch_bounds__(kThreads, 1) pgemm_kernel(const __grid_constan
         if (lane == 0) {  // ── producer
             int stage = 0;
             uint32_t phase = 0;
-            for (int kb = 0; kb < a.KB; ++kb) {
-                mbar_wait(&empty[stage], phase ^ 1);
-                uint8_t* sa = smem + stage * kPStage;
-                mbar_expect_tx(&full[stage], kPStage);
-                bulk_g2s(sa, a.W + (static_cast<size_t>(t) * a.KB + kb) * kABytes, kABytes, &full[stage]);
-                bulk_g2s(sa + kABytes, pa.X + (static_cast<size_t>(j) * a.KB + kb) * 3 * kPBBytes, 3 * kPBBytes,
-                         &full[stage]);
-                if (++stage == kPStages) {
-                    stage = 0;
-                    phase ^= 1;
+            for (int it = blockIdx.x; it < items; it += gridDim.x) {
+                const int t0 = (it / pa.TT) * kPTiles, j = it % pa.TT, nt = min(kPTiles, a.tiles - t0);
+                for (int kb = 0; kb < a.KB; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * kPStage;
+                    mbar_expect_tx(&full[stage], nt * kABytes + 3 * kPBBytes);
+                    for (int i = 0; i < nt; ++i)
+                        bulk_g2s(sa + i * kABytes, a.W + (static_cast<size_t>(t0 + i) * a.KB + kb) * kABytes, kABytes,
+                                 &full[stage]);
+                    bulk_g2s(sa + kPTiles * kABytes, pa.X + (static_cast<size_t>(j) * a.KB + kb) * 3 * kPBBytes,
+                             3 * kPBBytes, &full[stage]);
+                    if (++stage == kPStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ── MMA issuer: hi, mid, lo into one accumulator per K=16 step
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int kb = 0; kb < a.KB; ++kb) {
-                mbar_wait(&full[stage], phase);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_ph = 0;
+            for (int it = blockIdx.x; it < items; it += gridDim.x) {
+                const int t0 = (it / pa.TT) * kPTiles, nt = min(kPTiles, a.tiles - t0);
+                mbar_wait(&tempty[acc], acc_ph ^ 1);
                 tc_fence_after();
-                const uint32_t sa = smem_u32(smem + stage * kPStage);
-                const uint64_t da = smem_desc(sa);
+                const uint32_t d0 = tmem + acc * kAccW;
+                for (int kb = 0; kb < a.KB; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + stage * kPStage);
 #pragma unroll
-                for (int k = 0; k < kKB / 16; ++k)
+                    for (int i = 0; i < kPTiles; ++i) {
+                        if (i >= nt) break;
+                        const uint64_t da = smem_desc(sa + i * kABytes);
 #pragma unroll
-                    for (int pc = 0; pc < 3; ++pc)
-                        mma_bf16_n128(tmem, da + 2 * k, smem_desc(sa + kABytes + pc * kPBBytes) + 2 * k,
-                                      (kb > 0 || k > 0 || pc > 0) ? 1u : 0u);
-                mma_commit(&empty[stage]);
-                if (++stage == kPStages) {
-                    stage = 0;
-                    phase ^= 1;
+                        for (int k = 0; k < kKB / 16; ++k)
+#pragma unroll
+                            for (int pc = 0; pc < 3; ++pc)
+                                mma_bf16_n128(d0 + i * kPT, da + 2 * k,
+                                              smem_desc(sa + kPTiles * kABytes + pc * kPBBytes) + 2 * k,
+                                              (kb > 0 || k > 0 || pc > 0) ? 1u : 0u);
+                    }
+                    mma_commit(&empty[stage]);
+                    if (++stage == kPStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit(&tfull[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_ph ^= 1;
                 }
             }
-            mma_commit(tfull);
         }
     } else {  // ── epilogue: 16-token blocks of the tile through the decode epilogues
         const int q = warp & 3;
         const int m = q * 32 + lane;
-        mbar_wait(tfull, 0);
-        tc_fence_after();
-        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16);
-        for (int b = 0; b < kPT / kRows; ++b) {
-            const int row0 = j * kPT + b * kRows;
-            if (row0 >= pa.total_rows) break;  // uniform over the epilogue warps
-            float y[kRows];
-            tmem_ld16(ta + b * kRows, y);
-            tmem_wait_ld();
-            GemmArgs ab = a;
-            ab.row0 = a.row0 + row0;
-            ab.rows = min(kRows, pa.total_rows - row0);
-            final_epilogue<EPI>(ab, t, m, y, xch);
+        int acc = 0;
+        uint32_t acc_ph = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x) {
+            const int t0 = (it / pa.TT) * kPTiles, j = it % pa.TT, nt = min(kPTiles, a.tiles - t0);
+            mbar_wait(&tfull[acc], acc_ph);
+            tc_fence_after();
+            for (int i = 0; i < nt; ++i) {
+                const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * kAccW + i * kPT;
+                for (int b = 0; b < kPT / kRows; ++b) {
+                    const int row0 = j * kPT + b * kRows;
+                    if (row0 >= pa.total_rows) break;  // uniform over the epilogue warps
+                    float y[kRows];
+                    tmem_ld16(ta + b * kRows, y);
+                    tmem_wait_ld();
+                    GemmArgs ab = a;
+                    ab.row0 = a.row0 + row0;
+                    ab.rows = min(kRows, pa.total_rows - row0);
+                    final_epilogue<EPI>(ab, t0 + i, m, y, xch);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) {
+                acc = 0;
+                acc_ph ^= 1;
+            }
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kPT) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kAccW) : "memory");
     }
 }
 
@@ -682,7 +724,8 @@ __global__ void __launch_bounds__(256) pprep_kernel(const float* __restrict__ x,
 template <int EPI>
 void launch_pgemm(const PgArgs& pa, cudaStream_t s) {
     ensure_smem_attr(reinterpret_cast<const void*>(pgemm_kernel<EPI>), pgemm_smem_bytes());
-    pgemm_kernel<EPI><<<pa.g.tiles * pa.TT, kThreads, pgemm_smem_bytes(), s>>>(pa);
+    const int items = ((pa.g.tiles + kPTiles - 1) / kPTiles) * pa.TT;
+    pgemm_kernel<EPI><<<std::min(items, device_sm_count()), kThreads, pgemm_smem_bytes(), s>>>(pa);
 }
 
 // ── activation prologue: [RMSNorm] + 3-way bf16 split into the swizzled B image
