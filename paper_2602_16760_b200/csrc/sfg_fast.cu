@@ -521,6 +521,7 @@ constexpr size_t pgemm_smem_bytes() { return 1024 + static_cast<size_t>(kPStages
 
 struct PgArgs {
     GemmArgs g;           // weights, tiles, KB, n_out and the epilogue operands (row0/rows set per block)
+    int tpi;              // weight tiles per item (1 or kPTiles): 2 when there are enough items to fill the SMs
     const uint8_t* X;     // [TT][KB][3][kPT x 64] bf16 SW128 (hi | mid | lo)
     int TT;               // token tiles
     int total_rows;       // prompt rows of this pass
@@ -552,7 +553,8 @@ __global__ void __launch_bounds__(kThreads, 1) pgemm_kernel(const __grid_constan
     // persistent: item i = (weight tile pair i / TT, token tile i % TT); items
     // of one CTA alternate between two TMEM accumulators so one item's
     // epilogue overlaps the next item's MMAs
-    const int items = ((a.tiles + kPTiles - 1) / kPTiles) * pa.TT;
+    const int tpi = pa.tpi;
+    const int items = ((a.tiles + tpi - 1) / tpi) * pa.TT;
     constexpr uint32_t kAccW = kPTiles * kPT;  // TMEM columns per accumulator
     if (threadIdx.x == 0) {
         for (int s = 0; s < kPStages; ++s) {
@@ -581,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1) pgemm_kernel(const __grid_constan
             int stage = 0;
             uint32_t phase = 0;
             for (int it = blockIdx.x; it < items; it += gridDim.x) {
-                const int t0 = (it / pa.TT) * kPTiles, j = it % pa.TT, nt = min(kPTiles, a.tiles - t0);
+                const int t0 = (it / pa.TT) * tpi, j = it % pa.TT, nt = min(tpi, a.tiles - t0);
                 for (int kb = 0; kb < a.KB; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * kPStage;
@@ -603,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1) pgemm_kernel(const __grid_constan
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_ph = 0;
             for (int it = blockIdx.x; it < items; it += gridDim.x) {
-                const int t0 = (it / pa.TT) * kPTiles, nt = min(kPTiles, a.tiles - t0);
+                const int t0 = (it / pa.TT) * tpi, nt = min(tpi, a.tiles - t0);
                 mbar_wait(&tempty[acc], acc_ph ^ 1);
                 tc_fence_after();
                 const uint32_t d0 = tmem + acc * kAccW;
@@ -642,7 +644,7 @@ __global__ void __launch_bounds__(kThreads, 1) pgemm_kernel(const __grid_constan
         int acc = 0;
         uint32_t acc_ph = 0;
         for (int it = blockIdx.x; it < items; it += gridDim.x) {
-            const int t0 = (it / pa.TT) * kPTiles, j = it % pa.TT, nt = min(kPTiles, a.tiles - t0);
+            const int t0 = (it / pa.TT) * tpi, j = it % pa.TT, nt = min(tpi, a.tiles - t0);
             mbar_wait(&tfull[acc], acc_ph);
             tc_fence_after();
             for (int i = 0; i < nt; ++i) {
@@ -724,8 +726,12 @@ __global__ void __launch_bounds__(256) pprep_kernel(const float* __restrict__ x,
 template <int EPI>
 void launch_pgemm(const PgArgs& pa, cudaStream_t s) {
     ensure_smem_attr(reinterpret_cast<const void*>(pgemm_kernel<EPI>), pgemm_smem_bytes());
-    const int items = ((pa.g.tiles + kPTiles - 1) / kPTiles) * pa.TT;
-    pgemm_kernel<EPI><<<std::min(items, device_sm_count()), kThreads, pgemm_smem_bytes(), s>>>(pa);
+    PgArgs p = pa;
+    const int nsm = device_sm_count();
+    // two weight tiles per item when that still leaves >= one item per SM
+    p.tpi = ((pa.g.tiles + kPTiles - 1) / kPTiles) * pa.TT >= nsm ? kPTiles : 1;
+    const int items = ((pa.g.tiles + p.tpi - 1) / p.tpi) * pa.TT;
+    pgemm_kernel<EPI><<<std::min(items, nsm), kThreads, pgemm_smem_bytes(), s>>>(p);
 }
 
 // ── activation prologue: [RMSNorm] + 3-way bf16 split into the swizzled B image
