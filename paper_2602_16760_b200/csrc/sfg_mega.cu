@@ -127,7 +127,7 @@ struct MegaArgs {
     float* peer_inbox;     // the peer's (mapped)
     unsigned* peer_inflag;
     unsigned* epoch_ptr;   // launch counter
-    float* apart;      // attention chunk partials [n_kv][ceil(max_len/kKeyChunk)][128 queries][hd + 2]
+    float* apart;      // attention chunk partials [n_kv][ceil(max_len/kAttnMinKC)][128 queries][hd + 2]
     unsigned* acnt;    // [n_kv] chunk arrival counters (reset by the merging chunk)
     // optional [G][kBarSlots][kTraceW] (tools/trace_mega.py): per CTA and
     // barrier id, globaltimer stamps and wait totals (see tslot users)
@@ -314,7 +314,7 @@ __device__ __forceinline__ bool xblock_ready(const MegaArgs& a, int l, int p, in
             const int group = a.n_heads / a.n_kv;
             const int h0 = (kb * kKB) / a.hd / group, h1 = (kb * kKB + kKB - 1) / a.hd / group;
             for (int h = h0; h <= h1; ++h)
-                if (ld_acquire(fptr(a, l, K_ATT, h)) < static_cast<unsigned>(a.rows)) return false;
+                if (ld_acquire(fptr(a, l, K_ATT, h)) < static_cast<unsigned>(a.rows * group)) return false;
             return true;
         }
         case P_GU: return ld_acquire(fptr(a, l, K_O, kb >> 1)) >= 1u;
@@ -349,6 +349,16 @@ __device__ __forceinline__ void mwait(uint64_t* b, uint32_t parity) {
             : "memory");
         if (done) return;
         if (++spins > (1ull << 26)) asm volatile("trap;");
+    }
+}
+
+// long waits (the lent ring): poll with back-off so the waiting thread does
+// not compete with the attention warps for the shared-memory pipe
+__device__ __forceinline__ void mwait_sleep(uint64_t* b, uint32_t parity) {
+    unsigned long long spins = 0;
+    while (!mbar_test(b, parity)) {
+        __nanosleep(256);
+        if (++spins > (1ull << 24)) asm volatile("trap;");
     }
 }
 
@@ -722,310 +732,380 @@ __device__ __forceinline__ void attention_rows_dispatch(const MegaArgs& a, const
             default: attention_row_item<32, 8, R>(a, L, l, row, kvh, at, qs, wst, ocomb, cols); break;
         }
     }
-    if (at == 0) signal_add(fptr(a, l, K_ATT, kvh), 1u);  // item's att rows + image are published
+    if (at == 0) signal_add(fptr(a, l, K_ATT, kvh), static_cast<unsigned>(a.n_heads / a.n_kv));  // the row's queries are published
 }
 
-// ── attention over the KV cache ─────────────────────────────────────────
-// Work item = (kv head, key chunk, query group).  A chunk is kKeyChunk keys at
-// ABSOLUTE positions, walked in blocks of kKeyBlock keys that the whole CTA
-// stages into shared memory once (cp.async) and shares across its queries
-// (rows x the group's q heads; each warp owns QPW of them).  Blocks are
-// combined in key order with an online softmax, invisible keys contribute
-// exact zeros, and several chunks of a head are merged in chunk order by the
-// last one to finish: a row's result does not depend on the batch around it
-// (lookahead == sequential, bitwise) nor on how queries are grouped.
-constexpr int kKeyChunk = 128;
-constexpr int kKeyBlock = 16;
-
-__device__ __forceinline__ bool key_visible(const MegaArgs& a, int row, int key) {
-    const int r0 = a.row_off[row], r1 = a.row_off[row + 1];
-    for (int i = r0; i < r1; ++i) {
-        const MaskRun rr = a.runs[i];
-        if (key >= rr.start && key < rr.end) return true;
-    }
-    return false;
+// ── attention over the KV cache for long contexts (SFG_ATTN=chunked) ─────
+// Work item = (kv head, chunk of KC keys in COMPACTED order, group of up to
+// 64 queries = rows x the head group's q heads).  The CTA's weight ring is
+// idle during the attention phase -- the producer drains it and lends it
+// (see lend_ring) -- so an item stages its whole chunk in the ring's shared
+// memory with all 256 attention threads issuing cp.async at once (K, the
+// queries and the rows' tail slots in one group, V in a second that lands
+// while the scores are computed).  K/V are read ONCE per head for all of its
+// queries.
+//   scores: warp w owns item queries 8w..8w+7, lane owns keys lane + 32j (an
+//           8 x KC/32 register tile; K float4 columns XOR-swizzled by key so
+//           the 32 lanes' rows hit distinct banks, queries are broadcast);
+//   softmax per query over the chunk: fixed butterfly over the lanes;
+//   P^T [key][64 queries] overwrites the queries; PV: warp w, lane = head
+//           dims lane + 32d, keys in compacted order.
+// Compacted index i < prior is cache slot i (shared by every row); i >= prior
+// is the row's own tail slot, read from a per-row K/V row with the SAME fmaf
+// sequence, so a row's result depends only on its own compacted key list:
+// lookahead == sequential bitwise, independent of the batch.  Chunks of a
+// head merge in chunk order (last arriver).
+template <int HD>
+__host__ __device__ constexpr int attn_kc() { return HD <= 128 ? 128 : 64; }
+constexpr int kAttnMinKC = 64;  // chunk-slot stride of the partials buffer (smallest KC)
+// shared-memory floats an item needs inside the lent ring
+__host__ __device__ constexpr int attn_lend_floats(int hd, int kc) {
+    return 2 * kc * hd + (64 * hd > kc * 64 ? 64 * hd : kc * 64) + 2 * kRows * hd;
+}
+// packed fp32 FMA (sm_100 FFMA2): (d0, d1) += (a0, a1) * (b0, b1), each lane an IEEE fma
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+    asm("{\n.reg .b64 ra, rb, rd;\n"
+        "mov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\nmov.b64 rd, {%0, %1};\n"
+        "fma.rn.f32x2 rd, ra, rb, rd;\nmov.b64 {%0, %1}, rd;\n}"
+        : "+f"(d0), "+f"(d1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+// score partials over a float4 of head dims: even dims into se, odd into so
+// (the dot product is se + so at the end; one fixed order for every path)
+__device__ __forceinline__ void dot4x2(float& se, float& so, const float4 q, const float4 k) {
+    ffma2(se, so, q.x, q.y, k.x, k.y);
+    ffma2(se, so, q.z, q.w, k.z, k.w);
 }
 
-template <int HD, int QPW>
-__device__ __noinline__ void attention_chunk(const MegaArgs& a, const LayerDesc& L, int l, int kvh, int chunk, int nchunks,
-                                int qg, int at, float* sq, float* sp, float* skv, float* part, unsigned* acnt,
-                                int* flag) {
-    constexpr int QI = 8 * QPW;    // queries per item
-    constexpr int C4 = HD / 4;     // float4 columns per key row
-    constexpr int DPL = HD / 32;   // value dims per lane
-    constexpr int HH = HD / 2;     // score dims per lane (2 lanes per key)
+// the kernel's dynamic shared memory, named here so the attention phase
+// (a separate, non-inlined function) addresses the lent ring as SHARED
+// memory (LDS / STS) instead of through generic pointers
+extern __shared__ __align__(1024) uint8_t mega_dyn_smem[];
+__device__ __forceinline__ float* ring_base() {
+    // 1024-byte aligned (SW128 operands); pointer arithmetic keeps the address space
+    const uint32_t mis = static_cast<uint32_t>(__cvta_generic_to_shared(mega_dyn_smem)) & 1023u;
+    return reinterpret_cast<float*>(mega_dyn_smem + ((1024u - mis) & 1023u));
+}
+
+template <int HD>
+__device__ __noinline__ void attention_tile(const MegaArgs& a, int l, int kvh, int chunk, int nchunks, int qg, int at,
+                                            float* part, int xoff) {
+    float* ring = ring_base();
+    float* sTS = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ring) + xoff);  // [64][16] tail scores (epilogue scratch)
+    constexpr int KC = attn_kc<HD>();
+    constexpr int KPL = KC / 32;  // keys per lane in the score tile
+    constexpr int C4 = HD / 4;    // float4 columns per K / V / query row
+    constexpr int DPL = HD / 32;  // head dims per lane in PV
     const int group = a.n_heads / a.n_kv;
-    const int NQ = a.rows * group;  // query q = row * group + g
-    const int qbase = qg * QI;
-    const int nq = min(QI, NQ - qbase);
+    const int NQ = a.rows * group;  // item query q = row * group + g
+    const int qbase = qg * 64, nq = min(64, NQ - qbase);
     const int warp = at >> 5, lane = at & 31;
     const int prior = sh_prior;
     const int ncmax = prior + a.rows;  // bound on every row's compacted key count
-    // keys are walked in each row's COMPACTED order: index i < prior is cache
-    // slot i (shared by every row), i >= prior is the row's own tail slot
-    const int k0 = chunk * kKeyChunk, k1 = min(ncmax, k0 + kKeyChunk);
-    for (int t = at; t < nq * HD; t += 256) {
-        const int q = qbase + t / HD, d = t % HD, r = q / group, g = q % group;
-        sq[t] = __ldcg(a.q + static_cast<size_t>(r) * a.qd + static_cast<size_t>(kvh * group + g) * HD + d);
+    const int k0 = chunk * KC, k1 = min(ncmax, k0 + KC);
+    const int ns = max(0, min(k1, prior) - k0);  // shared-prefix keys [k0, k0 + ns)
+    const int kt0 = max(k0, prior);              // tail indices [kt0, k1)
+    float* sK = ring;                 // [KC][C4] float4, column c of key j at c ^ (j & 7)
+    float* sV = sK + KC * HD;         // [KC][HD]
+    float* sQ = sV + KC * HD;         // [64][HD] queries, then P^T [KC][64] (float4 chunk h of key j at h ^ (j & 15))
+    float* sKt = sQ + (64 * HD > KC * 64 ? 64 * HD : KC * 64);  // tail slots prior.. : [kRows][HD]
+    float* sVt = sKt + kRows * HD;
+    const size_t hoff = static_cast<size_t>(l) * a.slab_stride + static_cast<size_t>(kvh) * a.max_len * HD;
+    const float* kbase = a.kbank[0] + hoff;
+    const float* vbase = a.vbank[0] + hoff;
+    float4* sK4 = reinterpret_cast<float4*>(sK);
+    float4* sQ4 = reinterpret_cast<float4*>(sQ);
+    for (int t = at; t < ns * C4; t += 256) {
+        const int j = t / C4, c4 = t % C4;
+        cp_async16(sK4 + j * C4 + (c4 ^ (j & 7)), kbase + static_cast<size_t>(k0 + j) * HD + 4 * c4);
     }
-    const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(HD));
-    const float* kbase = a.kbank[0] + static_cast<size_t>(l) * a.slab_stride + static_cast<size_t>(kvh) * a.max_len * HD;
-    const float* vbase = a.vbank[0] + static_cast<size_t>(l) * a.slab_stride + static_cast<size_t>(kvh) * a.max_len * HD;
-    float* sk = skv;                          // 2 x { K [kKeyBlock][C4] float4 (XOR-swizzled by row & 7) | V }
-    float* skt = sk + 4 * kKeyBlock * HD;     // tail slots [prior, prior + rows): K (swizzled) | V
-    float* svt = skt + kRows * HD;
-    const int q0 = warp * QPW;                // the warp's queries (item-local)
-    const int key_l = lane & 15, half = lane >> 4;
-    if (k1 > prior) {  // this chunk reaches the rows' own tails: stage them once
-        for (int t = at; t < kRows * C4; t += 256) {
+    for (int t = at; t < nq * C4; t += 256) {
+        const int qi = t / C4, c4 = t % C4, q = qbase + qi, r = q / group, g = q % group;
+        cp_async16(sQ4 + qi * C4 + c4, a.q + static_cast<size_t>(r) * a.qd + static_cast<size_t>(kvh * group + g) * HD + 4 * c4);
+    }
+    if (k1 > prior)
+        for (int t = at; t < a.rows * C4; t += 256) {
             const int j = t / C4, c4 = t % C4;
-            float4* dk = reinterpret_cast<float4*>(skt) + j * C4 + (c4 ^ (j & 7));
-            float4* dv = reinterpret_cast<float4*>(svt) + j * C4 + c4;
-            if (j < a.rows) {
-                cp_async16(dk, kbase + static_cast<size_t>(prior + j) * HD + 4 * c4);
-                cp_async16(dv, vbase + static_cast<size_t>(prior + j) * HD + 4 * c4);
-            } else {
-                *dk = make_float4(0.f, 0.f, 0.f, 0.f);
-                *dv = make_float4(0.f, 0.f, 0.f, 0.f);
+            cp_async16(reinterpret_cast<float4*>(sKt) + j * C4 + (c4 ^ (j & 7)), kbase + static_cast<size_t>(prior + j) * HD + 4 * c4);
+            cp_async16(reinterpret_cast<float4*>(sVt) + t, vbase + static_cast<size_t>(prior + j) * HD + 4 * c4);
+        }
+    cp_async_commit();
+    for (int t = at; t < ns * C4; t += 256)
+        cp_async16(reinterpret_cast<float4*>(sV) + t, vbase + static_cast<size_t>(k0) * HD + 4 * t);
+    cp_async_commit();
+    const bool tr = a.trace && at == 0;
+    if (tr) *tslot(a, blockIdx.x, 230 + l, 0) = gtimer();
+    cp_async_wait_1();
+    named_sync(3, 256);
+    if (tr) *tslot(a, blockIdx.x, 230 + l, 1) = gtimer();
+    const int q0 = warp * 8;  // this warp's item queries
+    const bool wq = q0 < nq;
+    float s[8][KPL];
+    float mx[8], sm[8];
+    if (wq) {
+        // shared keys: every query of the warp against the lane's KPL keys
+        float so[8][KPL];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < KPL; ++j) s[i][j] = so[i][j] = 0.0f;
+#pragma unroll 2
+        for (int c = 0; c < C4; ++c) {
+            float4 k4[KPL];
+#pragma unroll
+            for (int j = 0; j < KPL; ++j) k4[j] = sK4[(lane + 32 * j) * C4 + (c ^ (lane & 7))];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float4 q4 = sQ4[(q0 + i) * C4 + c];
+#pragma unroll
+                for (int j = 0; j < KPL; ++j) dot4x2(s[i][j], so[i][j], q4, k4[j]);
             }
         }
-        cp_async_commit();
-    }
-    float m_run[QPW], l_run[QPW], o[QPW][DPL];
 #pragma unroll
-    for (int i = 0; i < QPW; ++i) {
-        m_run[i] = -INFINITY;
-        l_run[i] = 0.0f;
+        for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < DPL; ++j) o[i][j] = 0.0f;
+            for (int j = 0; j < KPL; ++j) s[i][j] += so[i][j];
     }
-    float* myp = sp + warp * QPW * kKeyBlock;
-    // K/V blocks are double buffered: block b+1 streams in while b is scored
-    auto stage = [&](int kb0, int buf) {
-        float* bk = sk + buf * 2 * kKeyBlock * HD;
-        float* bv = bk + kKeyBlock * HD;
-        const int np = max(0, min(kKeyBlock, prior - kb0));
-        for (int t = at; t < kKeyBlock * C4; t += 256) {
-            const int j = t / C4, c4 = t % C4;
-            float4* dk = reinterpret_cast<float4*>(bk) + j * C4 + (c4 ^ (j & 7));
-            float4* dv = reinterpret_cast<float4*>(bv) + j * C4 + c4;
-            if (j < np) {
-                cp_async16(dk, kbase + static_cast<size_t>(kb0 + j) * HD + 4 * c4);
-                cp_async16(dv, vbase + static_cast<size_t>(kb0 + j) * HD + 4 * c4);
-            } else {
-                *dk = make_float4(0.f, 0.f, 0.f, 0.f);
-                *dv = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        }
-        cp_async_commit();
-    };
-    if (a.trace && at == 0) *tslot(a, blockIdx.x, 5 * l + 2, 12) = gtimer();
-    if (k0 < k1) stage(k0, 0);
-    int buf = 0;
-    for (int kb0 = k0; kb0 < k1; kb0 += kKeyBlock, buf ^= 1) {
-        const int np = max(0, min(kKeyBlock, prior - kb0));  // shared-prefix keys of this block
-        if (kb0 + kKeyBlock < k1) {
-            stage(kb0 + kKeyBlock, buf ^ 1);
-            cp_async_wait_1();
-        } else {
-            cp_async_wait_all();
+    // tail keys (compacted indices >= prior, row-specific K rows): every (query,
+    // tail) pair by all 256 threads, the SAME dot4x2 sequence as a shared key
+    const int ntail = k1 - kt0;
+    if (ntail > 0) {
+        const float4* sKt4 = reinterpret_cast<const float4*>(sKt);
+        for (int pi = at; pi < nq * ntail; pi += 256) {
+            const int qi = pi / ntail, t = pi % ntail;
+            const int ts = sh_tail[(qbase + qi) / group][min(kt0 - prior + t, kRows - 1)] - prior;  // K rows swizzled by ts
+            float acc = 0.0f, acco = 0.0f;
+#pragma unroll 4
+            for (int c = 0; c < C4; ++c) dot4x2(acc, acco, sQ4[qi * C4 + c], sKt4[ts * C4 + (c ^ (ts & 7))]);
+            sTS[qi * 16 + t] = acc + acco;
         }
         named_sync(3, 256);
-        const float* bk = sk + buf * 2 * kKeyBlock * HD;
-        const float* bv = bk + kKeyBlock * HD;
-        if (q0 < nq) {
-            const int ci = kb0 + key_l;  // this lane's compacted key index
-            float sc[QPW];
-#pragma unroll
-            for (int i = 0; i < QPW; ++i) sc[i] = 0.0f;
-            if (np == kKeyBlock) {  // shared prefix: one K row per lane for every query
-                const float4* kr = reinterpret_cast<const float4*>(bk) + key_l * C4;
-                const int sw = key_l & 7;
-#pragma unroll 4
-                for (int c = 0; c < HH / 4; ++c) {
-                    const int c4 = half * (HH / 4) + c;
-                    const float4 k4 = kr[c4 ^ sw];
-#pragma unroll
-                    for (int i = 0; i < QPW; ++i) {
-                        const float4 q4 = reinterpret_cast<const float4*>(sq + (q0 + i) * HD)[c4];
-                        sc[i] += q4.x * k4.x + q4.y * k4.y + q4.z * k4.z + q4.w * k4.w;
-                    }
-                }
-            } else {  // block reaching the rows' tails: K row per query row
-#pragma unroll
-                for (int i = 0; i < QPW; ++i) {
-                    const float4* kr;
-                    int sw;
-                    if (ci < prior) {
-                        kr = reinterpret_cast<const float4*>(bk) + key_l * C4;
-                        sw = key_l & 7;
-                    } else {
-                        const int r = (qbase + q0 + min(i, nq - 1 - q0)) / group;
-                        const int t = ci - prior < kRows ? sh_tail[r][ci - prior] - prior : 0;
-                        kr = reinterpret_cast<const float4*>(skt) + t * C4;
-                        sw = t & 7;
-                    }
-#pragma unroll 4
-                    for (int c = 0; c < HH / 4; ++c) {
-                        const int c4 = half * (HH / 4) + c;
-                        const float4 k4 = kr[c4 ^ sw];
-                        const float4 q4 = reinterpret_cast<const float4*>(sq + (q0 + i) * HD)[c4];
-                        sc[i] += q4.x * k4.x + q4.y * k4.y + q4.z * k4.z + q4.w * k4.w;
-                    }
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < QPW; ++i) {
-                sc[i] += __shfl_xor_sync(0xffffffffu, sc[i], 16);
-                const int q = qbase + q0 + i;
-                const bool vis = q0 + i < nq && ci < sh_ncols[q / group];
-                const float s = vis ? sc[i] * inv_sqrt_hd : -INFINITY;
-                float mb = s;
-                for (int off = 8; off > 0; off >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, off));
-                const float mn = fmaxf(m_run[i], mb);
-                const float scale_old = m_run[i] == -INFINITY ? (mn == -INFINITY ? 1.0f : 0.0f) : expf(m_run[i] - mn);
-                const float pj = vis ? expf(s - mn) : 0.0f;
-                float ps = pj;
-                for (int off = 8; off > 0; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
-                l_run[i] = l_run[i] * scale_old + ps;
-                m_run[i] = mn;
-#pragma unroll
-                for (int j = 0; j < DPL; ++j) o[i][j] *= scale_old;
-                if (half == 0) myp[i * kKeyBlock + key_l] = pj;
-            }
-            __syncwarp();
-            // values: lane = dims, the block's keys in compacted order
-            if (np == kKeyBlock) {  // shared prefix block: one V row for every query
-#pragma unroll 4
-                for (int j = 0; j < kKeyBlock; ++j) {
-                    float v[DPL];
-#pragma unroll
-                    for (int dd = 0; dd < DPL; ++dd) v[dd] = bv[j * HD + lane + 32 * dd];
-#pragma unroll
-                    for (int i = 0; i < QPW; ++i) {
-                        const float pj = myp[i * kKeyBlock + j];
-#pragma unroll
-                        for (int dd = 0; dd < DPL; ++dd) o[i][dd] += pj * v[dd];
-                    }
-                }
-            } else {
-                for (int j = 0; j < kKeyBlock; ++j) {
-                    const int cj = kb0 + j;
-#pragma unroll
-                    for (int i = 0; i < QPW; ++i) {
-                        const int r = (qbase + q0 + min(i, nq - 1 - q0)) / group;
-                        const float* vr = cj < prior ? bv + j * HD
-                                                     : svt + (cj - prior < kRows ? sh_tail[r][cj - prior] - prior : 0) * HD;
-                        const float pj = myp[i * kKeyBlock + j];
-#pragma unroll
-                        for (int dd = 0; dd < DPL; ++dd) o[i][dd] += pj * vr[lane + 32 * dd];
-                    }
-                }
-            }
-        }
-        named_sync(3, 256);  // the buffer is restaged two blocks later
     }
-    // publish: one chunk -> final values; several -> partials, the last chunk merges
-    auto finish = [&](int q, float lsum, const float* ov) {
-        const int r = q / group, g = q % group;
-        if (!(lsum > 0.0f) && lane == 0) atomicOr(a.status, ST_EMPTY_ROW);
+    if (wq) {
 #pragma unroll
-        for (int dd = 0; dd < DPL; ++dd) {
-            const int d = lane + 32 * dd;
-            const float val = ov[dd] / lsum;
-            const int f = (kvh * group + g) * HD + d;
-            a.att[static_cast<size_t>(r) * a.qd + f] = val;
-            put_split<kRows>(a.xim[P_O], f, r, val);
+        for (int j = 0; j < KPL; ++j) {
+            const int ki = k0 + lane + 32 * j;
+            if (ki >= kt0 && ki < k1)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) s[i][j] = sTS[(q0 + i) * 16 + (ki - kt0)];
         }
-    };
-    if (a.trace && at == 0) *tslot(a, blockIdx.x, 5 * l + 2, 13) = gtimer();
-    const int cpk = (a.max_len + kKeyChunk - 1) / kKeyChunk;  // chunk slots per kv head
-    const size_t qstride = HD + 2;
-    if (nchunks > 1) {
-        float* pc = part + (static_cast<size_t>(kvh) * cpk + chunk) * 128 * qstride;
+        const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(HD));
 #pragma unroll
-        for (int i = 0; i < QPW; ++i) {
+        for (int i = 0; i < 8; ++i) {
             const int q = qbase + q0 + i;
-            if (q0 + i >= nq) continue;
-            float* dst = pc + q * qstride;
-            if (lane == 0) {
-                dst[0] = m_run[i];
-                dst[1] = l_run[i];
+            const int nc = q < NQ ? sh_ncols[q / group] : 0;  // the row's compacted key count
+            float m = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < KPL; ++j) {
+                const int ki = k0 + lane + 32 * j;
+                s[i][j] = (ki < k1 && ki < nc) ? s[i][j] * inv_sqrt_hd : -INFINITY;
+                m = fmaxf(m, s[i][j]);
             }
 #pragma unroll
-            for (int dd = 0; dd < DPL; ++dd) dst[2 + lane + 32 * dd] = o[i][dd];
+            for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+            float sum = 0.0f;
+#pragma unroll
+            for (int j = 0; j < KPL; ++j) {
+                const float p = s[i][j] == -INFINITY ? 0.0f : expf(s[i][j] - m);
+                s[i][j] = p;
+                sum += p;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+            mx[i] = m;
+            sm[i] = sum;
         }
-        __threadfence();
+    }
+    named_sync(3, 256);  // every warp is done with the queries: P^T overwrites them
+    if (tr) *tslot(a, blockIdx.x, 230 + l, 2) = gtimer();
+    if (wq) {
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) {
+            const int key = lane + 32 * j, sw = key & 15;
+            sQ4[key * 16 + ((q0 >> 2) ^ sw)] = make_float4(s[0][j], s[1][j], s[2][j], s[3][j]);
+            sQ4[key * 16 + (((q0 >> 2) + 1) ^ sw)] = make_float4(s[4][j], s[5][j], s[6][j], s[7][j]);
+        }
+    }
+    cp_async_wait_all();
+    named_sync(3, 256);
+    if (tr) *tslot(a, blockIdx.x, 230 + l, 3) = gtimer();
+    float o[8][DPL];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int d = 0; d < DPL; ++d) o[i][d] = 0.0f;
+    if (wq) {
+#pragma unroll 4
+        for (int j = 0; j < ns; ++j) {
+            const float4 p0 = sQ4[j * 16 + ((q0 >> 2) ^ (j & 15))];
+            const float4 p1 = sQ4[j * 16 + (((q0 >> 2) + 1) ^ (j & 15))];
+            const float pp[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+            float v[DPL];
+#pragma unroll
+            for (int d = 0; d < DPL; ++d) v[d] = sV[j * HD + lane + 32 * d];
+#pragma unroll
+            for (int i = 0; i < 8; i += 2)
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) ffma2(o[i][d], o[i + 1][d], pp[i], pp[i + 1], v[d], v[d]);
+        }
+        for (int ki = kt0; ki < k1; ++ki) {  // tail keys: each query's own V row
+            const int j = ki - k0;
+            const float4 p0 = sQ4[j * 16 + ((q0 >> 2) ^ (j & 15))];
+            const float4 p1 = sQ4[j * 16 + (((q0 >> 2) + 1) ^ (j & 15))];
+            const float pp[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int r = min(qbase + q0 + i, NQ - 1) / group;
+                const float* vr = sVt + (sh_tail[r][min(ki - prior, kRows - 1)] - prior) * HD;
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) o[i][d] = fmaf(pp[i], vr[lane + 32 * d], o[i][d]);
+            }
+        }
+    }
+    if (tr) *tslot(a, blockIdx.x, 230 + l, 5) = gtimer();
+    // publish: one chunk -> final values; several -> partials, the last chunk merges
+    auto finish = [&](int q, float lsum, int d, float ov) {  // query q, head dim lane + 32 d
+        const int r = q / group, g = q % group;
+        if (d == 0 && !(lsum > 0.0f) && lane == 0) atomicOr(a.status, ST_EMPTY_ROW);
+        const float val = ov / lsum;
+        const int f = (kvh * group + g) * HD + lane + 32 * d;
+        a.att[static_cast<size_t>(r) * a.qd + f] = val;
+        put_split<kRows>(a.xim[P_O], f, r, val);
+    };
+    const int cpk = (a.max_len + kAttnMinKC - 1) / kAttnMinKC;  // chunk slots per kv head
+    constexpr size_t qstride = HD + 2;
+    int qa = 0, qb = nq;  // item queries this CTA finishes
+    if (nchunks > 1) {
+        // every chunk publishes (m, l, o) partials; once all chunks of this
+        // (kv head, query group) have arrived, chunk c merges queries
+        // [c * per, (c + 1) * per) over the chunks in chunk order (the merge is
+        // spread over the head's CTAs, which all run concurrently: items per
+        // head <= grid, mega_supported)
+        float* p0 = part + static_cast<size_t>(kvh) * cpk * 128 * qstride;
+        float* pc = p0 + static_cast<size_t>(chunk) * 128 * qstride;
+        if (wq)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (q0 + i >= nq) continue;
+                float* dst = pc + static_cast<size_t>(qbase + q0 + i) * qstride;
+                if (lane == 0) {
+                    dst[0] = mx[i];
+                    dst[1] = sm[i];
+                }
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) dst[2 + lane + 32 * d] = o[i][d];
+            }
         named_sync(3, 256);
+        unsigned* cnt = fptr(a, l, K_ATT, a.n_kv + 1 + 2 * kvh + qg);
         if (at == 0) {
-            unsigned* cnt = acnt + kvh * 16 + qg;
-            const unsigned old = atomicAdd(cnt, 1u);
-            *flag = old == static_cast<unsigned>(nchunks - 1) ? 1 : 0;
-            if (old == static_cast<unsigned>(nchunks - 1)) *cnt = 0u;
+            __threadfence();  // cumulative over the CTA's partial stores ordered by the barrier
+            atomicAdd(cnt, 1u);
+            if (a.trace) *tslot(a, blockIdx.x, 230 + l, 6) = gtimer();
+            wait_ge(cnt, static_cast<unsigned>(nchunks));
+            if (a.trace) *tslot(a, blockIdx.x, 230 + l, 7) = gtimer();
         }
         named_sync(3, 256);
-        if (!*flag) return;
-        __threadfence();
-        const float* p0 = part + static_cast<size_t>(kvh) * cpk * 128 * qstride;
-        for (int qi = warp; qi < nq; qi += 8) {  // merge this group's queries over the chunks
-            const int q = qbase + qi;
-            // lane ch holds chunk ch's (m, l); all loads in flight together
-            float mc = -INFINITY, lc = 0.0f;
-            if (lane < nchunks) {
-                const float* src = p0 + (static_cast<size_t>(lane) * 128 + q) * qstride;
-                mc = __ldcg(src);
-                lc = __ldcg(src + 1);
+        const int per = (nq + nchunks - 1) / nchunks;
+        qa = min(nq, chunk * per);
+        qb = min(nq, qa + per);
+        const int nm = qb - qa;
+        if (nm > 0) {
+            // (m, l) of the merged queries x chunks -> per-chunk weights (the ring is still lent)
+            float* sw = ring;                 // [nm][nchunks] (m, then the chunk weights)
+            float* sll = sw + 64 * 64;        // [nm][nchunks] l
+            float* sl = sll + 64 * 64;        // [nm] sums
+            for (int t = at; t < nm * nchunks; t += 256) {
+                const int qi = t / nchunks, ch = t % nchunks;
+                const float* src = p0 + (static_cast<size_t>(ch) * 128 + qbase + qa + qi) * qstride;
+                sw[t] = __ldcg(src);
+                sll[t] = __ldcg(src + 1);
             }
-            float M = mc;
-            for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-            const float w = mc == -INFINITY ? 0.0f : expf(mc - M);
-            float lsum = lc * w;  // fixed butterfly; absent chunks add exact zeros
-            for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
-            float ov[DPL];
+            named_sync(3, 256);
+            if (at < nm) {
+                float M = -INFINITY;
+                for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, sw[at * nchunks + ch]);
+                float lsum = 0.0f;  // chunk order; chunks past the row's keys add exact zeros
+                for (int ch = 0; ch < nchunks; ++ch) {
+                    const float mc = sw[at * nchunks + ch];
+                    const float w = mc == -INFINITY ? 0.0f : expf(mc - M);
+                    lsum = fmaf(sll[at * nchunks + ch], w, lsum);
+                    sw[at * nchunks + ch] = w;
+                }
+                sl[at] = lsum;
+            }
+            named_sync(3, 256);
+            for (int t0 = at; t0 < nm * HD; t0 += 512) {  // two outputs per thread, all their loads in flight
+                float acc2[2] = {0.0f, 0.0f};
+                for (int ch0 = 0; ch0 < nchunks; ch0 += 32) {  // chunk order
+                    float t32[2][32];
 #pragma unroll
-            for (int dd = 0; dd < DPL; ++dd) ov[dd] = 0.0f;
-            for (int ch0 = 0; ch0 < nchunks; ch0 += 8) {  // chunks in key order, 8 rows of loads in flight
-                float t8[8][DPL];
+                    for (int u = 0; u < 2; ++u) {
+                        const int t = t0 + 256 * u, qi = min(t, nm * HD - 1) / HD, dd = t % HD;
+                        const float* src = p0 + static_cast<size_t>(qbase + qa + qi) * qstride + 2 + dd;
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
+                        for (int j = 0; j < 32; ++j)
+                            t32[u][j] = ch0 + j < nchunks ? __ldcg(src + static_cast<size_t>(ch0 + j) * 128 * qstride) : 0.0f;
+                    }
 #pragma unroll
-                    for (int dd = 0; dd < DPL; ++dd)
-                        t8[j][dd] = ch0 + j < nchunks
-                                        ? __ldcg(p0 + (static_cast<size_t>(ch0 + j) * 128 + q) * qstride + 2 + lane + 32 * dd)
-                                        : 0.0f;
+                    for (int u = 0; u < 2; ++u) {
+                        const int qi = min(t0 + 256 * u, nm * HD - 1) / HD;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float wj = __shfl_sync(0xffffffffu, w, (ch0 + j) & 31);
-                    if (ch0 + j < nchunks)
+                        for (int j = 0; j < 32; ++j)
+                            if (ch0 + j < nchunks) acc2[u] = fmaf(t32[u][j], sw[qi * nchunks + ch0 + j], acc2[u]);
+                    }
+                }
 #pragma unroll
-                        for (int dd = 0; dd < DPL; ++dd) ov[dd] += t8[j][dd] * wj;
+                for (int u = 0; u < 2; ++u) {
+                const int t = t0 + 256 * u;
+                if (t >= nm * HD) break;
+                const int qi = t / HD, dd = t % HD, q = qbase + qa + qi;
+                const float acc = acc2[u];
+                const float lsum = sl[qi];
+                const int r = q / group, g = q % group;
+                if (dd == 0 && !(lsum > 0.0f)) atomicOr(a.status, ST_EMPTY_ROW);
+                const float val = acc / lsum;
+                const int f = (kvh * group + g) * HD + dd;
+                a.att[static_cast<size_t>(r) * a.qd + f] = val;
+                put_split<kRows>(a.xim[P_O], f, r, val);
                 }
             }
-            finish(q, lsum, ov);
         }
-    } else {
+    } else if (wq) {
 #pragma unroll
-        for (int i = 0; i < QPW; ++i)
-            if (q0 + i < nq) finish(qbase + q0 + i, l_run[i], o[i]);
+        for (int i = 0; i < 8; ++i)
+            if (q0 + i < nq)
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) {
+                    const int q = qbase + q0 + i, r = q / group, g = q % group;
+                    const float lsum = sm[i];
+                    if (d == 0 && lane == 0 && !(lsum > 0.0f)) atomicOr(a.status, ST_EMPTY_ROW);
+                    const float val = fmaf(o[i][d], 1.0f, 0.0f) / lsum;
+                    const int f = (kvh * group + g) * HD + lane + 32 * d;
+                    a.att[static_cast<size_t>(r) * a.qd + f] = val;
+                    put_split<kRows>(a.xim[P_O], f, r, val);
+                }
     }
     fence_proxy_async_global();
     named_sync(3, 256);
-    if (at == 0) {  // these rows of this kv head are published
+    if (at == 0) {  // these queries of this kv head are published
         __threadfence();
-        atomicAdd(fptr(a, l, K_ATT, kvh), static_cast<unsigned>(nq / group));
+        if (qb > qa) atomicAdd(fptr(a, l, K_ATT, kvh), static_cast<unsigned>(qb - qa));
+        if (a.trace) *tslot(a, blockIdx.x, 230 + l, 8) = gtimer();
     }
 }
 
-// queries per warp for this launch: fewer queries per item (more items) when
-// there are few key chunks.  Numerics do not depend on this choice.
-__device__ __forceinline__ int attn_qpw(const MegaArgs& a, int nchunks) { return nchunks * a.n_kv >= 64 ? 4 : 2; }
-
-__device__ __forceinline__ void attention_dispatch(const MegaArgs& a, const LayerDesc& L, int l, int item, int nchunks,
-                                                   int at, float* sq, float* sp, float* skv, float* part,
-                                                   unsigned* acnt, int* flag) {
+__device__ __forceinline__ int attn_chunks(const MegaArgs& a) {
+    const int kc = a.hd <= 128 ? attn_kc<128>() : attn_kc<160>();
+    return (sh_prior + a.rows + kc - 1) / kc;
+}
+__device__ __forceinline__ int attention_items(const MegaArgs& a, int nchunks) {
+    const int nqg = (a.rows * (a.n_heads / a.n_kv) + 63) / 64;
+    return a.n_kv * nchunks * nqg;
+}
+__device__ __forceinline__ void attention_dispatch(const MegaArgs& a, int l, int item, int nchunks, int at, float* part,
+                                                   int xoff) {
     const int group = a.n_heads / a.n_kv;
-    const int qpw = attn_qpw(a, nchunks);
-    const int nqg = (a.rows * group + 8 * qpw - 1) / (8 * qpw);
+    const int nqg = (a.rows * group + 63) / 64;
     const int kvh = item / (nchunks * nqg), rem = item % (nchunks * nqg), chunk = rem / nqg, qg = rem % nqg;
     {  // wait for this kv head's QKV tiles: its q heads, K and V
         const int q0 = kvh * group * a.hd / kM, q1 = ((kvh + 1) * group * a.hd - 1) / kM;
@@ -1038,28 +1118,25 @@ __device__ __forceinline__ void attention_dispatch(const MegaArgs& a, const Laye
         }
         named_sync(3, 256);
     }
-#define SFG_ATT(HDV, Q) attention_chunk<HDV, Q>(a, L, l, kvh, chunk, nchunks, qg, at, sq, sp, skv, part, acnt, flag)
-    if (qpw == 4) {
-        switch (a.hd) {
-            case 64: SFG_ATT(64, 4); break;
-            case 128: SFG_ATT(128, 4); break;
-            case 160: SFG_ATT(160, 4); break;
-            default: SFG_ATT(32, 4); break;
-        }
-    } else {
-        switch (a.hd) {
-            case 64: SFG_ATT(64, 2); break;
-            case 128: SFG_ATT(128, 2); break;
-            case 160: SFG_ATT(160, 2); break;
-            default: SFG_ATT(32, 2); break;
-        }
+    switch (a.hd) {
+        case 32: attention_tile<32>(a, l, kvh, chunk, nchunks, qg, at, part, xoff); break;
+        case 64: attention_tile<64>(a, l, kvh, chunk, nchunks, qg, at, part, xoff); break;
+        case 160: attention_tile<160>(a, l, kvh, chunk, nchunks, qg, at, part, xoff); break;
+        default: attention_tile<128>(a, l, kvh, chunk, nchunks, qg, at, part, xoff); break;
     }
-#undef SFG_ATT
 }
-__device__ __forceinline__ int attention_items(const MegaArgs& a, int nchunks) {
-    const int qpw = attn_qpw(a, nchunks);
-    const int nqg = (a.rows * (a.n_heads / a.n_kv) + 8 * qpw - 1) / (8 * qpw);
-    return a.n_kv * nchunks * nqg;
+// the chunked design's attention phase of layer l for the attention threads
+// (warps 2..9): wait for the lent ring, run this CTA's items, give it back
+__device__ __forceinline__ void attention_phase_lent(const MegaArgs& a, int l, int at, uint64_t* lentb, uint64_t* retb,
+                                                     int xoff) {
+    if (at == 0) mwait(lentb, static_cast<uint32_t>(l & 1));
+    named_sync(3, 256);
+    const int nchunks = attn_chunks(a);
+    for (int it = blockIdx.x; it < attention_items(a, nchunks); it += gridDim.x)
+        attention_dispatch(a, l, it, nchunks, at, a.apart, xoff);
+    fence_proxy_async();  // generic-proxy ring accesses before the producer's bulk copies
+    named_sync(3, 256);
+    if (at == 0) mbar_arrive(retb);
 }
 
 // A CTA's walk over its weight units: (layer, phase, unit) in stream order.
@@ -1099,8 +1176,8 @@ __device__ __forceinline__ void cursor_prefetch_next(const MegaArgs& a, int c, C
 
 // shared-memory floats of the attention scratch: the larger of the two layouts
 __host__ __device__ __forceinline__ int attn_scratch_floats(bool rows_attn, int hd, int group, int max_len) {
-    return rows_attn ? kMaxGroup * hd + 8 * kMaxGroup * 2 + 8 * group * hd
-                     : 32 * hd + 8 * 4 * kKeyBlock + 4 * kKeyBlock * hd + 2 * kRows * hd;
+    // the chunked design stages its items in the lent weight ring (attention_tile)
+    return rows_attn ? kMaxGroup * hd + 8 * kMaxGroup * 2 + 8 * group * hd : 0;
 }
 
 // ── the kernel ────────────────────────────────────────────────────────────
@@ -1111,22 +1188,20 @@ __host__ __device__ __forceinline__ int attn_scratch_floats(bool rows_attn, int 
 // 16-row path keeps its constant-folded addressing)
 template <bool kRowsAttn, int RR>
 __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant__ MegaArgs a) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = reinterpret_cast<uint8_t*>(ring_base());
     const int S = a.stages;
     const int SB = a.stage_bytes;  // [16 KB weights | 3R x 64 activation image] per stage
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * SB);
     uint64_t* empty = full + kMaxStages;
     uint64_t* tfull = empty + kMaxStages;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* lentb = tempty + 2;  // chunked attention: ring lent to the attention phase / given back
+    uint64_t* retb = lentb + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(retb + 1);
     int* flag = reinterpret_cast<int*>(tmem_slot + 4);
     float* xch = reinterpret_cast<float*>(flag + 4);          // 64*16 gate|up + 4*16 sumsq
     float* rs = xch + 64 * kRows + 4 * kRows;                  // [kMaxRows] per-row 1/rms of the phase
-    // attention scratch, one of two layouts (MegaArgs::attn_rows):
-    float* sq = rs + kMaxRows;                                 // chunked: [32 queries][hd] queries
-    float* sp = sq + 32 * a.hd;                                //   [8 warps][4][kKeyBlock] probabilities
-    float* skv = sp + 8 * 4 * kKeyBlock;                       //   2 staged K | V blocks + tail slots
+    // attention scratch of the per-row design (the chunked design uses the lent ring)
     float* qs = rs + kMaxRows;                                 // per-row: [group][hd] queries
     float* wst = qs + kMaxGroup * a.hd;                        //   [8][kMaxGroup][2] warp stats
     float* ocomb = wst + 8 * kMaxGroup * 2;                    //   [8][group][hd] warp partials
@@ -1184,6 +1259,8 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 4);
         }
+        mbar_init(lentb, 1);
+        mbar_init(retb, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
@@ -1266,6 +1343,31 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                     }
                     }
                     if (a.trace) *tslot(a, c, input_barrier(l, p), 5) = wacc;
+                    if (!kRowsAttn && p == P_QKV) {
+                        // lend the whole ring to the attention phase: wait until
+                        // every pair is consumed (no copy in flight), hand it
+                        // over, and on its return complete the lent pairs with
+                        // plain arrivals (the MMA issuer skips them)
+                        int st2 = stage;
+                        uint32_t ph2 = ph;
+                        for (int i = 0; i < NP; ++i) {
+                            mwait(&empty[st2], ph2 ^ 1);
+                            if (++st2 == NP) {
+                                st2 = 0;
+                                ph2 ^= 1;
+                            }
+                        }
+                        mbar_arrive(lentb);
+                        mwait_sleep(retb, static_cast<uint32_t>(l & 1));
+                        for (int i = 0; i < NP; ++i) {
+                            mbar_arrive(&full[stage]);
+                            mbar_arrive(&full[stage]);
+                            if (++stage == NP) {
+                                stage = 0;
+                                ph ^= 1;
+                            }
+                        }
+                    }
                 }
         }
     } else if (warp == 1) {
@@ -1331,6 +1433,16 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         *tslot(a, c, input_barrier(l, p), 4) = wacc;
                         *tslot(a, c, input_barrier(l, p), 17) = gtimer();
                         *tslot(a, c, input_barrier(l, p), 18) = tacc;
+                    }
+                    if (!kRowsAttn && p == P_QKV) {  // the lent pairs: nothing to multiply
+                        for (int i = 0; i < NP; ++i) {
+                            mwait_sleep(&full[stage], ph);
+                            mbar_arrive(&empty[stage]);
+                            if (++stage == NP) {
+                                stage = 0;
+                                ph ^= 1;
+                            }
+                        }
                     }
                 }
         }
@@ -1535,10 +1647,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                             attention_rows_dispatch<RR>(a, L, l, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst,
                                                     ocomb, cols);
                     } else {
-                        const int nchunks = (sh_prior + a.rows + kKeyChunk - 1) / kKeyChunk;
-                        for (int it = c; it < attention_items(a, nchunks); it += G)
-                            attention_dispatch(a, L, l, it, nchunks, threadIdx.x - 64, sq, sp, skv, a.apart, a.acnt,
-                                               flag);
+                        attention_phase_lent(a, l, threadIdx.x - 64, lentb, retb, static_cast<int>(reinterpret_cast<uint8_t*>(xch) - smem));
                     }
                     if (a.trace && et == 0) *tslot(a, c, 5 * l + 2, 2) = gtimer();
                 }
@@ -1603,6 +1712,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                         *tslot(a, c, input_barrier(l, p), 1) = gtimer();
                         *tslot(a, c, input_barrier(l, p), 3) = xwacc;
                     }
+                    if (!kRowsAttn && p == P_QKV) ph ^= 1;  // the lent pairs (one whole wrap of the ring)
                     __syncwarp();
                 }
                 if (p == P_QKV) {  // join the attention phase
@@ -1611,10 +1721,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                             attention_rows_dispatch<RR>(a, L, l, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst,
                                                     ocomb, cols);
                     } else {
-                        const int nchunks = (sh_prior + a.rows + kKeyChunk - 1) / kKeyChunk;
-                        for (int it = c; it < attention_items(a, nchunks); it += G)
-                            attention_dispatch(a, L, l, it, nchunks, threadIdx.x - 64, sq, sp, skv, a.apart, a.acnt,
-                                               flag);
+                        attention_phase_lent(a, l, threadIdx.x - 64, lentb, retb, static_cast<int>(reinterpret_cast<uint8_t*>(xch) - smem));
                     }
                 }
             }
@@ -1662,7 +1769,7 @@ size_t dyn_smem_budget(bool rows_attn) {
 // dynamic shared memory of a launch with row capacity R (must match the
 // kernel's carve-up: ring | barriers | xch | rs | attention | ropeT | hpre)
 size_t smem_bytes(bool rows_attn, int stages, int hd, int group, int max_len, int R = kRows) {
-    return 1024 + static_cast<size_t>(stages) * (kABytes + 384 * R) + (2 * kMaxStages + 4) * 8 + 32 +
+    return 1024 + static_cast<size_t>(stages) * (kABytes + 384 * R) + (2 * kMaxStages + 6) * 8 + 32 +
            sizeof(float) * (64 * kRows + 4 * kRows + kMaxRows + attn_scratch_floats(rows_attn, hd, group, max_len) +
                             (R == kRows ? kRows * hd : 0) + R * kM + kM) + 16;
 }
@@ -1682,16 +1789,31 @@ using namespace mega;
 // The megakernel covers decode batches (<= 16 rows) with frame-style masks
 // (visible mask value 0); seam-2 additive masks and long prompts take the
 // per-GEMM path.
+// ring stages of a launch: the deepest even ring whose shared memory fits
+int mega_stages(bool ra, int hd, int group, int max_len, int RS, int cap) {
+    int stages = cap & ~1;  // the ring is walked in pairs of stages
+    while (stages > 4 && smem_bytes(ra, stages, hd, group, max_len, RS) > dyn_smem_budget(ra)) stages -= 2;
+    return stages;
+}
+
 bool mega_supported(const Engine& e, int rows, bool additive_mask) {
     if (rows < 1 || rows > tc::kRows || additive_mask) return false;
     const ModelCfg& c = e.cfg();
     const int group = c.n_heads / c.n_kv_heads;
-    if (group > kMaxGroup || c.head_dim % 32 != 0 || c.head_dim > 160) return false;
+    if (group > kMaxGroup || !(c.head_dim == 32 || c.head_dim == 64 || c.head_dim == 128 || c.head_dim == 160)) return false;
     if (group > 4 && c.head_dim > 64) return false;  // register budget of the attention phase
     if (c.hidden_dim % tc::kKB || c.q_dim() % tc::kKB || c.ffn_dim % tc::kKB) return false;
     const bool ra = rows_attention();
     const size_t sm = smem_bytes(ra, 4, c.head_dim, c.n_heads / c.n_kv_heads, c.max_seq_len);
-    return sm <= dyn_smem_budget(ra);
+    if (sm > dyn_smem_budget(ra)) return false;
+    if (!ra) {  // the chunked design stages a whole key chunk in the lent ring; at most 64 chunks merge
+        const int kc = c.head_dim <= 128 ? attn_kc<128>() : attn_kc<160>();
+        const int st = mega_stages(false, c.head_dim, group, c.max_seq_len, tc::kRows, kMaxStages);
+        if (static_cast<size_t>(attn_lend_floats(c.head_dim, kc)) * 4 > static_cast<size_t>(st) * (tc::kABytes + 384 * tc::kRows))
+            return false;
+        if ((c.max_seq_len + kc - 1) / kc > 64) return false;
+    }
+    return true;
 }
 
 // Rows one cross-session weight pass can carry: 32 (two 16-row blocks, MMA
@@ -1803,10 +1925,10 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
             SFG_CUDA(cudaMemset(st.counters, 0, sizeof(int) * 2 * st.cnt_stride));
             // must match fptr(): stats tiles + counter, then per layer
             // (QKV, attention kv heads, O, gate|up, down) tiles + counter each
-            const int lay = (tQ + 1) + (c.n_kv_heads + 1) + (tilesH + 1) + (tG + 1) + (tilesH + 1);
+            const int lay = (tQ + 1) + (3 * c.n_kv_heads + 1) + (tilesH + 1) + (tG + 1) + (tilesH + 1);
             st.nflags = tilesH + 1 + (le - lb) * lay;
             SFG_CUDA(cudaMalloc(&st.flags, sizeof(unsigned) * st.nflags));
-            const size_t cpk = (c.max_seq_len + kKeyChunk - 1) / kKeyChunk;
+            const size_t cpk = (c.max_seq_len + kAttnMinKC - 1) / kAttnMinKC;
             SFG_CUDA(cudaMalloc(&st.apart, sizeof(float) * c.n_kv_heads * cpk * 128 * (c.head_dim + 2)));
             SFG_CUDA(cudaMalloc(&st.acnt, sizeof(unsigned) * c.n_kv_heads * 16));
             SFG_CUDA(cudaMemset(st.acnt, 0, sizeof(unsigned) * c.n_kv_heads * 16));
@@ -1843,13 +1965,17 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         const char* v = getenv("SFG_MEGA_STAGES");  // dev knob: ring depth sensitivity
         return v ? std::min(std::max(atoi(v), 2), kMaxStages) : kMaxStages;
     }();
-    int stages = stages_cap & ~1;  // the ring is walked in pairs of stages
     const int RS = stp->rcap;      // the buffers' row stride (>= R)
     const bool ra = rows_attention();
     const void* kfn = !ra ? reinterpret_cast<const void*>(mega_kernel<false, kRows>)
                       : RS == kRows ? reinterpret_cast<const void*>(mega_kernel<true, kRows>)
                                     : reinterpret_cast<const void*>(mega_kernel<true, kMaxRows>);
-    while (stages > 4 && smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len, RS) > dyn_smem_budget(ra)) stages -= 2;
+    const int stages = mega_stages(ra, c.head_dim, group, c.max_seq_len, RS, stages_cap);
+    if (!ra) {
+        const int kc = c.head_dim <= 128 ? attn_kc<128>() : attn_kc<160>();
+        if (static_cast<size_t>(attn_lend_floats(c.head_dim, kc)) * 4 > static_cast<size_t>(stages) * (tc::kABytes + 384 * RS))
+            throw Error(Kind::internal, "chunked attention: a key chunk does not fit the lent weight ring");
+    }
     const size_t smem = smem_bytes(ra, stages, c.head_dim, group, c.max_seq_len, RS);
     {
         ensure_smem_attr(kfn, smem);
@@ -1990,7 +2116,8 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         for (int p = 0; p < 4; ++p) a.W[p] = whole_env ? whole_tiles(tiles_of[p], kb_of[p], a.G[p]) : 0;
         // flag layout (must match kind_tiles): statistics tiles + counter, then
         // per layer QKV, attention kv heads, O, gate|up, down tiles + counter each
-        const int kt[6] = {tH, tQ, dl.n_kv, tH, dl.F / 64, tH};
+        // (K_ATT: per kv head published-query counts, then 2 chunk-arrival counters per head)
+        const int kt[6] = {tH, tQ, 3 * dl.n_kv, tH, dl.F / 64, tH};
         a.fl_base = tH + 1;
         int off = 0;
         for (int k = mega::K_QKV; k <= mega::K_DOWN; ++k) {

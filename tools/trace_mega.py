@@ -154,3 +154,21 @@ for l in range(1, 3):
             parts.append(f"{name} med {np.median(v):.0f} max {v.max():.0f}")
     if parts:
         print(f"L{l} walk cycles per warp:", "; ".join(parts))
+# chunked attention items (ids 230 + l): 0 staged issue, 1 K landed, 2 scores done,
+# 3 P^T written + V landed, 5 PV done, 6 partial published, 7 all chunks arrived, 8 merged + published
+for l in range(1, NL - 1):
+    T = tr[:, 230 + l, :]
+    m = T[:, 0] > 0
+    if not m.any():
+        continue
+    T = T[m]
+    rel = lambda v: (v - t0) / 1000  # noqa: E731
+    def md(x):
+        return f"{np.median(x) / 1000:5.2f}/{x.max() / 1000:5.2f}"
+    seg = [("K land", 0, 1), ("scores", 1, 2), ("P+V", 2, 3), ("PV", 3, 5)]
+    parts = ", ".join(f"{n} {md(T[:, b] - T[:, a])}" for n, a, b in seg)
+    has6 = T[:, 6] > 0
+    if has6.any():
+        parts += f", publish {md(T[has6, 6] - T[has6, 5])}, arrive-wait {md(T[has6, 7] - T[has6, 6])}, merge {md(T[has6, 8] - T[has6, 7])}"
+    print(f"L{l} chunked attention ({m.sum()} CTAs): first start {rel(T[:, 0]).min():.1f} last publish "
+          f"{rel(T[:, 8]).max():.1f}; {parts}")
