@@ -217,29 +217,48 @@ int launch_hd(const float* q, const float* kc, const float* vc, const int32_t* r
 constexpr int kPQ = 64;   // queries per CTA
 constexpr int kPK = 64;   // keys per block
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Shared memory: Q [kPQ][HD] and K [kPK][HD] with float4 column c of row r at
+// c ^ (r & 7) (the 16 key rows a half-warp reads at once hit 8 bank groups),
+// V [kPK][HD]; P [kPQ][kPK + 4] reuses K's space once the scores are taken.
+// 96 KB at HD = 128: two CTAs per SM, so one CTA's K / V copies (cp.async,
+// straight to shared memory) overlap the other's arithmetic.
 template <int HD>
-__global__ void __launch_bounds__(256) attn_prompt_kernel(const float* __restrict__ q, const float* __restrict__ kc,
-                                                          const float* __restrict__ vc,
-                                                          const int32_t* __restrict__ row_off,
-                                                          const MaskRun* __restrict__ runs, Dims d, int rows,
-                                                          float* __restrict__ att, uint32_t* status) {
+__global__ void __launch_bounds__(256, 2) attn_prompt_kernel(const float* __restrict__ q, const float* __restrict__ kc,
+                                                             const float* __restrict__ vc,
+                                                             const int32_t* __restrict__ row_off,
+                                                             const MaskRun* __restrict__ runs, Dims d, int rows,
+                                                             float* __restrict__ att, uint32_t* status) {
+    constexpr int C4 = HD / 4;    // float4 columns per row
     constexpr int DPT = HD / 16;  // value dims per thread
     extern __shared__ float4 smem4[];
-    float* QT = reinterpret_cast<float*>(smem4);  // [HD][kPQ]
-    float* KT = QT + HD * kPQ;                     // [HD][kPK]
-    float* Vs = KT + HD * kPK;                     // [kPK][HD]
-    float* P = Vs + kPK * HD;                      // [kPQ][kPK + 4]
+    float4* Q4 = smem4;                                // [kPQ][C4] swizzled
+    float4* K4 = Q4 + kPQ * C4;                        // [kPK][C4] swizzled
+    float* Vs = reinterpret_cast<float*>(K4) + kPK * (HD > kPK + 4 ? HD : kPK + 4);  // [kPK][HD]
+    float* P = reinterpret_cast<float*>(K4);           // [kPQ][kPK + 4] (after the scores)
     __shared__ int lim_s[kPQ];
     const int G = d.n_heads / d.n_kv, RPB = kPQ / G;
     // the heaviest (latest, longest causal) row blocks are scheduled first
     const int rb0 = (gridDim.x - 1 - blockIdx.x) * RPB, kvh = blockIdx.y;
     const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
     // query qi = g * RPB + r: row rb0 + r, head kvh * G + g
-    for (int idx = tid; idx < kPQ * HD; idx += 256) {
-        const int qi = idx % kPQ, dd = idx / kPQ, r = qi % RPB, g = qi / RPB, row = rb0 + r;
-        QT[dd * kPQ + qi] = row < rows ? q[static_cast<size_t>(row) * d.qd + static_cast<size_t>(kvh * G + g) * HD + dd]
-                                       : 0.0f;
+    for (int idx = tid; idx < kPQ * C4; idx += 256) {
+        const int qi = idx / C4, c = idx % C4, r = qi % RPB, g = qi / RPB, row = rb0 + r;
+        float4* dst = Q4 + qi * C4 + (c ^ (qi & 7));
+        if (row < rows)
+            cp_async16(dst, q + static_cast<size_t>(row) * d.qd + static_cast<size_t>(kvh * G + g) * HD + 4 * c);
+        else
+            *dst = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    cp_async_commit();
     if (tid < kPQ) {
         const int row = rb0 + tid % RPB;
         lim_s[tid] = row < rows ? runs[row_off[row]].end : 0;
@@ -262,45 +281,49 @@ __global__ void __launch_bounds__(256) attn_prompt_kernel(const float* __restric
         for (int c = 0; c < DPT; ++c) o[i][c] = 0.0f;
     }
     for (int k0 = 0; k0 < kmax; k0 += kPK) {
-        __syncthreads();  // the previous block's K / V / P are consumed
-        for (int idx = tid; idx < kPK * (HD / 4); idx += 256) {
-            const int kk = idx % kPK, d4 = idx / kPK, key = k0 + kk;
-            float4 kv = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (key < kmax) kv = __ldg(reinterpret_cast<const float4*>(kb + static_cast<size_t>(key) * HD) + d4);
-            KT[(4 * d4 + 0) * kPK + kk] = kv.x;
-            KT[(4 * d4 + 1) * kPK + kk] = kv.y;
-            KT[(4 * d4 + 2) * kPK + kk] = kv.z;
-            KT[(4 * d4 + 3) * kPK + kk] = kv.w;
+        const int nk = min(kPK, kmax - k0);
+        __syncthreads();  // the previous block's P / V are consumed
+        for (int idx = tid; idx < nk * C4; idx += 256) {
+            const int kk = idx / C4, c = idx % C4;
+            cp_async16(K4 + kk * C4 + (c ^ (kk & 7)), kb + static_cast<size_t>(k0 + kk) * HD + 4 * c);
         }
-        for (int idx = tid; idx < kPK * (HD / 4); idx += 256) {
-            const int d4 = idx % (HD / 4), kk = idx / (HD / 4), key = k0 + kk;
-            reinterpret_cast<float4*>(Vs)[kk * (HD / 4) + d4] =
-                key < kmax ? __ldg(reinterpret_cast<const float4*>(vb + static_cast<size_t>(key) * HD) + d4)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        cp_async_commit();
+        for (int idx = tid; idx < nk * C4; idx += 256)
+            cp_async16(reinterpret_cast<float4*>(Vs) + idx, vb + static_cast<size_t>(k0) * HD + 4 * idx);
+        cp_async_commit();
+        cp_async_wait<1>();  // queries + K
         __syncthreads();
+        // scores: queries 4ty + i, keys tx + 16 j (rows past nk are masked below)
         float sc[4][4];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) sc[i][j] = 0.0f;
-#pragma unroll 8
-        for (int dd = 0; dd < HD; ++dd) {
-            const float4 q4 = reinterpret_cast<const float4*>(QT + dd * kPQ)[ty];
-            const float4 k4 = reinterpret_cast<const float4*>(KT + dd * kPK)[tx];
-            const float qv[4] = {q4.x, q4.y, q4.z, q4.w}, kv[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll 2
+        for (int c = 0; c < C4; ++c) {
+            float4 q4[4], k4[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) q4[i] = Q4[(4 * ty + i) * C4 + (c ^ ((4 * ty + i) & 7))];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) k4[j] = K4[(tx + 16 * j) * C4 + (c ^ (tx & 7))];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) sc[i][j] += qv[i] * kv[j];
+                for (int j = 0; j < 4; ++j) {
+                    sc[i][j] = fmaf(q4[i].x, k4[j].x, sc[i][j]);
+                    sc[i][j] = fmaf(q4[i].y, k4[j].y, sc[i][j]);
+                    sc[i][j] = fmaf(q4[i].z, k4[j].z, sc[i][j]);
+                    sc[i][j] = fmaf(q4[i].w, k4[j].w, sc[i][j]);
+                }
         }
-        // online softmax per query (its 64 keys sit on the 16 tx lanes of its group)
+        __syncthreads();  // K is consumed: P takes its space
+        // online softmax per query (its 64 keys sit on the 16 tx lanes of its half-warp)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             float bm = -INFINITY;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const int key = k0 + 4 * tx + j;
+                const int key = k0 + tx + 16 * j;
                 sc[i][j] = key < lim[i] ? sc[i][j] * inv_sqrt_hd : -INFINITY;
                 bm = fmaxf(bm, sc[i][j]);
             }
@@ -311,7 +334,7 @@ __global__ void __launch_bounds__(256) attn_prompt_kernel(const float* __restric
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const float pj = sc[i][j] == -INFINITY ? 0.0f : expf(sc[i][j] - mn);
-                P[(4 * ty + i) * (kPK + 4) + 4 * tx + j] = pj;
+                P[(4 * ty + i) * (kPK + 4) + tx + 16 * j] = pj;
                 rs += pj;
             }
             for (int off = 8; off > 0; off >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, off);
@@ -320,9 +343,11 @@ __global__ void __launch_bounds__(256) attn_prompt_kernel(const float* __restric
 #pragma unroll
             for (int c = 0; c < DPT; ++c) o[i][c] *= alpha;
         }
+        cp_async_wait<0>();  // V
         __syncthreads();
         // O += P V: rows 4ty..4ty+3, dims tx*DPT ..
-        for (int kk = 0; kk < kPK; ++kk) {
+#pragma unroll 2
+        for (int kk = 0; kk < nk; ++kk) {
             float pv[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) pv[i] = P[(4 * ty + i) * (kPK + 4) + kk];
@@ -332,8 +357,8 @@ __global__ void __launch_bounds__(256) attn_prompt_kernel(const float* __restric
                 const float2 v2 = vr[c2];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    o[i][2 * c2] += pv[i] * v2.x;
-                    o[i][2 * c2 + 1] += pv[i] * v2.y;
+                    o[i][2 * c2] = fmaf(pv[i], v2.x, o[i][2 * c2]);
+                    o[i][2 * c2 + 1] = fmaf(pv[i], v2.y, o[i][2 * c2 + 1]);
                 }
             }
         }
@@ -356,7 +381,8 @@ __global__ void __launch_bounds__(256) attn_prompt_kernel(const float* __restric
 template <int HD>
 int launch_prompt_hd(const float* q, const float* kc, const float* vc, const int32_t* row_off, const MaskRun* runs,
                      int rows, const Dims& d, float* att, uint32_t* status, cudaStream_t s) {
-    const size_t smem = sizeof(float) * (static_cast<size_t>(HD) * kPQ + HD * kPK + kPK * HD + kPQ * (kPK + 4));
+    // Q | K (then P) | V; P [kPQ][kPK + 4] fits in K's [kPK][HD] for HD >= 68
+    const size_t smem = sizeof(float) * (static_cast<size_t>(kPQ) * HD + 2 * static_cast<size_t>(kPK) * std::max(HD, kPK + 4));
     ensure_smem_attr(reinterpret_cast<const void*>(attn_prompt_kernel<HD>), smem);
     const int rpb = kPQ / (d.n_heads / d.n_kv);
     const dim3 grid((rows + rpb - 1) / rpb, d.n_kv);
