@@ -787,6 +787,143 @@ __device__ __forceinline__ float* ring_base() {
     return reinterpret_cast<float*>(mega_dyn_smem + ((1024u - mis) & 1023u));
 }
 
+// publish an item's (m, l, o) rows: one chunk -> the final attention rows and
+// O-projection image; several -> partials, then the chunks of this (kv head,
+// query group) merge in chunk order, each CTA a slice of the queries
+template <int HD>
+__device__ __forceinline__ void attn_publish(const MegaArgs& a, int l, int kvh, int chunk, int nchunks, int qg, int at,
+                                             float* part, float* ring, const float (&mx)[8], const float (&sm)[8],
+                                             const float (&o)[8][HD / 32]) {
+    constexpr int DPL = HD / 32;
+    const int group = a.n_heads / a.n_kv;
+    const int NQ = a.rows * group;
+    const int qbase = qg * 64, nq = min(64, NQ - qbase);
+    const int warp = at >> 5, lane = at & 31;
+    const int q0 = warp * 8;
+    const bool wq = q0 < nq;
+    // publish: one chunk -> final values; several -> partials, the last chunk merges
+    const int cpk = (a.max_len + kAttnMinKC - 1) / kAttnMinKC;  // chunk slots per kv head
+    constexpr size_t qstride = HD + 2;
+    int qa = 0, qb = nq;  // item queries this CTA finishes
+    if (nchunks > 1) {
+        // every chunk publishes (m, l, o) partials; once all chunks of this
+        // (kv head, query group) have arrived, chunk c merges queries
+        // [c * per, (c + 1) * per) over the chunks in chunk order (the merge is
+        // spread over the head's CTAs, which all run concurrently: items per
+        // head <= grid, mega_supported)
+        float* p0 = part + static_cast<size_t>(kvh) * cpk * 128 * qstride;
+        float* pc = p0 + static_cast<size_t>(chunk) * 128 * qstride;
+        if (wq)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (q0 + i >= nq) continue;
+                float* dst = pc + static_cast<size_t>(qbase + q0 + i) * qstride;
+                if (lane == 0) {
+                    dst[0] = mx[i];
+                    dst[1] = sm[i];
+                }
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) dst[2 + lane + 32 * d] = o[i][d];
+            }
+        named_sync(3, 256);
+        unsigned* cnt = fptr(a, l, K_ATT, a.n_kv + 1 + 2 * kvh + qg);
+        if (at == 0) {
+            __threadfence();  // cumulative over the CTA's partial stores ordered by the barrier
+            atomicAdd(cnt, 1u);
+            if (a.trace) *tslot(a, blockIdx.x, 230 + l, 6) = gtimer();
+            wait_ge(cnt, static_cast<unsigned>(nchunks));
+            if (a.trace) *tslot(a, blockIdx.x, 230 + l, 7) = gtimer();
+        }
+        named_sync(3, 256);
+        const int per = (nq + nchunks - 1) / nchunks;
+        qa = min(nq, chunk * per);
+        qb = min(nq, qa + per);
+        const int nm = qb - qa;
+        if (nm > 0) {
+            // (m, l) of the merged queries x chunks -> per-chunk weights (the ring is still lent)
+            float* sw = ring;                 // [nm][nchunks] (m, then the chunk weights)
+            float* sll = sw + 64 * 64;        // [nm][nchunks] l
+            float* sl = sll + 64 * 64;        // [nm] sums
+            for (int t = at; t < nm * nchunks; t += 256) {
+                const int qi = t / nchunks, ch = t % nchunks;
+                const float* src = p0 + (static_cast<size_t>(ch) * 128 + qbase + qa + qi) * qstride;
+                sw[t] = __ldcg(src);
+                sll[t] = __ldcg(src + 1);
+            }
+            named_sync(3, 256);
+            if (at < nm) {
+                float M = -INFINITY;
+                for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, sw[at * nchunks + ch]);
+                float lsum = 0.0f;  // chunk order; chunks past the row's keys add exact zeros
+                for (int ch = 0; ch < nchunks; ++ch) {
+                    const float mc = sw[at * nchunks + ch];
+                    const float w = mc == -INFINITY ? 0.0f : expf(mc - M);
+                    lsum = fmaf(sll[at * nchunks + ch], w, lsum);
+                    sw[at * nchunks + ch] = w;
+                }
+                sl[at] = lsum;
+            }
+            named_sync(3, 256);
+            for (int t0 = at; t0 < nm * HD; t0 += 512) {  // two outputs per thread, all their loads in flight
+                float acc2[2] = {0.0f, 0.0f};
+                for (int ch0 = 0; ch0 < nchunks; ch0 += 32) {  // chunk order
+                    float t32[2][32];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int t = t0 + 256 * u, qi = min(t, nm * HD - 1) / HD, dd = t % HD;
+                        const float* src = p0 + static_cast<size_t>(qbase + qa + qi) * qstride + 2 + dd;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            t32[u][j] = ch0 + j < nchunks ? __ldcg(src + static_cast<size_t>(ch0 + j) * 128 * qstride) : 0.0f;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int qi = min(t0 + 256 * u, nm * HD - 1) / HD;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (ch0 + j < nchunks) acc2[u] = fmaf(t32[u][j], sw[qi * nchunks + ch0 + j], acc2[u]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                const int t = t0 + 256 * u;
+                if (t >= nm * HD) break;
+                const int qi = t / HD, dd = t % HD, q = qbase + qa + qi;
+                const float acc = acc2[u];
+                const float lsum = sl[qi];
+                const int r = q / group, g = q % group;
+                if (dd == 0 && !(lsum > 0.0f)) atomicOr(a.status, ST_EMPTY_ROW);
+                const float val = acc / lsum;
+                const int f = (kvh * group + g) * HD + dd;
+                a.att[static_cast<size_t>(r) * a.qd + f] = val;
+                put_split<kRows>(a.xim[P_O], f, r, val);
+                }
+            }
+        }
+    } else if (wq) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (q0 + i < nq)
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) {
+                    const int q = qbase + q0 + i, r = q / group, g = q % group;
+                    const float lsum = sm[i];
+                    if (d == 0 && lane == 0 && !(lsum > 0.0f)) atomicOr(a.status, ST_EMPTY_ROW);
+                    const float val = fmaf(o[i][d], 1.0f, 0.0f) / lsum;
+                    const int f = (kvh * group + g) * HD + lane + 32 * d;
+                    a.att[static_cast<size_t>(r) * a.qd + f] = val;
+                    put_split<kRows>(a.xim[P_O], f, r, val);
+                }
+    }
+    fence_proxy_async_global();
+    named_sync(3, 256);
+    if (at == 0) {  // these queries of this kv head are published
+        __threadfence();
+        if (qb > qa) atomicAdd(fptr(a, l, K_ATT, kvh), static_cast<unsigned>(qb - qa));
+        if (a.trace) *tslot(a, blockIdx.x, 230 + l, 8) = gtimer();
+    }
+}
+
 template <int HD>
 __device__ __noinline__ void attention_tile(const MegaArgs& a, int l, int kvh, int chunk, int nchunks, int qg, int at,
                                             float* part, int xoff) {
@@ -963,135 +1100,280 @@ __device__ __noinline__ void attention_tile(const MegaArgs& a, int l, int kvh, i
         }
     }
     if (tr) *tslot(a, blockIdx.x, 230 + l, 5) = gtimer();
-    // publish: one chunk -> final values; several -> partials, the last chunk merges
-    auto finish = [&](int q, float lsum, int d, float ov) {  // query q, head dim lane + 32 d
-        const int r = q / group, g = q % group;
-        if (d == 0 && !(lsum > 0.0f) && lane == 0) atomicOr(a.status, ST_EMPTY_ROW);
-        const float val = ov / lsum;
-        const int f = (kvh * group + g) * HD + lane + 32 * d;
-        a.att[static_cast<size_t>(r) * a.qd + f] = val;
-        put_split<kRows>(a.xim[P_O], f, r, val);
-    };
-    const int cpk = (a.max_len + kAttnMinKC - 1) / kAttnMinKC;  // chunk slots per kv head
-    constexpr size_t qstride = HD + 2;
-    int qa = 0, qb = nq;  // item queries this CTA finishes
-    if (nchunks > 1) {
-        // every chunk publishes (m, l, o) partials; once all chunks of this
-        // (kv head, query group) have arrived, chunk c merges queries
-        // [c * per, (c + 1) * per) over the chunks in chunk order (the merge is
-        // spread over the head's CTAs, which all run concurrently: items per
-        // head <= grid, mega_supported)
-        float* p0 = part + static_cast<size_t>(kvh) * cpk * 128 * qstride;
-        float* pc = p0 + static_cast<size_t>(chunk) * 128 * qstride;
-        if (wq)
+    attn_publish<HD>(a, l, kvh, chunk, nchunks, qg, at, part, ring, mx, sm, o);
+}
+
+// ── chunked attention, HD = 128: scores on the tensor cores ───────────────
+// S^T [128 keys][64 queries] = K Q^T as tcgen05.mma kind::f16 with BOTH
+// operands split into three bf16 pieces (hi | mid | lo, ~fp32 accuracy):
+// A = the chunk's K pieces (M = 128 key rows), B = the queries' pieces stacked
+// along N (rows 0-63 hi, 64-127 mid, 128-191 lo); per K=16 step
+//   A_hi x B[hi|mid|lo] (N = 192), A_mid x B[hi|mid] (N = 128), A_lo x B[hi] (N = 64)
+// so the three TMEM column blocks hold hi-, mid- and lo-query products and
+// S = (blk0 + blk1) + blk2 drops only the 2^-32-scale cross terms.  The
+// rows' tail keys (row-specific slots) go through a SECOND pass of the same
+// MMAs with the tail K rows in rows 0..15 of the A tile: every (key, query)
+// score is the same tensor-core arithmetic whatever the key's position, so a
+// row's result still depends only on its own compacted key list.  Softmax
+// per query over the chunk (4 threads per query, fixed order) and PV on the
+// CUDA cores in compacted key order, as in attention_tile.
+// Lent-ring layout: [0, 96 KB) K pieces, later V (fp32) + tail V; [96, 144 KB)
+// query pieces, later per-query (m, l); [144, 176 KB) S^T / P^T (float4 chunk
+// h of key j at h ^ (j & 15)).
+constexpr int kTmS = 128;  // TMEM columns [128, 320): the chunk's score pieces
+constexpr int kTmT = 320;  // [320, 512): the tail keys' score pieces
+__host__ __device__ constexpr uint32_t attn_idesc(int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
+}
+__shared__ uint32_t sh_attph;  // phase of the attention MMA barrier
+
+// three bf16 pieces of 4 consecutive features (k % 4 == 0) of row r into SW128
+// K-major tiles: piece p at base + p * pstride, k-block k / 64 at + kbstride
+__device__ __forceinline__ void put3x4(uint8_t* base, uint32_t pstride, uint32_t kbstride, int r, int k, float4 x) {
+    const float v[4] = {x.x, x.y, x.z, x.w};
+    uint32_t h[2], m[2], lo[2];
+#pragma unroll
+    for (int e = 0; e < 4; e += 2) {
+        __nv_bfloat16 hb[2], mb[2], lb[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            hb[u] = __float2bfloat16_rn(v[e + u]);
+            const float r1 = v[e + u] - __bfloat162float(hb[u]);
+            mb[u] = __float2bfloat16_rn(r1);
+            lb[u] = __float2bfloat16_rn(r1 - __bfloat162float(mb[u]));
+        }
+        h[e / 2] = static_cast<uint32_t>(__bfloat16_as_ushort(hb[0])) | (static_cast<uint32_t>(__bfloat16_as_ushort(hb[1])) << 16);
+        m[e / 2] = static_cast<uint32_t>(__bfloat16_as_ushort(mb[0])) | (static_cast<uint32_t>(__bfloat16_as_ushort(mb[1])) << 16);
+        lo[e / 2] = static_cast<uint32_t>(__bfloat16_as_ushort(lb[0])) | (static_cast<uint32_t>(__bfloat16_as_ushort(lb[1])) << 16);
+    }
+    uint8_t* t = base + (k >> 6) * kbstride + sw128_off(r, k & 63);
+    *reinterpret_cast<uint2*>(t) = make_uint2(h[0], h[1]);
+    *reinterpret_cast<uint2*>(t + pstride) = make_uint2(m[0], m[1]);
+    *reinterpret_cast<uint2*>(t + 2 * pstride) = make_uint2(lo[0], lo[1]);
+}
+
+// issue the score MMAs of one pass (thread 0) and wait for them
+__device__ __forceinline__ void attn_score_mma(uint32_t kp, uint32_t qp, uint32_t tcol, uint64_t* attb) {
+    tc_fence_after();
+#pragma unroll
+    for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t bq = smem_desc(qp + kb * 24576) + 2 * ks;
+            const uint64_t ah = smem_desc(kp + kb * 16384) + 2 * ks;
+            mma_bf16_id(tcol, ah, bq, attn_idesc(192), (kb | ks) ? 1u : 0u);
+            mma_bf16_id(tcol, ah + (32768 >> 4), bq, attn_idesc(128), 1u);
+            mma_bf16_id(tcol, ah + (65536 >> 4), bq, attn_idesc(64), 1u);
+        }
+    mma_commit(attb);
+    mwait(attb, sh_attph & 1u);
+    ++sh_attph;
+}
+
+__device__ __noinline__ void attention_tile_tc(const MegaArgs& a, int l, int kvh, int chunk, int nchunks, int qg, int at,
+                                               float* part, int xoff, uint32_t tmem, uint64_t* attb) {
+    constexpr int HD = 128, KC = 128, C4 = 32, DPL = 4;
+    uint8_t* ringb = reinterpret_cast<uint8_t*>(ring_base());
+    uint8_t* sKp = ringb;                                        // 3 x [2 k-blocks][128 rows][128 B]
+    uint8_t* sQp = ringb + 98304;                                // [2 k-blocks][192 rows][128 B]
+    float* sV = reinterpret_cast<float*>(ringb);                 // after the MMAs: V [KC][HD] | tail V [kRows][HD]
+    float* sVt = sV + KC * HD;
+    float* sML = reinterpret_cast<float*>(sQp);                  // after the MMAs: (m, l) per item query
+    float4* sP4 = reinterpret_cast<float4*>(ringb + 147456);     // S^T / P^T [KC][16] float4 (swizzled)
+    float* sTS = reinterpret_cast<float*>(ringb + xoff);         // [16][64] tail scores (epilogue scratch)
+    const int group = a.n_heads / a.n_kv;
+    const int NQ = a.rows * group;
+    const int qbase = qg * 64, nq = min(64, NQ - qbase);
+    const int warp = at >> 5, lane = at & 31;
+    const int prior = sh_prior;
+    const int ncmax = prior + a.rows;
+    const int k0 = chunk * KC, k1 = min(ncmax, k0 + KC);
+    const int ns = max(0, min(k1, prior) - k0);
+    const int kt0 = max(k0, prior);
+    const int ntail = k1 - kt0;
+    const size_t hoff = static_cast<size_t>(l) * a.slab_stride + static_cast<size_t>(kvh) * a.max_len * HD;
+    const float* kbase = a.kbank[0] + hoff;
+    const float* vbase = a.vbank[0] + hoff;
+    const bool tr = a.trace && at == 0;
+    if (tr) *tslot(a, blockIdx.x, 230 + l, 0) = gtimer();
+    // K rows, queries (and tail K rows) into registers, all loads in flight, then split
+    {
+        float4 kx[16], qx[8], tx2[2];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int f = at + 256 * i, r = f >> 5, c = f & 31;
+            kx[i] = r < ns ? __ldcg(reinterpret_cast<const float4*>(kbase + static_cast<size_t>(k0 + r) * HD) + c)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int f = at + 256 * i, qi = f >> 5, c = f & 31, q = qbase + qi;
+            qx[i] = qi < nq ? __ldcg(reinterpret_cast<const float4*>(a.q + static_cast<size_t>(q / group) * a.qd +
+                                                                     static_cast<size_t>(kvh * group + q % group) * HD) + c)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int f = at + 256 * i, r = f >> 5, c = f & 31;
+            tx2[i] = ntail > 0 && r < a.rows
+                         ? __ldcg(reinterpret_cast<const float4*>(kbase + static_cast<size_t>(prior + r) * HD) + c)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int f = at + 256 * i;
+            put3x4(sKp, 32768, 16384, f >> 5, 4 * (f & 31), kx[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {  // query qi: B rows qi (hi), 64 + qi (mid), 128 + qi (lo)
+            const int f = at + 256 * i;
+            put3x4(sQp, 64 * 128, 24576, f >> 5, 4 * (f & 31), qx[i]);
+        }
+        fence_proxy_async();
+        named_sync(3, 256);
+        if (tr) *tslot(a, blockIdx.x, 230 + l, 1) = gtimer();
+        if (at == 0) attn_score_mma(smem_u32(sKp), smem_u32(sQp), tmem + kTmS, attb);
+        named_sync(3, 256);
+        if (ntail > 0) {  // second pass: the tail slots' K rows in rows 0..15 of the A tile
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int f = at + 256 * i;
+                put3x4(sKp, 32768, 16384, f >> 5, 4 * (f & 31), tx2[i]);
+            }
+            fence_proxy_async();
+            named_sync(3, 256);
+            if (at == 0) attn_score_mma(smem_u32(sKp), smem_u32(sQp), tmem + kTmT, attb);
+            named_sync(3, 256);
+        }
+    }
+    // V (and the tail V rows) stream in while the scores are read out
+    for (int t = at; t < ns * C4; t += 256) cp_async16(reinterpret_cast<float4*>(sV) + t, vbase + static_cast<size_t>(k0) * HD + 4 * t);
+    if (ntail > 0)
+        for (int t = at; t < a.rows * C4; t += 256)
+            cp_async16(reinterpret_cast<float4*>(sVt) + t, vbase + static_cast<size_t>(prior) * HD + 4 * t);
+    cp_async_commit();
+    tc_fence_after();
+    {  // S^T rows: the warp's TMEM lane quadrant = keys, half the queries
+        const int quad = (warp + 2) & 3, qh = warp >> 2, key = 32 * quad + lane;
+        const uint32_t lb = static_cast<uint32_t>(32 * quad) << 16;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            float vh[16], vm[16], vl[16];
+            const int qc = 32 * qh + 16 * h;
+            tmem_ld16(tmem + lb + kTmS + qc, vh);
+            tmem_ld16(tmem + lb + kTmS + 64 + qc, vm);
+            tmem_ld16(tmem + lb + kTmS + 128 + qc, vl);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                sP4[key * 16 + ((qc / 4 + c) ^ (key & 15))] =
+                    make_float4((vh[4 * c] + vm[4 * c]) + vl[4 * c], (vh[4 * c + 1] + vm[4 * c + 1]) + vl[4 * c + 1],
+                                (vh[4 * c + 2] + vm[4 * c + 2]) + vl[4 * c + 2], (vh[4 * c + 3] + vm[4 * c + 3]) + vl[4 * c + 3]);
+        }
+        if (ntail > 0 && quad == 0) {  // tail slot `lane`'s scores (tcgen05.ld is warp-collective)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float vh[16], vm[16], vl[16];
+                const int qc = 32 * qh + 16 * h;
+                tmem_ld16(tmem + lb + kTmT + qc, vh);
+                tmem_ld16(tmem + lb + kTmT + 64 + qc, vm);
+                tmem_ld16(tmem + lb + kTmT + 128 + qc, vl);
+                tmem_wait_ld();
+                if (lane < kRows)
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) sTS[lane * 64 + qc + c] = (vh[c] + vm[c]) + vl[c];
+            }
+        }
+    }
+    tc_fence_before();
+    named_sync(3, 256);
+    if (ntail > 0) {  // place each query's tail scores at its compacted positions
+        for (int pi = at; pi < nq * ntail; pi += 256) {
+            const int qi = pi / ntail, t = pi % ntail;
+            const int ts = sh_tail[(qbase + qi) / group][min(kt0 - prior + t, kRows - 1)] - prior;
+            const int key = ns + t;
+            reinterpret_cast<float*>(sP4 + key * 16 + ((qi >> 2) ^ (key & 15)))[qi & 3] = sTS[ts * 64 + qi];
+        }
+        named_sync(3, 256);
+    }
+    if (tr) *tslot(a, blockIdx.x, 230 + l, 2) = gtimer();
+    {  // softmax: 4 threads per query, keys part + 4 t (fixed order)
+        const int qi = at >> 2, part = at & 3, q = qbase + qi;
+        const int nc = qi < nq ? sh_ncols[q / group] : 0;
+        const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(HD));
+        float* sPf = reinterpret_cast<float*>(sP4);
+        float sv[32];
+        float m = -INFINITY;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+            const int key = part + 4 * t, ki = k0 + key;
+            const float x = sPf[(key * 16 + ((qi >> 2) ^ (key & 15))) * 4 + (qi & 3)];
+            sv[t] = (ki < k1 && ki < nc) ? x * inv_sqrt_hd : -INFINITY;
+            m = fmaxf(m, sv[t]);
+        }
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+        float sum = 0.0f;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+            const int key = part + 4 * t;
+            const float p = sv[t] == -INFINITY ? 0.0f : expf(sv[t] - m);
+            sPf[(key * 16 + ((qi >> 2) ^ (key & 15))) * 4 + (qi & 3)] = p;
+            sum += p;
+        }
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        if (part == 0) {
+            sML[2 * qi] = m;
+            sML[2 * qi + 1] = sum;
+        }
+    }
+    cp_async_wait_all();
+    named_sync(3, 256);
+    if (tr) *tslot(a, blockIdx.x, 230 + l, 3) = gtimer();
+    const int q0 = warp * 8;
+    const bool wq = q0 < nq;
+    float mx[8], sm[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        mx[i] = sML[2 * (q0 + i)];
+        sm[i] = sML[2 * (q0 + i) + 1];
+    }
+    float o[8][DPL];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int d = 0; d < DPL; ++d) o[i][d] = 0.0f;
+    if (wq) {
+#pragma unroll 4
+        for (int j = 0; j < ns; ++j) {
+            const float4 p0 = sP4[j * 16 + ((q0 >> 2) ^ (j & 15))];
+            const float4 p1 = sP4[j * 16 + (((q0 >> 2) + 1) ^ (j & 15))];
+            const float pp[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+            float v[DPL];
+#pragma unroll
+            for (int d = 0; d < DPL; ++d) v[d] = sV[j * HD + lane + 32 * d];
+#pragma unroll
+            for (int i = 0; i < 8; i += 2)
+#pragma unroll
+                for (int d = 0; d < DPL; ++d) ffma2(o[i][d], o[i + 1][d], pp[i], pp[i + 1], v[d], v[d]);
+        }
+        for (int ki = kt0; ki < k1; ++ki) {  // tail keys: each query's own V row
+            const int j = ki - k0;
+            const float4 p0 = sP4[j * 16 + ((q0 >> 2) ^ (j & 15))];
+            const float4 p1 = sP4[j * 16 + (((q0 >> 2) + 1) ^ (j & 15))];
+            const float pp[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                if (q0 + i >= nq) continue;
-                float* dst = pc + static_cast<size_t>(qbase + q0 + i) * qstride;
-                if (lane == 0) {
-                    dst[0] = mx[i];
-                    dst[1] = sm[i];
-                }
+                const int r = min(qbase + q0 + i, NQ - 1) / group;
+                const float* vr = sVt + (sh_tail[r][min(ki - prior, kRows - 1)] - prior) * HD;
 #pragma unroll
-                for (int d = 0; d < DPL; ++d) dst[2 + lane + 32 * d] = o[i][d];
-            }
-        named_sync(3, 256);
-        unsigned* cnt = fptr(a, l, K_ATT, a.n_kv + 1 + 2 * kvh + qg);
-        if (at == 0) {
-            __threadfence();  // cumulative over the CTA's partial stores ordered by the barrier
-            atomicAdd(cnt, 1u);
-            if (a.trace) *tslot(a, blockIdx.x, 230 + l, 6) = gtimer();
-            wait_ge(cnt, static_cast<unsigned>(nchunks));
-            if (a.trace) *tslot(a, blockIdx.x, 230 + l, 7) = gtimer();
-        }
-        named_sync(3, 256);
-        const int per = (nq + nchunks - 1) / nchunks;
-        qa = min(nq, chunk * per);
-        qb = min(nq, qa + per);
-        const int nm = qb - qa;
-        if (nm > 0) {
-            // (m, l) of the merged queries x chunks -> per-chunk weights (the ring is still lent)
-            float* sw = ring;                 // [nm][nchunks] (m, then the chunk weights)
-            float* sll = sw + 64 * 64;        // [nm][nchunks] l
-            float* sl = sll + 64 * 64;        // [nm] sums
-            for (int t = at; t < nm * nchunks; t += 256) {
-                const int qi = t / nchunks, ch = t % nchunks;
-                const float* src = p0 + (static_cast<size_t>(ch) * 128 + qbase + qa + qi) * qstride;
-                sw[t] = __ldcg(src);
-                sll[t] = __ldcg(src + 1);
-            }
-            named_sync(3, 256);
-            if (at < nm) {
-                float M = -INFINITY;
-                for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, sw[at * nchunks + ch]);
-                float lsum = 0.0f;  // chunk order; chunks past the row's keys add exact zeros
-                for (int ch = 0; ch < nchunks; ++ch) {
-                    const float mc = sw[at * nchunks + ch];
-                    const float w = mc == -INFINITY ? 0.0f : expf(mc - M);
-                    lsum = fmaf(sll[at * nchunks + ch], w, lsum);
-                    sw[at * nchunks + ch] = w;
-                }
-                sl[at] = lsum;
-            }
-            named_sync(3, 256);
-            for (int t0 = at; t0 < nm * HD; t0 += 512) {  // two outputs per thread, all their loads in flight
-                float acc2[2] = {0.0f, 0.0f};
-                for (int ch0 = 0; ch0 < nchunks; ch0 += 32) {  // chunk order
-                    float t32[2][32];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int t = t0 + 256 * u, qi = min(t, nm * HD - 1) / HD, dd = t % HD;
-                        const float* src = p0 + static_cast<size_t>(qbase + qa + qi) * qstride + 2 + dd;
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            t32[u][j] = ch0 + j < nchunks ? __ldcg(src + static_cast<size_t>(ch0 + j) * 128 * qstride) : 0.0f;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int qi = min(t0 + 256 * u, nm * HD - 1) / HD;
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (ch0 + j < nchunks) acc2[u] = fmaf(t32[u][j], sw[qi * nchunks + ch0 + j], acc2[u]);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                const int t = t0 + 256 * u;
-                if (t >= nm * HD) break;
-                const int qi = t / HD, dd = t % HD, q = qbase + qa + qi;
-                const float acc = acc2[u];
-                const float lsum = sl[qi];
-                const int r = q / group, g = q % group;
-                if (dd == 0 && !(lsum > 0.0f)) atomicOr(a.status, ST_EMPTY_ROW);
-                const float val = acc / lsum;
-                const int f = (kvh * group + g) * HD + dd;
-                a.att[static_cast<size_t>(r) * a.qd + f] = val;
-                put_split<kRows>(a.xim[P_O], f, r, val);
-                }
+                for (int d = 0; d < DPL; ++d) o[i][d] = fmaf(pp[i], vr[lane + 32 * d], o[i][d]);
             }
         }
-    } else if (wq) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (q0 + i < nq)
-#pragma unroll
-                for (int d = 0; d < DPL; ++d) {
-                    const int q = qbase + q0 + i, r = q / group, g = q % group;
-                    const float lsum = sm[i];
-                    if (d == 0 && lane == 0 && !(lsum > 0.0f)) atomicOr(a.status, ST_EMPTY_ROW);
-                    const float val = fmaf(o[i][d], 1.0f, 0.0f) / lsum;
-                    const int f = (kvh * group + g) * HD + lane + 32 * d;
-                    a.att[static_cast<size_t>(r) * a.qd + f] = val;
-                    put_split<kRows>(a.xim[P_O], f, r, val);
-                }
     }
-    fence_proxy_async_global();
-    named_sync(3, 256);
-    if (at == 0) {  // these queries of this kv head are published
-        __threadfence();
-        if (qb > qa) atomicAdd(fptr(a, l, K_ATT, kvh), static_cast<unsigned>(qb - qa));
-        if (a.trace) *tslot(a, blockIdx.x, 230 + l, 8) = gtimer();
-    }
+    if (tr) *tslot(a, blockIdx.x, 230 + l, 5) = gtimer();
+    attn_publish<HD>(a, l, kvh, chunk, nchunks, qg, at, part, reinterpret_cast<float*>(ringb), mx, sm, o);
 }
 
 __device__ __forceinline__ int attn_chunks(const MegaArgs& a) {
@@ -1103,7 +1385,7 @@ __device__ __forceinline__ int attention_items(const MegaArgs& a, int nchunks) {
     return a.n_kv * nchunks * nqg;
 }
 __device__ __forceinline__ void attention_dispatch(const MegaArgs& a, int l, int item, int nchunks, int at, float* part,
-                                                   int xoff) {
+                                                   int xoff, uint32_t tmem, uint64_t* attb) {
     const int group = a.n_heads / a.n_kv;
     const int nqg = (a.rows * group + 63) / 64;
     const int kvh = item / (nchunks * nqg), rem = item % (nchunks * nqg), chunk = rem / nqg, qg = rem % nqg;
@@ -1122,18 +1404,18 @@ __device__ __forceinline__ void attention_dispatch(const MegaArgs& a, int l, int
         case 32: attention_tile<32>(a, l, kvh, chunk, nchunks, qg, at, part, xoff); break;
         case 64: attention_tile<64>(a, l, kvh, chunk, nchunks, qg, at, part, xoff); break;
         case 160: attention_tile<160>(a, l, kvh, chunk, nchunks, qg, at, part, xoff); break;
-        default: attention_tile<128>(a, l, kvh, chunk, nchunks, qg, at, part, xoff); break;
+        default: attention_tile_tc(a, l, kvh, chunk, nchunks, qg, at, part, xoff, tmem, attb); break;
     }
 }
 // the chunked design's attention phase of layer l for the attention threads
 // (warps 2..9): wait for the lent ring, run this CTA's items, give it back
 __device__ __forceinline__ void attention_phase_lent(const MegaArgs& a, int l, int at, uint64_t* lentb, uint64_t* retb,
-                                                     int xoff) {
+                                                     int xoff, uint32_t tmem, uint64_t* attb) {
     if (at == 0) mwait(lentb, static_cast<uint32_t>(l & 1));
     named_sync(3, 256);
     const int nchunks = attn_chunks(a);
     for (int it = blockIdx.x; it < attention_items(a, nchunks); it += gridDim.x)
-        attention_dispatch(a, l, it, nchunks, at, a.apart, xoff);
+        attention_dispatch(a, l, it, nchunks, at, a.apart, xoff, tmem, attb);
     fence_proxy_async();  // generic-proxy ring accesses before the producer's bulk copies
     named_sync(3, 256);
     if (at == 0) mbar_arrive(retb);
@@ -1197,7 +1479,8 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
     uint64_t* tempty = tfull + 2;
     uint64_t* lentb = tempty + 2;  // chunked attention: ring lent to the attention phase / given back
     uint64_t* retb = lentb + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(retb + 1);
+    uint64_t* attb = retb + 1;     // chunked attention: score MMAs complete
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(attb + 1);
     int* flag = reinterpret_cast<int*>(tmem_slot + 4);
     float* xch = reinterpret_cast<float*>(flag + 4);          // 64*16 gate|up + 4*16 sumsq
     float* rs = xch + 64 * kRows + 4 * kRows;                  // [kMaxRows] per-row 1/rms of the phase
@@ -1261,6 +1544,8 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
         }
         mbar_init(lentb, 1);
         mbar_init(retb, 1);
+        mbar_init(attb, 1);
+        sh_attph = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
@@ -1647,7 +1932,8 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                             attention_rows_dispatch<RR>(a, L, l, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst,
                                                     ocomb, cols);
                     } else {
-                        attention_phase_lent(a, l, threadIdx.x - 64, lentb, retb, static_cast<int>(reinterpret_cast<uint8_t*>(xch) - smem));
+                        attention_phase_lent(a, l, threadIdx.x - 64, lentb, retb, static_cast<int>(reinterpret_cast<uint8_t*>(xch) - smem),
+                                             tmem, attb);
                     }
                     if (a.trace && et == 0) *tslot(a, c, 5 * l + 2, 2) = gtimer();
                 }
@@ -1721,7 +2007,8 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
                             attention_rows_dispatch<RR>(a, L, l, it / a.n_kv, it % a.n_kv, threadIdx.x - 64, qs, wst,
                                                     ocomb, cols);
                     } else {
-                        attention_phase_lent(a, l, threadIdx.x - 64, lentb, retb, static_cast<int>(reinterpret_cast<uint8_t*>(xch) - smem));
+                        attention_phase_lent(a, l, threadIdx.x - 64, lentb, retb, static_cast<int>(reinterpret_cast<uint8_t*>(xch) - smem),
+                                             tmem, attb);
                     }
                 }
             }
@@ -1769,7 +2056,7 @@ size_t dyn_smem_budget(bool rows_attn) {
 // dynamic shared memory of a launch with row capacity R (must match the
 // kernel's carve-up: ring | barriers | xch | rs | attention | ropeT | hpre)
 size_t smem_bytes(bool rows_attn, int stages, int hd, int group, int max_len, int R = kRows) {
-    return 1024 + static_cast<size_t>(stages) * (kABytes + 384 * R) + (2 * kMaxStages + 6) * 8 + 32 +
+    return 1024 + static_cast<size_t>(stages) * (kABytes + 384 * R) + (2 * kMaxStages + 7) * 8 + 32 +
            sizeof(float) * (64 * kRows + 4 * kRows + kMaxRows + attn_scratch_floats(rows_attn, hd, group, max_len) +
                             (R == kRows ? kRows * hd : 0) + R * kM + kM) + 16;
 }
@@ -2000,6 +2287,7 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     a.stage_bytes = tc::kABytes + a.xbytes;
     a.acc_cols = RS == tc::kRows ? kAccCols : 128;
     a.tmem_cols = 2 * a.acc_cols > kTmemCols ? 2 * a.acc_cols : kTmemCols;
+    if (!ra) a.tmem_cols = 512;  // chunked attention: score pieces in columns [128, 512)
     a.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>((3 * RS) >> 3) << 17) |
               (static_cast<uint32_t>(tc::kM >> 4) << 24);
     const Dims dl = e.dims();  // this engine's shard (tensor parallelism: local heads / FFN columns)
