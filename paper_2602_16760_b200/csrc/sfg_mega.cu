@@ -1480,7 +1480,8 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
     uint64_t* lentb = tempty + 2;  // chunked attention: ring lent to the attention phase / given back
     uint64_t* retb = lentb + 1;
     uint64_t* attb = retb + 1;     // chunked attention: score MMAs complete
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(attb + 1);
+    // (one pad slot: the scratch below stays 16-byte aligned for float4 / cp.async)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(attb + 2);
     int* flag = reinterpret_cast<int*>(tmem_slot + 4);
     float* xch = reinterpret_cast<float*>(flag + 4);          // 64*16 gate|up + 4*16 sumsq
     float* rs = xch + 64 * kRows + 4 * kRows;                  // [kMaxRows] per-row 1/rms of the phase
@@ -1494,6 +1495,7 @@ __global__ void __launch_bounds__(kThreads, 1) mega_kernel(const __grid_constant
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = gridDim.x, c = blockIdx.x;
+    if (threadIdx.x == 0 && (smem_u32(xch) & 15u)) asm volatile("trap;");  // float4 / cp.async scratch alignment
     if (threadIdx.x == 0 && a.trace) *tslot(a, c, kBarSlots - 1, 0) = gtimer();
     if (threadIdx.x < kMaxRows) sh_pos[threadIdx.x] = static_cast<int>(threadIdx.x) < a.rows ? a.pos[threadIdx.x] : 0;
     for (int i = threadIdx.x; RR == kRows && i < kRows * a.hd; i += blockDim.x) {  // RoPE table rows (host-libm values)
@@ -2056,7 +2058,7 @@ size_t dyn_smem_budget(bool rows_attn) {
 // dynamic shared memory of a launch with row capacity R (must match the
 // kernel's carve-up: ring | barriers | xch | rs | attention | ropeT | hpre)
 size_t smem_bytes(bool rows_attn, int stages, int hd, int group, int max_len, int R = kRows) {
-    return 1024 + static_cast<size_t>(stages) * (kABytes + 384 * R) + (2 * kMaxStages + 7) * 8 + 32 +
+    return 1024 + static_cast<size_t>(stages) * (kABytes + 384 * R) + (2 * kMaxStages + 8) * 8 + 32 +
            sizeof(float) * (64 * kRows + 4 * kRows + kMaxRows + attn_scratch_floats(rows_attn, hd, group, max_len) +
                             (R == kRows ? kRows * hd : 0) + R * kM + kM) + 16;
 }
