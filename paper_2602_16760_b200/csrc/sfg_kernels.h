@@ -76,6 +76,11 @@ int launch_attention_fast(const float* q, const float* kcache, const float* vcac
 // prompt passes whose mask follows the prefix law (every row one run [0, lim),
 // value 0): K/V blocks staged once per 64 queries
 bool attention_prompt_supported(const Dims& d);
+// tensor-core causal prompt attention (sfg_attn_tc.cu): head_dim 128
+bool attention_prompt_tc_supported(const Dims& d);
+int launch_attention_prompt_tc(const float* q, const float* kcache, const float* vcache, const int32_t* row_off,
+                               const MaskRun* runs, int rows, const Dims& d, float* att, uint32_t* status,
+                               cudaStream_t s);
 int launch_attention_prompt(const float* q, const float* kcache, const float* vcache, const int32_t* row_off,
                             const MaskRun* runs, int rows, const Dims& d, float* att, uint32_t* status,
                             cudaStream_t s);
