@@ -400,10 +400,11 @@ bool attention_prompt_supported(const Dims& d) {
 }
 
 int launch_attention_prompt(const float* q, const float* kcache, const float* vcache, const int32_t* row_off,
-                            const MaskRun* runs, int rows, const Dims& d, float* att, uint32_t* status,
-                            cudaStream_t s) {
+                            const MaskRun* runs, int rows, int keys, const Dims& d, float* att, uint32_t* status,
+                            cudaStream_t s, void** scratch, size_t* scratch_bytes) {
     if (attention_prompt_tc_supported(d))
-        return launch_attention_prompt_tc(q, kcache, vcache, row_off, runs, rows, d, att, status, s);
+        return launch_attention_prompt_tc(q, kcache, vcache, row_off, runs, rows, keys, d, att, status, s, scratch,
+                                          scratch_bytes);
     switch (d.hd) {
         case 64: return launch_prompt_hd<64>(q, kcache, vcache, row_off, runs, rows, d, att, status, s);
         case 128: return launch_prompt_hd<128>(q, kcache, vcache, row_off, runs, rows, d, att, status, s);

@@ -16,13 +16,17 @@
 // running max, its O row is rescaled in TMEM (tcgen05.ld / st) before the
 // next PV MMA accumulates into it.
 //
-// Warp roles (288 threads, one CTA per SM: 192 KB of shared memory, 512 TMEM
+// The fp32 queries and KV cache are split ONCE per layer by split_q_kernel /
+// split_kv_kernel into bf16 pieces already in the MMA's SW128 K-major tile
+// layout (Q [kv head][query block][piece][k-block][128 x 128 B], K [kv head][key
+// block][piece][k-block][64 x 128 B], V^T [kv head][key block][piece][128 dims x
+// 128 B]); the attention CTAs fetch them with one bulk copy per operand block
+// (the ~32 query blocks reading a key block no longer re-split it).
+// Warp roles (192 threads, one CTA per SM: 192 KB of shared memory, 512 TMEM
 // columns):
 //   warps 0-3  softmax + output: thread = query = TMEM lane;
-//   warps 4-7  producer: Q once, then per block the K pieces ([key][dim],
-//              K-major) and the V^T pieces ([dim][key], K-major) from the
-//              fp32 KV cache, split on the fly;
-//   warp 8     MMA issuer (one thread).
+//   warp 4     producer (one thread): bulk copies of Q once, then K / V^T per block;
+//   warp 5     MMA issuer (one thread).
 // mbarriers: k_ready / v_ready (producer -> MMA), s_full (MMA -> softmax and
 // producer: K consumed), s_free (softmax -> MMA: S read), p_ready (softmax ->
 // MMA), pv_done (MMA -> softmax: O final for the block, P and V consumed).
@@ -43,16 +47,16 @@ using namespace tc;
 
 constexpr int kHD = 128;
 constexpr int kQ = 128;       // queries per CTA (TMEM lanes)
-constexpr int kKB = 64;       // keys per block
-constexpr int kThreadsTC = 288;
+constexpr int kKeyBlk = 64;       // keys per block
+constexpr int kThreadsTC = 192;
 // shared memory: Q pieces 3 x [2 k-blocks][128 rows][128 B] | K pieces 3 x [2][64][128 B] | V^T pieces 3 x [128 dims][128 B]
 constexpr int kQBytes = 3 * 2 * 128 * 128;  // 96 KB
 constexpr int kKBytes = 3 * 2 * 64 * 128;   // 48 KB
 constexpr int kVBytes = 3 * 128 * 128;      // 48 KB
 constexpr int kSmemTC = 1024 + kQBytes + kKBytes + kVBytes + 256;
 // TMEM columns
-constexpr uint32_t kColS = 0;    // S [128 q][64 keys] fp32
-constexpr uint32_t kColP = 64;   // P pieces 3 x 32 columns (bf16 pairs)
+constexpr uint32_t kColS = 0;    // S [128 q][64 keys] fp32, two buffers (block parity): columns 0 / 64
+constexpr uint32_t kColP = 128;  // P pieces 3 x 32 columns (bf16 pairs)
 constexpr uint32_t kColO = 256;  // O [128 q][128 dims] fp32
 
 __host__ __device__ constexpr uint32_t idesc_mn(int M, int N) {
@@ -114,6 +118,12 @@ __device__ __forceinline__ void bwait(uint64_t* b, uint32_t parity) {
     }
 }
 
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // three bf16 pieces of x
 struct Split3 {
     __nv_bfloat16 h, m, l;
@@ -140,8 +150,51 @@ __device__ __forceinline__ void put3x4(uint8_t* base, uint32_t pstride, uint32_t
     *reinterpret_cast<uint2*>(t + 2 * pstride) = make_uint2(pack2(s0.l, s1.l), pack2(s2.l, s3.l));
 }
 
-__global__ void __launch_bounds__(kThreadsTC, 1) attn_prompt_tc_kernel(const float* __restrict__ q, const float* __restrict__ kc,
-                                                                        const float* __restrict__ vc,
+// the queries / K / V^T as bf16 pieces in the MMA tile layout (see the header)
+__global__ void split_q_kernel(const float* __restrict__ q, Dims d, int rows, int nqb, uint8_t* __restrict__ Qp) {
+    const int G = d.n_heads / d.n_kv, RB = kQ / G;
+    const size_t n = static_cast<size_t>(d.n_kv) * nqb * kQ * 32;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i & 31), qi = static_cast<int>((i >> 5) % kQ);
+        const size_t hb = i / (32 * kQ);  // kv head * nqb + query block
+        const int qb = static_cast<int>(hb % nqb), h = static_cast<int>(hb / nqb);
+        const int row = qb * RB + qi / G, g = qi % G;
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < rows)
+            x = __ldg(reinterpret_cast<const float4*>(q + static_cast<size_t>(row) * d.qd + static_cast<size_t>(h * G + g) * kHD) + c);
+        put3x4(Qp + hb * kQBytes, 32768, 16384, qi, 4 * c, x.x, x.y, x.z, x.w);
+    }
+}
+__global__ void split_kv_kernel(const float* __restrict__ kc, const float* __restrict__ vc, Dims d, int keys, int nkb,
+                                uint8_t* __restrict__ Kp, uint8_t* __restrict__ Vp) {
+    const size_t n = static_cast<size_t>(d.n_kv) * nkb * kKeyBlk * 32;  // per head: nkb*64 keys x 32 float4 (K); same count of V quads
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        {  // K: key j, dims 4c..4c+3
+            const int c = static_cast<int>(i & 31);
+            const size_t hj = i >> 5;
+            const int j = static_cast<int>(hj % (static_cast<size_t>(nkb) * kKeyBlk)), h = static_cast<int>(hj / (static_cast<size_t>(nkb) * kKeyBlk));
+            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (j < keys) x = __ldg(reinterpret_cast<const float4*>(kc + (static_cast<size_t>(h) * d.max_len + j) * kHD) + c);
+            put3x4(Kp + (static_cast<size_t>(h) * nkb + j / kKeyBlk) * kKBytes, 16384, 8192, j % kKeyBlk, 4 * c, x.x, x.y, x.z, x.w);
+        }
+        {  // V^T: dim dd, keys 4jq..4jq+3 (consecutive threads: consecutive dims, coalesced loads)
+            const int dd = static_cast<int>(i % kHD);
+            const size_t hq = i / kHD;
+            const int jq = static_cast<int>(hq % (static_cast<size_t>(nkb) * kKeyBlk / 4)), h = static_cast<int>(hq / (static_cast<size_t>(nkb) * kKeyBlk / 4));
+            float v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = 4 * jq + u;
+                v[u] = j < keys ? __ldg(vc + (static_cast<size_t>(h) * d.max_len + j) * kHD + dd) : 0.0f;
+            }
+            put3x4(Vp + (static_cast<size_t>(h) * nkb + (4 * jq) / kKeyBlk) * kVBytes, 16384, 0, dd, (4 * jq) % kKeyBlk, v[0], v[1], v[2], v[3]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreadsTC, 1) attn_prompt_tc_kernel(const uint8_t* __restrict__ Qp,
+                                                                        const uint8_t* __restrict__ Kp,
+                                                                        const uint8_t* __restrict__ Vp, int nkb,
                                                                         const int32_t* __restrict__ row_off,
                                                                         const MaskRun* __restrict__ runs, Dims d, int rows,
                                                                         float* __restrict__ att, uint32_t* status) {
@@ -151,8 +204,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) attn_prompt_tc_kernel(const flo
     uint8_t* sK = sQ + kQBytes;
     uint8_t* sV = sK + kKBytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVBytes);
-    uint64_t *k_ready = bars, *v_ready = bars + 1, *s_full = bars + 2, *s_free = bars + 3, *p_ready = bars + 4,
-             *pv_done = bars + 5;
+    // s_full / s_free: one pair per S buffer (block parity), so no waiter can
+    // ever be two phases behind its barrier
+    uint64_t *k_ready = bars, *v_ready = bars + 1, *s_full = bars + 2, *s_free = bars + 4, *p_ready = bars + 6,
+             *pv_done = bars + 7;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
     __shared__ int lim_s[kQ];
     __shared__ int kmax_s;
@@ -165,10 +220,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) attn_prompt_tc_kernel(const flo
         lim_s[threadIdx.x] = row < rows ? runs[row_off[row]].end : 0;
     }
     if (threadIdx.x == 0) {
-        mbar_init(k_ready, 128);
-        mbar_init(v_ready, 128);
-        mbar_init(s_full, 1);
-        mbar_init(s_free, 128);
+        mbar_init(k_ready, 1);
+        mbar_init(v_ready, 1);
+        mbar_init(&s_full[0], 1);
+        mbar_init(&s_full[1], 1);
+        mbar_init(&s_free[0], 128);
+        mbar_init(&s_free[1], 128);
         mbar_init(p_ready, 128);
         mbar_init(pv_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -184,67 +241,48 @@ __global__ void __launch_bounds__(kThreadsTC, 1) attn_prompt_tc_kernel(const flo
     }
     __syncthreads();
     const uint32_t tmem = *tslot;
-    const int nblk = (kmax_s + kKB - 1) / kKB;
-    const float* kbase = kc + static_cast<size_t>(kvh) * d.max_len * kHD;
-    const float* vbase = vc + static_cast<size_t>(kvh) * d.max_len * kHD;
+    const int nblk = (kmax_s + kKeyBlk - 1) / kKeyBlk;
 
-    if (warp >= 4 && warp < 8) {
-        // ── producer: Q once, then K / V^T pieces per block ──────────────
-        const int pt = threadIdx.x - 128;
-        for (int i = 0; i < 32; ++i) {  // 128 queries x 32 float4
-            const int f = pt + 128 * i, qi = f >> 5, c = f & 31, row = r0 + qi / G, g = qi % G;
-            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (row < rows)
-                x = __ldg(reinterpret_cast<const float4*>(q + static_cast<size_t>(row) * d.qd +
-                                                           static_cast<size_t>(kvh * G + g) * kHD) + c);
-            put3x4(sQ, 32768, 16384, qi, 4 * c, x.x, x.y, x.z, x.w);
-        }
-        for (int b = 0; b < nblk; ++b) {
-            const int k0 = b * kKB, nk = min(kKB, kmax_s - k0);
-            float4 kx[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {  // 64 keys x 32 float4
-                const int f = pt + 128 * i, r = f >> 5, c = f & 31;
-                kx[i] = r < nk ? __ldg(reinterpret_cast<const float4*>(kbase + static_cast<size_t>(k0 + r) * kHD) + c)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (warp == 4) {
+        // ── producer: bulk copies of the pre-split operand blocks ─────────
+        if (lane == 0) {
+            const uint8_t* qsrc = Qp + (static_cast<size_t>(kvh) * gridDim.x + (gridDim.x - 1 - blockIdx.x)) * kQBytes;
+            for (int b = 0; b < nblk; ++b) {
+                if (b > 0) bwait(&s_full[(b - 1) & 1], static_cast<uint32_t>(((b - 1) >> 1) & 1));  // S_{b-1} has consumed K
+                mbar_expect_tx(k_ready, (b == 0 ? kQBytes : 0) + kKBytes);
+                if (b == 0) bulk_g2s(sQ, qsrc, kQBytes, k_ready);
+                bulk_g2s(sK, Kp + (static_cast<size_t>(kvh) * nkb + b) * kKBytes, kKBytes, k_ready);
+                if (b > 0) bwait(pv_done, static_cast<uint32_t>((b - 1) & 1));  // PV_{b-1} has consumed V
+                mbar_expect_tx(v_ready, kVBytes);
+                bulk_g2s(sV, Vp + (static_cast<size_t>(kvh) * nkb + b) * kVBytes, kVBytes, v_ready);
             }
-            // V^T: this thread's dim = pt, keys 4j..4j+3 (lanes read consecutive dims: coalesced)
-            float vx[64];
-#pragma unroll
-            for (int j = 0; j < 64; ++j) vx[j] = j < nk ? __ldg(vbase + static_cast<size_t>(k0 + j) * kHD + pt) : 0.0f;
-            if (b > 0) bwait(s_full, static_cast<uint32_t>((b - 1) & 1));  // S_{b-1} has consumed K
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int f = pt + 128 * i;
-                put3x4(sK, 16384, 8192, f >> 5, 4 * (f & 31), kx[i].x, kx[i].y, kx[i].z, kx[i].w);
-            }
-            fence_proxy_async();
-            mbar_arrive(k_ready);
-            if (b > 0) bwait(pv_done, static_cast<uint32_t>((b - 1) & 1));  // PV_{b-1} has consumed V
-#pragma unroll
-            for (int j = 0; j < 64; j += 4) put3x4(sV, 16384, 0, pt, j, vx[j], vx[j + 1], vx[j + 2], vx[j + 3]);
-            fence_proxy_async();
-            mbar_arrive(v_ready);
         }
-    } else if (warp == 8) {
+    } else if (warp == 5) {
         // ── MMA issuer ───────────────────────────────────────────────────
         if (lane == 0) {
             const uint32_t aq = smem_u32(sQ), bk = smem_u32(sK), bv = smem_u32(sV);
             const uint32_t idS = idesc_mn(128, 64), idO = idesc_mn(128, 128);
             // piece pairs (a, b): hh hm mh hl mm lh
             const int pa[6] = {0, 0, 1, 0, 1, 2}, pb[6] = {0, 1, 0, 2, 1, 0};
-            for (int b = 0; b < nblk; ++b) {
-                bwait(k_ready, static_cast<uint32_t>(b & 1));
-                if (b > 0) bwait(s_free, static_cast<uint32_t>((b - 1) & 1));
+            // software pipelined: S_{b+1} is issued before PV_b, so the tensor
+            // pipe computes the next scores while the softmax warps work on block b
+            auto issue_s = [&](int j) {
+                bwait(k_ready, static_cast<uint32_t>(j & 1));
+                if (j >= 2) bwait(&s_free[j & 1], static_cast<uint32_t>(((j - 2) >> 1) & 1));  // S_{j-2} read
                 tc_fence_after();
+                const uint32_t ds = tmem + kColS + 64 * (j & 1);
                 for (int kb = 0; kb < 2; ++kb)
                     for (int ks = 0; ks < 4; ++ks)
                         for (int e = 0; e < 6; ++e) {
                             const uint64_t a = smem_desc(aq + pa[e] * 32768 + kb * 16384) + 2 * ks;
                             const uint64_t bb = smem_desc(bk + pb[e] * 16384 + kb * 8192) + 2 * ks;
-                            mma_ss(tmem + kColS, a, bb, idS, (kb | ks | e) ? 1u : 0u);
+                            mma_ss(ds, a, bb, idS, (kb | ks | e) ? 1u : 0u);
                         }
-                mma_commit(s_full);
+                mma_commit(&s_full[j & 1]);
+            };
+            if (nblk > 0) issue_s(0);
+            for (int b = 0; b < nblk; ++b) {
+                if (b + 1 < nblk) issue_s(b + 1);
                 bwait(p_ready, static_cast<uint32_t>(b & 1));
                 bwait(v_ready, static_cast<uint32_t>(b & 1));
                 tc_fence_after();
@@ -261,18 +299,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1) attn_prompt_tc_kernel(const flo
         const int qi = threadIdx.x;
         const int lim = lim_s[qi];
         const uint32_t lb = static_cast<uint32_t>(warp * 32) << 16;
-        const float scale = 1.0f / sqrtf(static_cast<float>(kHD));
+        // scores live in the log2 domain: p = 2^(s * scale * log2(e) - m) (ex2.approx,
+        // ~2^-22 relative), the same softmax as exp(s * scale - m')
+        const float scale = 1.4426950408889634f / sqrtf(static_cast<float>(kHD));
         float m = -INFINITY, l = 0.0f;
         for (int b = 0; b < nblk; ++b) {
-            const int k0 = b * kKB;
-            bwait(s_full, static_cast<uint32_t>(b & 1));
+            const int k0 = b * kKeyBlk;
+            bwait(&s_full[b & 1], static_cast<uint32_t>((b >> 1) & 1));
             tc_fence_after();
             uint32_t sr[2][32];
-            tmem_ld32(tmem + lb + kColS, sr[0]);
-            tmem_ld32(tmem + lb + kColS + 32, sr[1]);
+            tmem_ld32(tmem + lb + kColS + 64 * (b & 1), sr[0]);
+            tmem_ld32(tmem + lb + kColS + 64 * (b & 1) + 32, sr[1]);
             tmem_wait_ld();
             tc_fence_before();
-            mbar_arrive(s_free);
+            mbar_arrive(&s_free[b & 1]);
             float s[64];
             float mb = -INFINITY;
 #pragma unroll
@@ -285,8 +325,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) attn_prompt_tc_kernel(const flo
             uint32_t ph[32], pm[32], pl[32];
 #pragma unroll
             for (int j = 0; j < 64; j += 2) {
-                const float p0 = s[j] == -INFINITY ? 0.0f : expf(s[j] - mn);
-                const float p1 = s[j + 1] == -INFINITY ? 0.0f : expf(s[j + 1] - mn);
+                const float p0 = s[j] == -INFINITY ? 0.0f : ex2(s[j] - mn);
+                const float p1 = s[j + 1] == -INFINITY ? 0.0f : ex2(s[j + 1] - mn);
                 rs += p0 + p1;
                 const Split3 a = split3(p0), c = split3(p1);
                 ph[j >> 1] = pack2(a.h, c.h);
@@ -300,7 +340,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) attn_prompt_tc_kernel(const flo
             // the warp rescales together, alpha = 1 for the other lanes)
             const bool need = b > 0 && m != -INFINITY && mn > m;
             if (__any_sync(0xffffffffu, need)) {
-                const float alpha = need ? expf(m - mn) : 1.0f;
+                const float alpha = need ? ex2(m - mn) : 1.0f;
 #pragma unroll
                 for (int c4 = 0; c4 < 4; ++c4) {
                     uint32_t o[32];
@@ -366,13 +406,28 @@ bool attention_prompt_tc_supported(const Dims& d) {
 }
 
 int launch_attention_prompt_tc(const float* q, const float* kcache, const float* vcache, const int32_t* row_off,
-                               const MaskRun* runs, int rows, const Dims& d, float* att, uint32_t* status,
-                               cudaStream_t s) {
+                               const MaskRun* runs, int rows, int keys, const Dims& d, float* att, uint32_t* status,
+                               cudaStream_t s, void** scratch, size_t* scratch_bytes) {
+    const int G = d.n_heads / d.n_kv, rb = kQ / G;
+    const int nqb = (rows + rb - 1) / rb, nkb = (keys + kKeyBlk - 1) / kKeyBlk;
+    const size_t qb = static_cast<size_t>(d.n_kv) * nqb * kQBytes, kb = static_cast<size_t>(d.n_kv) * nkb * kKBytes;
+    const size_t need = qb + 2 * kb;
+    if (*scratch_bytes < need) {  // grow (rare): the previous user of the buffer must be done
+        SFG_CUDA(cudaStreamSynchronize(s));
+        if (*scratch) cudaFree(*scratch);
+        *scratch = nullptr;
+        SFG_CUDA(cudaMalloc(scratch, need));
+        *scratch_bytes = need;
+    }
+    uint8_t* Qp = static_cast<uint8_t*>(*scratch);
+    uint8_t* Kp = Qp + qb;
+    uint8_t* Vp = Kp + kb;
+    const int nsm = device_sm_count();
+    split_q_kernel<<<4 * nsm, 256, 0, s>>>(q, d, rows, nqb, Qp);
+    split_kv_kernel<<<4 * nsm, 256, 0, s>>>(kcache, vcache, d, keys, nkb, Kp, Vp);
     ensure_smem_attr(reinterpret_cast<const void*>(attn_prompt_tc_kernel), kSmemTC);
-    const int rb = kQ / (d.n_heads / d.n_kv);
-    const dim3 grid((rows + rb - 1) / rb, d.n_kv);
-    attn_prompt_tc_kernel<<<grid, kThreadsTC, kSmemTC, s>>>(q, kcache, vcache, row_off, runs, d, rows, att, status);
-    return 1;
+    attn_prompt_tc_kernel<<<dim3(nqb, d.n_kv), kThreadsTC, kSmemTC, s>>>(Qp, Kp, Vp, nkb, row_off, runs, d, rows, att, status);
+    return 3;
 }
 
 }  // namespace sfg

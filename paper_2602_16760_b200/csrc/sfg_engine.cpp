@@ -140,7 +140,7 @@ MaskRuns runs_from_dense(const float* mask, int rows, int kv) {
 void Workspace::release() {
     for (void* p : {(void*)h, (void*)xn, (void*)q, (void*)att, (void*)act, (void*)logits, (void*)pos,
                     (void*)ids, (void*)argmax, (void*)keep, (void*)row_off, (void*)runs, (void*)status,
-                    (void*)clamped, wire, fast, pimg, (void*)meta})
+                    (void*)clamped, wire, fast, pimg, apieces, (void*)meta})
         if (p) cudaFree(p);
     if (pinned) cudaFreeHost(pinned);
     if (meta_pin) cudaFreeHost(meta_pin);

@@ -87,6 +87,8 @@ struct Workspace {
     size_t fast_bytes = 0;
     void* pimg = nullptr;          // FAST prompt passes: token-tiled split image [tiles][KB][3][128 x 64]
     size_t pimg_bytes = 0;
+    void* apieces = nullptr;       // FAST prompt attention: pre-split Q / K / V^T tiles (sfg_attn_tc.cu)
+    size_t apieces_bytes = 0;
     void* pinned = nullptr;        // host staging
     size_t pinned_bytes = 0;
     void* wire_pin = nullptr;      // pinned wire rows [cap_rows x H] (4 B each): frame tensors cross here

@@ -1064,7 +1064,8 @@ static int fast_forward_layer_prompt(Engine& e, Bank& b, int layer, int rows, Wo
         const double kvb = 2.0 * 4.0 * d.kvd * (prior + rows);
         ProfScope ps(K_ATTN, s, kvb + 8.0 * R * d.qd, 4.0 * R * d.qd * (prior + rows));
         if (ws.prefix_mask && attention_prompt_supported(d)) {
-            n += launch_attention_prompt(ws.q, kc, vc, ws.row_off, ws.runs, rows, d, ws.att, ws.status, s);
+            n += launch_attention_prompt(ws.q, kc, vc, ws.row_off, ws.runs, rows, prior + rows, d, ws.att, ws.status, s,
+                                         &ws.apieces, &ws.apieces_bytes);
         } else {
             int cap = 0;  // prompt passes are never graph-captured: size by the cache length
             cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;

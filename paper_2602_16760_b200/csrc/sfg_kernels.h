@@ -79,11 +79,13 @@ bool attention_prompt_supported(const Dims& d);
 // tensor-core causal prompt attention (sfg_attn_tc.cu): head_dim 128
 bool attention_prompt_tc_supported(const Dims& d);
 int launch_attention_prompt_tc(const float* q, const float* kcache, const float* vcache, const int32_t* row_off,
-                               const MaskRun* runs, int rows, const Dims& d, float* att, uint32_t* status,
-                               cudaStream_t s);
+                               const MaskRun* runs, int rows, int keys, const Dims& d, float* att, uint32_t* status,
+                               cudaStream_t s, void** scratch, size_t* scratch_bytes);
+// keys: the cache length the prompt rows attend over (prior + rows); scratch:
+// the workspace's buffer for the tensor-core path's pre-split operands
 int launch_attention_prompt(const float* q, const float* kcache, const float* vcache, const int32_t* row_off,
-                            const MaskRun* runs, int rows, const Dims& d, float* att, uint32_t* status,
-                            cudaStream_t s);
+                            const MaskRun* runs, int rows, int keys, const Dims& d, float* att, uint32_t* status,
+                            cudaStream_t s, void** scratch, size_t* scratch_bytes);
 
 // ── shared kernels (sfg_common.cu) ────────────────────────────────────────
 int launch_embed(const void* table, int wt, const int32_t* ids, int rows, int H, float* out,
