@@ -792,7 +792,7 @@ __device__ __forceinline__ float* ring_base() {
 // query group) merge in chunk order, each CTA a slice of the queries
 template <int HD>
 __device__ __forceinline__ void attn_publish(const MegaArgs& a, int l, int kvh, int chunk, int nchunks, int qg, int at,
-                                             float* part, float* ring, const float (&mx)[8], const float (&sm)[8],
+                                             float* part, float* scratch, const float (&mx)[8], const float (&sm)[8],
                                              const float (&o)[8][HD / 32]) {
     constexpr int DPL = HD / 32;
     const int group = a.n_heads / a.n_kv;
@@ -840,10 +840,27 @@ __device__ __forceinline__ void attn_publish(const MegaArgs& a, int l, int kvh, 
         qb = min(nq, qa + per);
         const int nm = qb - qa;
         if (nm > 0) {
+            // this thread's first batch of partial o values (<= 2 outputs x 32
+            // chunks) is requested BEFORE the (m, l) staging below, so both
+            // travel in the same L2 round trip
+            float t32[2][32];
+            auto load_batch = [&](int t0, int ch0) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int t = t0 + 256 * u, qi = min(t, nm * HD - 1) / HD, dd = t % HD;
+                    const float* src = p0 + static_cast<size_t>(qbase + qa + qi) * qstride + 2 + dd;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        t32[u][j] = ch0 + j < nchunks ? __ldcg(src + static_cast<size_t>(ch0 + j) * 128 * qstride) : 0.0f;
+                }
+            };
+            load_batch(at, 0);
             // (m, l) of the merged queries x chunks -> per-chunk weights (the ring is still lent)
-            float* sw = ring;                 // [nm][nchunks] (m, then the chunk weights)
-            float* sll = sw + 64 * 64;        // [nm][nchunks] l
-            float* sl = sll + 64 * 64;        // [nm] sums
+            // small scratch outside the ring (nm * nchunks < nq + nchunks <= 128): the
+            // tensor-core path has already given the ring back to the producer
+            float* sw = scratch;              // [nm][nchunks] (m, then the chunk weights)
+            float* sll = sw + 128;            // [nm][nchunks] l
+            float* sl = sll + 128;            // [nm] sums
             for (int t = at; t < nm * nchunks; t += 256) {
                 const int qi = t / nchunks, ch = t % nchunks;
                 const float* src = p0 + (static_cast<size_t>(ch) * 128 + qbase + qa + qi) * qstride;
@@ -851,31 +868,30 @@ __device__ __forceinline__ void attn_publish(const MegaArgs& a, int l, int kvh, 
                 sll[t] = __ldcg(src + 1);
             }
             named_sync(3, 256);
-            if (at < nm) {
-                float M = -INFINITY;
-                for (int ch = 0; ch < nchunks; ++ch) M = fmaxf(M, sw[at * nchunks + ch]);
-                float lsum = 0.0f;  // chunk order; chunks past the row's keys add exact zeros
-                for (int ch = 0; ch < nchunks; ++ch) {
-                    const float mc = sw[at * nchunks + ch];
-                    const float w = mc == -INFINITY ? 0.0f : expf(mc - M);
-                    lsum = fmaf(sll[at * nchunks + ch], w, lsum);
-                    sw[at * nchunks + ch] = w;
-                }
-                sl[at] = lsum;
+            if (a.trace && at == 0) *tslot(a, blockIdx.x, 230 + l, 9) = gtimer();
+            for (int qi = warp; qi < nm; qi += 8) {  // warp per query, lane = chunk (and chunk + 32)
+                const int c0 = lane, c1 = lane + 32;
+                const float m0 = c0 < nchunks ? sw[qi * nchunks + c0] : -INFINITY;
+                const float m1 = c1 < nchunks ? sw[qi * nchunks + c1] : -INFINITY;
+                float M = fmaxf(m0, m1);
+                for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+                const float w0 = m0 == -INFINITY ? 0.0f : expf(m0 - M);
+                const float w1 = m1 == -INFINITY ? 0.0f : expf(m1 - M);
+                // fixed butterfly over chunk lanes; chunks past the row's keys add exact zeros
+                float lsum = fmaf(c0 < nchunks ? sll[qi * nchunks + c0] : 0.0f, w0,
+                                  (c1 < nchunks ? sll[qi * nchunks + c1] : 0.0f) * w1);
+                for (int off = 16; off > 0; off >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, off);
+                __syncwarp();
+                if (c0 < nchunks) sw[qi * nchunks + c0] = w0;
+                if (c1 < nchunks) sw[qi * nchunks + c1] = w1;
+                if (lane == 0) sl[qi] = lsum;
             }
             named_sync(3, 256);
+            if (a.trace && at == 0) *tslot(a, blockIdx.x, 230 + l, 10) = gtimer();
             for (int t0 = at; t0 < nm * HD; t0 += 512) {  // two outputs per thread, all their loads in flight
                 float acc2[2] = {0.0f, 0.0f};
                 for (int ch0 = 0; ch0 < nchunks; ch0 += 32) {  // chunk order
-                    float t32[2][32];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int t = t0 + 256 * u, qi = min(t, nm * HD - 1) / HD, dd = t % HD;
-                        const float* src = p0 + static_cast<size_t>(qbase + qa + qi) * qstride + 2 + dd;
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            t32[u][j] = ch0 + j < nchunks ? __ldcg(src + static_cast<size_t>(ch0 + j) * 128 * qstride) : 0.0f;
-                    }
+                    if (t0 != at || ch0 != 0) load_batch(t0, ch0);
 #pragma unroll
                     for (int u = 0; u < 2; ++u) {
                         const int qi = min(t0 + 256 * u, nm * HD - 1) / HD;
@@ -915,8 +931,10 @@ __device__ __forceinline__ void attn_publish(const MegaArgs& a, int l, int kvh, 
                     put_split<kRows>(a.xim[P_O], f, r, val);
                 }
     }
+    if (a.trace && at == 0) *tslot(a, blockIdx.x, 230 + l, 11) = gtimer();
     fence_proxy_async_global();
     named_sync(3, 256);
+    if (a.trace && at == 0) *tslot(a, blockIdx.x, 230 + l, 12) = gtimer();
     if (at == 0) {  // these queries of this kv head are published
         __threadfence();
         if (qb > qa) atomicAdd(fptr(a, l, K_ATT, kvh), static_cast<unsigned>(qb - qa));
@@ -1100,7 +1118,7 @@ __device__ __noinline__ void attention_tile(const MegaArgs& a, int l, int kvh, i
         }
     }
     if (tr) *tslot(a, blockIdx.x, 230 + l, 5) = gtimer();
-    attn_publish<HD>(a, l, kvh, chunk, nchunks, qg, at, part, ring, mx, sm, o);
+    attn_publish<HD>(a, l, kvh, chunk, nchunks, qg, at, part, sTS, mx, sm, o);
 }
 
 // ── chunked attention, HD = 128: scores on the tensor cores ───────────────
@@ -1170,8 +1188,23 @@ __device__ __forceinline__ void attn_score_mma(uint32_t kp, uint32_t qp, uint32_
     ++sh_attph;
 }
 
+// wait for kv head kvh's QKV tiles of layer l: its q heads, K and V (all 256 attention threads)
+__device__ __forceinline__ void wait_head_qkv(const MegaArgs& a, int l, int kvh, int at) {
+    const int group = a.n_heads / a.n_kv;
+    const int q0 = kvh * group * a.hd / kM, q1 = ((kvh + 1) * group * a.hd - 1) / kM;
+    const int kt = (a.qd + kvh * a.hd) / kM, kt1 = (a.qd + kvh * a.hd + a.hd - 1) / kM;
+    const int vt = (a.qd + a.kvd + kvh * a.hd) / kM, vt1 = (a.qd + a.kvd + kvh * a.hd + a.hd - 1) / kM;
+    const int nq = q1 - q0 + 1, nk = kt1 - kt + 1, nv = vt1 - vt + 1;
+    if (at < nq + nk + nv) {
+        const int t = at < nq ? q0 + at : (at < nq + nk ? kt + at - nq : vt + at - nq - nk);
+        wait_ge(fptr(a, l, K_QKV, t), 1u);
+    }
+    named_sync(3, 256);
+}
+
 __device__ __noinline__ void attention_tile_tc(const MegaArgs& a, int l, int kvh, int chunk, int nchunks, int qg, int at,
-                                               float* part, int xoff, uint32_t tmem, uint64_t* attb) {
+                                               float* part, int xoff, uint32_t tmem, uint64_t* attb, uint64_t* retb,
+                                               bool last) {
     constexpr int HD = 128, KC = 128, C4 = 32, DPL = 4;
     uint8_t* ringb = reinterpret_cast<uint8_t*>(ring_base());
     uint8_t* sKp = ringb;                                        // 3 x [2 k-blocks][128 rows][128 B]
@@ -1196,7 +1229,10 @@ __device__ __noinline__ void attention_tile_tc(const MegaArgs& a, int l, int kvh
     const float* vbase = a.vbank[0] + hoff;
     const bool tr = a.trace && at == 0;
     if (tr) *tslot(a, blockIdx.x, 230 + l, 0) = gtimer();
-    // K rows, queries (and tail K rows) into registers, all loads in flight, then split
+    // K rows, queries (and tail K rows) into registers, all loads in flight, then
+    // split.  (Loading the cached K before this step's QKV tiles are done was
+    // measured slower: the loads compete with the QKV weight stream for HBM.)
+    wait_head_qkv(a, l, kvh, at);
     {
         float4 kx[16], qx[8], tx2[2];
 #pragma unroll
@@ -1204,6 +1240,11 @@ __device__ __noinline__ void attention_tile_tc(const MegaArgs& a, int l, int kvh
             const int f = at + 256 * i, r = f >> 5, c = f & 31;
             kx[i] = r < ns ? __ldcg(reinterpret_cast<const float4*>(kbase + static_cast<size_t>(k0 + r) * HD) + c)
                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int f = at + 256 * i;
+            put3x4(sKp, 32768, 16384, f >> 5, 4 * (f & 31), kx[i]);
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -1218,11 +1259,6 @@ __device__ __noinline__ void attention_tile_tc(const MegaArgs& a, int l, int kvh
             tx2[i] = ntail > 0 && r < a.rows
                          ? __ldcg(reinterpret_cast<const float4*>(kbase + static_cast<size_t>(prior + r) * HD) + c)
                          : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int f = at + 256 * i;
-            put3x4(sKp, 32768, 16384, f >> 5, 4 * (f & 31), kx[i]);
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {  // query qi: B rows qi (hi), 64 + qi (mid), 128 + qi (lo)
@@ -1373,7 +1409,12 @@ __device__ __noinline__ void attention_tile_tc(const MegaArgs& a, int l, int kvh
         }
     }
     if (tr) *tslot(a, blockIdx.x, 230 + l, 5) = gtimer();
-    attn_publish<HD>(a, l, kvh, chunk, nchunks, qg, at, part, reinterpret_cast<float*>(ringb), mx, sm, o);
+    if (last) {  // the ring is free: give it back now, the merge below only needs the small scratch
+        fence_proxy_async();
+        named_sync(3, 256);
+        if (at == 0) mbar_arrive(retb);
+    }
+    attn_publish<HD>(a, l, kvh, chunk, nchunks, qg, at, part, sTS, mx, sm, o);
 }
 
 __device__ __forceinline__ int attn_chunks(const MegaArgs& a) {
@@ -1385,10 +1426,14 @@ __device__ __forceinline__ int attention_items(const MegaArgs& a, int nchunks) {
     return a.n_kv * nchunks * nqg;
 }
 __device__ __forceinline__ void attention_dispatch(const MegaArgs& a, int l, int item, int nchunks, int at, float* part,
-                                                   int xoff, uint32_t tmem, uint64_t* attb) {
+                                                   int xoff, uint32_t tmem, uint64_t* attb, uint64_t* retb, bool last) {
     const int group = a.n_heads / a.n_kv;
     const int nqg = (a.rows * group + 63) / 64;
     const int kvh = item / (nchunks * nqg), rem = item % (nchunks * nqg), chunk = rem / nqg, qg = rem % nqg;
+    if (a.hd == 128) {  // the tensor-core path stages the cached K before it waits for this step's QKV
+        attention_tile_tc(a, l, kvh, chunk, nchunks, qg, at, part, xoff, tmem, attb, retb, last);
+        return;
+    }
     {  // wait for this kv head's QKV tiles: its q heads, K and V
         const int q0 = kvh * group * a.hd / kM, q1 = ((kvh + 1) * group * a.hd - 1) / kM;
         const int kt = (a.qd + kvh * a.hd) / kM, kt1 = (a.qd + kvh * a.hd + a.hd - 1) / kM;
@@ -1404,7 +1449,7 @@ __device__ __forceinline__ void attention_dispatch(const MegaArgs& a, int l, int
         case 32: attention_tile<32>(a, l, kvh, chunk, nchunks, qg, at, part, xoff); break;
         case 64: attention_tile<64>(a, l, kvh, chunk, nchunks, qg, at, part, xoff); break;
         case 160: attention_tile<160>(a, l, kvh, chunk, nchunks, qg, at, part, xoff); break;
-        default: attention_tile_tc(a, l, kvh, chunk, nchunks, qg, at, part, xoff, tmem, attb); break;
+        default: attention_tile<128>(a, l, kvh, chunk, nchunks, qg, at, part, xoff); break;
     }
 }
 // the chunked design's attention phase of layer l for the attention threads
@@ -1414,11 +1459,18 @@ __device__ __forceinline__ void attention_phase_lent(const MegaArgs& a, int l, i
     if (at == 0) mwait(lentb, static_cast<uint32_t>(l & 1));
     named_sync(3, 256);
     const int nchunks = attn_chunks(a);
-    for (int it = blockIdx.x; it < attention_items(a, nchunks); it += gridDim.x)
-        attention_dispatch(a, l, it, nchunks, at, a.apart, xoff, tmem, attb);
-    fence_proxy_async();  // generic-proxy ring accesses before the producer's bulk copies
-    named_sync(3, 256);
-    if (at == 0) mbar_arrive(retb);
+    const int items = attention_items(a, nchunks);
+    bool returned = false;  // the tensor-core path returns the ring after its last item's PV
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const bool last = it + static_cast<int>(gridDim.x) >= items;
+        attention_dispatch(a, l, it, nchunks, at, a.apart, xoff, tmem, attb, retb, last);
+        returned = returned || (last && a.hd == 128);
+    }
+    if (!returned) {
+        fence_proxy_async();  // generic-proxy ring accesses before the producer's bulk copies
+        named_sync(3, 256);
+        if (at == 0) mbar_arrive(retb);
+    }
 }
 
 // A CTA's walk over its weight units: (layer, phase, unit) in stream order.

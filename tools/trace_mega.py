@@ -170,5 +170,10 @@ for l in range(1, NL - 1):
     has6 = T[:, 6] > 0
     if has6.any():
         parts += f", publish {md(T[has6, 6] - T[has6, 5])}, arrive-wait {md(T[has6, 7] - T[has6, 6])}, merge {md(T[has6, 8] - T[has6, 7])}"
+        h9 = has6 & (T[:, 9] > 0)
+        if h9.any():
+            parts += (f" [merge: stage {md(T[h9, 9] - T[h9, 7])}, weights {md(T[h9, 10] - T[h9, 9])},"
+                      f" o + stores {md(T[h9, 11] - T[h9, 10])}, proxy fence {md(T[h9, 12] - T[h9, 11])},"
+                      f" gpu fence + flag {md(T[h9, 8] - T[h9, 12])}]")
     print(f"L{l} chunked attention ({m.sum()} CTAs): first start {rel(T[:, 0]).min():.1f} last publish "
           f"{rel(T[:, 8]).max():.1f}; {parts}")
