@@ -124,9 +124,12 @@ class Engine:
         return CacheBank(self, layer_begin, layer_end)
 
     # forward_layers (tinyformer.hpp:174-176)
-    def forward_layers(self, layer_begin, layer_end, hidden, positions, bank, mask=None) -> np.ndarray:
+    def forward_layers(self, layer_begin, layer_end, hidden, positions, bank, mask=None, out=None) -> np.ndarray:
         h = _f32(hidden)
-        out = np.empty_like(h)
+        if out is None:
+            out = np.empty_like(h)
+        elif out.shape != h.shape or out.dtype != np.float32 or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float32 array shaped like hidden")
         m = None if mask is None else _f32(mask)
         check(_lib.lib().sfg_forward_layers(self.h, bank.h, layer_begin, layer_end, h.shape[0], _p(h, _f32p),
                                             _p(_i32(positions), _i32p), _p(m, _f32p), _p(out, _f32p)))
