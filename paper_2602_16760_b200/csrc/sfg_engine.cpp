@@ -406,7 +406,8 @@ Engine::Engine(const ModelCfg& cfg, const sfg_engine_options& opt, const float* 
 void Engine::tp_setup_peer() {
     const ModelCfg& c = cfg_;
     const size_t tilesH = (c.hidden_dim + 127) / 128;
-    tp_peer_.data_floats = static_cast<size_t>(c.n_layers) * 2 * tilesH * 16 * 128;
+    // one 64-bit word {epoch, f32} per exchanged value (sfg_mega.cu epi_final)
+    tp_peer_.data_floats = static_cast<size_t>(c.n_layers) * 2 * tilesH * 16 * 128 * 2;
     const size_t nflags = static_cast<size_t>(c.n_layers) * 2 * tilesH;
     const size_t bytes = tp_peer_.data_floats * sizeof(float) + nflags * sizeof(unsigned) + 256;
     SFG_CUDA(cudaMalloc(&tp_peer_.base, bytes));

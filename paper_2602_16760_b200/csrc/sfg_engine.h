@@ -219,7 +219,7 @@ void tp_allgather_bytes(void* comm, const void* src, void* dst, size_t n, cudaSt
 // over NVLink (CUDA IPC mapping), so the O / down all-reduce happens inside
 // the producing tile's epilogue instead of as a separate collective.
 struct TpPeer {
-    float* inbox = nullptr;          // mine: [layers][2][tilesH][16][128] partial tiles
+    float* inbox = nullptr;          // mine: [layers][2][tilesH][16][128] partial tiles, 64-bit {epoch, f32} words
     unsigned* inflag = nullptr;      // mine: [layers][2][tilesH] epoch flags
     float* peer_inbox = nullptr;     // the peer's, mapped
     unsigned* peer_inflag = nullptr;

@@ -443,6 +443,14 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ float ld_relaxed_sys(const float* p) {
     float v;
     asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
@@ -524,30 +532,52 @@ __device__ void epi_final(const MegaArgs& a, const LayerDesc& L, int l, int p, i
         const int f = tile * kM + m;
         if (a.tp > 1) {
             // row-parallel output: swap partial tiles with the peer over NVLink
-            // and sum them in rank order (bitwise identical on both GPUs)
+            // and sum them in rank order (bitwise identical on both GPUs).  Every
+            // value travels as ONE 64-bit word {launch epoch, f32 bits}: the
+            // receiver polls its own words until they carry this launch's epoch,
+            // so no system-scope fence or flag is needed (a __threadfence_system
+            // per tile cost 7-10 us: tools/trace_mega_tp.py)
             const int tilesH = (a.H + kM - 1) / kM;
             const size_t slot = (static_cast<size_t>(l) * 2 + (p == P_O ? 0 : 1)) * tilesH + tile;
-            float* dst = a.peer_inbox + slot * kRows * kM;
+            const int xid = (p == P_O ? 240 : 248) + (l & 7);  // trace ids of the exchange
+            if (a.trace && et == 0) *tslot(a, blockIdx.x, xid, 0) = gtimer();
+            unsigned long long* dst = reinterpret_cast<unsigned long long*>(a.peer_inbox) + slot * kRows * kM;
+            const unsigned long long tag = static_cast<unsigned long long>(sh_epoch) << 32;
 #pragma unroll
             for (int r = 0; r < kRows; ++r)  // static bound: y[] stays in registers
-                if (r < a.rows) dst[r * kM + m] = y[r];
-            __threadfence_system();
-            named_sync(1, 128);
-            if (et == 0) {
-                st_release_sys(a.peer_inflag + slot, sh_epoch);
-                unsigned long long spins = 0;
-                while (ld_acquire_sys(a.inflag + slot) < sh_epoch) {
-                    __nanosleep(32);
-                    if (++spins > (1ull << 27)) asm volatile("trap;");  // peer gone: fail, do not hang
-                }
-            }
-            named_sync(1, 128);
-            const float* src = a.inbox + slot * kRows * kM;
+                if (r < a.rows) st_relaxed_sys_u64(dst + r * kM + m, tag | __float_as_uint(y[r]));
+            if (a.trace && et == 0) *tslot(a, blockIdx.x, xid, 1) = gtimer();
+            const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a.inbox) + slot * kRows * kM;
+            float other[kRows];
+            unsigned pending = 0;
 #pragma unroll
             for (int r = 0; r < kRows; ++r) {
-                const float other = r < a.rows ? ld_relaxed_sys(src + r * kM + m) : 0.0f;
-                y[r] = a.tp_rank == 0 ? y[r] + other : other + y[r];
+                other[r] = 0.0f;
+                if (r < a.rows) {
+                    const unsigned long long v = ld_relaxed_sys_u64(src + r * kM + m);
+                    if ((v >> 32) == sh_epoch) other[r] = __uint_as_float(static_cast<unsigned>(v));
+                    else pending |= 1u << r;
+                }
             }
+            unsigned long long spins = 0;
+            while (pending) {
+                __nanosleep(32);
+                if (++spins > (1ull << 27)) asm volatile("trap;");  // peer gone: fail, do not hang
+#pragma unroll
+                for (int r = 0; r < kRows; ++r)
+                    if ((pending >> r) & 1u) {
+                        const unsigned long long v = ld_relaxed_sys_u64(src + r * kM + m);
+                        if ((v >> 32) == sh_epoch) {
+                            other[r] = __uint_as_float(static_cast<unsigned>(v));
+                            pending &= ~(1u << r);
+                        }
+                    }
+            }
+            if (a.trace && et == 0) *tslot(a, blockIdx.x, xid, 3) = gtimer();
+#pragma unroll
+            for (int r = 0; r < kRows; ++r)
+                if (r < a.rows) y[r] = a.tp_rank == 0 ? y[r] + other[r] : other[r] + y[r];
+            if (a.trace && et == 0) *tslot(a, blockIdx.x, xid, 4) = gtimer();
         }
         // the next GEMM's input image: split(h * gain) of ffn_norm (after O)
         // or of the next layer's attn_norm (after down; none after the last)
