@@ -5,7 +5,7 @@
 #   tools/sass_histogram.sh > profiles/r02_sass_histogram.txt
 set -e
 cd "$(dirname "$0")/.."
-for obj in build/sfg/sfg_mega.o build/sfg/sfg_fast.o build/sfg/sfg_attn.o build/sfg/sfg_common.o; do
+for obj in build/sfg/sfg_mega.o build/sfg/sfg_fast.o build/sfg/sfg_attn.o build/sfg/sfg_attn_tc.o build/sfg/sfg_common.o; do
   echo "=== $obj"
   cuobjdump -sass "$obj" | awk '
     /Function :/ { fn = $3 }
