@@ -207,10 +207,11 @@ def ncu_traffic(args):
     import csv
     import glob
     # long contexts (>= 1024 cached keys) have their own capture (KV streaming in the launch)
-    long_ctx = args.prompt_len >= 1024
+    plen = getattr(args, "prompt_len", PROMPT_LEN)
+    long_ctx = plen >= 1024
     caps = sorted(c for c in glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_mega_summary.csv"))
                   if ("_ctx2k_" in os.path.basename(c)) == long_ctx)
-    if long_ctx and (not caps or args.prompt_len != 2048):
+    if long_ctx and (not caps or plen != 2048):
         return {"traffic": None}
     path = caps[-1] if caps else os.path.join(ROOT, "profiles", "r01_ncu_full_mega_summary.csv")
     try:
@@ -225,7 +226,7 @@ def ncu_traffic(args):
         H, qd, kvd, F = m["hidden_dim"], m["n_heads"] * m["head_dim"], m["n_kv_heads"] * m["head_dim"], m["ffn_dim"]
         layer = 2 * (H * (qd + 2 * kvd) + qd * H + 3 * H * F)
         if long_ctx:  # + the K/V cache read of ~prompt_len keys and the 16 rows' K/V writes, per layer
-            layer += 2 * kvd * 4 * (args.prompt_len + 16)
+            layer += 2 * kvd * 4 * (plen + 16)
         return {"traffic": rd + wr, "traffic_launch": f"one 28-layer server launch (ncu --set full, {os.path.basename(path)})",
                 "traffic_launch_algorithmic_bytes": 28 * layer}
     except Exception:
