@@ -161,6 +161,26 @@ static void grow(void** p, size_t bytes) {
 
 void Engine::ensure_ws(Workspace& ws, int rows, int runs, int logit_rows) {
     const ModelCfg& c = cfg_;
+    // A prompt pass grows the row-scaled buffers to the prompt length (~0.7 GB
+    // for a 2048-token prompt at the 7B shape); the first decode step after it
+    // gives them back, so 64 concurrent long-context sessions fit one GPU.
+    const bool trim = rows <= 64 && ws.cap_rows > 256;
+    if (trim) {
+        SFG_CUDA(cudaDeviceSynchronize());
+        for (void** p : {(void**)&ws.h, (void**)&ws.xn, (void**)&ws.q, (void**)&ws.att, (void**)&ws.act, (void**)&ws.pos,
+                         (void**)&ws.ids, (void**)&ws.argmax, (void**)&ws.keep, (void**)&ws.row_off, &ws.wire, &ws.fast,
+                         &ws.pimg, &ws.apieces}) {
+            if (*p) cudaFree(*p);
+            *p = nullptr;
+        }
+        ws.fast_bytes = ws.pimg_bytes = ws.apieces_bytes = 0;
+        if (ws.wire_pin) cudaFreeHost(ws.wire_pin);
+        ws.wire_pin = nullptr;
+        if (ws.pinned) cudaFreeHost(ws.pinned);
+        ws.pinned = nullptr;
+        ws.pinned_bytes = 0;
+        ws.cap_rows = 0;
+    }
     const bool growing = rows > ws.cap_rows || runs > ws.cap_runs || logit_rows > ws.cap_logit_rows;
     if (!growing) return;
     // old buffers may still be read by queued work; new ones are zero-filled

@@ -832,7 +832,7 @@ __device__ __forceinline__ void attn_publish(const MegaArgs& a, int l, int kvh, 
     const int q0 = warp * 8;
     const bool wq = q0 < nq;
     // publish: one chunk -> final values; several -> partials, the last chunk merges
-    const int cpk = (a.max_len + kAttnMinKC - 1) / kAttnMinKC;  // chunk slots per kv head
+    const int cpk = (a.max_len + attn_kc<HD>() - 1) / attn_kc<HD>();  // chunk slots per kv head
     constexpr size_t qstride = HD + 2;
     int qa = 0, qb = nq;  // item queries this CTA finishes
     if (nchunks > 1) {
@@ -2197,6 +2197,40 @@ int mega_batch_rows(const Engine& e) {
     return sm <= dyn_smem_budget(true) ? kMaxRows : tc::kRows;
 }
 
+// per-phase CTA split (phase_ctas) and whole tiles (whole_tiles) of a launch,
+// shared by the launch and by MegaState's partial-buffer sizing
+static int mega_align_pct() {
+    static const int v = [] {
+        const char* e = getenv("SFG_MEGA_ALIGN");
+        return e ? atoi(e) : 85;
+    }();
+    return v;
+}
+static bool mega_whole_on() {
+    static const int v = [] {
+        const char* e = getenv("SFG_MEGA_WHOLE");  // dev knob: 0 = plain stream-K everywhere
+        return e ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+static void mega_split(const Dims& dl, int nsm, int (&G)[4], int (&W)[4], int (&tiles)[4]) {
+    const int tQ = (dl.qd + 2 * dl.kvd + tc::kM - 1) / tc::kM, tH = (dl.H + tc::kM - 1) / tc::kM;
+    const int t_of[4] = {tQ, tH, dl.F / 64, tH};
+    const int kb_of[4] = {dl.H / tc::kKB, dl.qd / tc::kKB, dl.H / tc::kKB, dl.F / tc::kKB};
+    for (int p = 0; p < 4; ++p) {
+        tiles[p] = t_of[p];
+        G[p] = phase_ctas(t_of[p], kb_of[p], nsm, mega_align_pct());
+        W[p] = mega_whole_on() ? whole_tiles(t_of[p], kb_of[p], G[p]) : 0;
+    }
+}
+static int mega_split_tiles_max(const Engine& e) {
+    int G[4], W[4], t[4];
+    mega_split(e.dims(), device_sm_count(), G, W, t);
+    int m = 0;
+    for (int p = 0; p < 4; ++p) m = std::max(m, t[p] - W[p] * G[p]);
+    return m;
+}
+
 namespace {
 struct MegaState {
     LayerDesc* d_layers = nullptr;
@@ -2290,8 +2324,9 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         const int tilesH = (c.hidden_dim + tc::kM - 1) / tc::kM;
         {
             const int tQ = (c.q_dim() + 2 * c.kv_dim() + tc::kM - 1) / tc::kM, tG = c.ffn_dim / 64;
-            const int tiles_max = std::max(std::max(tQ, tG), tilesH);
-            st.cnt_stride = tiles_max;
+            // stream-K partial slots only for the tiles a phase actually splits
+            // (its whole tiles never store partials): 76 instead of 224 at 7B
+            st.cnt_stride = std::max(1, mega_split_tiles_max(e));
             SFG_CUDA(cudaMalloc(&st.counters, sizeof(int) * 2 * st.cnt_stride));
             SFG_CUDA(cudaMemset(st.counters, 0, sizeof(int) * 2 * st.cnt_stride));
             // must match fptr(): stats tiles + counter, then per layer
@@ -2299,7 +2334,9 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
             const int lay = (tQ + 1) + (3 * c.n_kv_heads + 1) + (tilesH + 1) + (tG + 1) + (tilesH + 1);
             st.nflags = tilesH + 1 + (le - lb) * lay;
             SFG_CUDA(cudaMalloc(&st.flags, sizeof(unsigned) * st.nflags));
-            const size_t cpk = (c.max_seq_len + kAttnMinKC - 1) / kAttnMinKC;
+            // chunked attention partials (per kv head, chunk, query): only that design uses them
+            const int kc = c.head_dim <= 128 ? attn_kc<128>() : attn_kc<160>();
+            const size_t cpk = rows_attention() ? 1 : (c.max_seq_len + kc - 1) / kc;
             SFG_CUDA(cudaMalloc(&st.apart, sizeof(float) * c.n_kv_heads * cpk * 128 * (c.head_dim + 2)));
             SFG_CUDA(cudaMalloc(&st.acnt, sizeof(unsigned) * c.n_kv_heads * 16));
             SFG_CUDA(cudaMemset(st.acnt, 0, sizeof(unsigned) * c.n_kv_heads * 16));
@@ -2470,22 +2507,9 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
             return v ? atoi(v) : 0;
         }();
         a.noload = noload_env;
-        static const int al_env = [] {
-            const char* v = getenv("SFG_MEGA_ALIGN");
-            return v ? atoi(v) : 85;
-        }();
-        const int tQ = (dl.qd + 2 * dl.kvd + tc::kM - 1) / tc::kM, tH = (dl.H + tc::kM - 1) / tc::kM;
-        a.G[P_QKV] = phase_ctas(tQ, dl.H / tc::kKB, nsm, al_env);
-        a.G[P_O] = phase_ctas(tH, dl.qd / tc::kKB, nsm, al_env);
-        a.G[P_GU] = phase_ctas(dl.F / 64, dl.H / tc::kKB, nsm, al_env);
-        a.G[P_DOWN] = phase_ctas(tH, dl.F / tc::kKB, nsm, al_env);
-        static const int whole_env = [] {
-            const char* v = getenv("SFG_MEGA_WHOLE");  // dev knob: 0 = plain stream-K everywhere
-            return v ? atoi(v) : 1;
-        }();
-        const int tiles_of[4] = {tQ, tH, dl.F / 64, tH};
-        const int kb_of[4] = {dl.H / tc::kKB, dl.qd / tc::kKB, dl.H / tc::kKB, dl.F / tc::kKB};
-        for (int p = 0; p < 4; ++p) a.W[p] = whole_env ? whole_tiles(tiles_of[p], kb_of[p], a.G[p]) : 0;
+        int tiles_of[4];
+        mega_split(dl, nsm, a.G, a.W, tiles_of);
+        const int tQ = tiles_of[P_QKV], tH = tiles_of[P_O];
         // flag layout (must match kind_tiles): statistics tiles + counter, then
         // per layer QKV, attention kv heads, O, gate|up, down tiles + counter each
         // (K_ATT: per kv head published-query counts, then 2 chunk-arrival counters per head)

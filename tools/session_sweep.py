@@ -7,11 +7,13 @@ Batcher: per-GPU queue feeding handle_batch), one client thread per session
     python tools/session_sweep.py [--sessions 1,4,16,64] [--ctx 24] [--tokens 24]
 
 Each session's local side (2+2 layers, LM head) runs on the engine of the
-GPU its index maps to; frames cross host memory.  Prints one JSON line per
-point: aggregate committed tok/s over the decode phase, per-session step
-time, batching statistics.
+GPU its index maps to; frames cross host memory.  Every session prefills its
+prompt first; then all sessions decode together (a barrier), and the point
+reports aggregate committed tok/s over that decode phase, the per-session step
+time, the mean prefill time and batching statistics.
 """
 import argparse
+import ctypes as C
 import json
 import os
 import sys
@@ -58,15 +60,44 @@ def main():
         bq = sfg.Batcher(router)
         prompts = [np.random.default_rng(1000 + i).integers(0, cfg.vocab_size, args.ctx).tolist() for i in range(k)]
         res, errs = [None] * k, []
+        # every session prefills first (its prompt frame), then all decode
+        # together: aggregate tok/s is the DECODE phase with k sessions live
+        gate = threading.Barrier(k)
+        L = sfg.lib()
+        la_c = sfg._lib.DecodeConfig(2, 5, 3, 5, 1 << 20)
 
         def client(i):
+            d = None
             try:
                 cl = sfg.SplitClient(engines[i % ndev], sfg.SplitConfig(split, split, sfg.F16), bq.handler,
                                      session_id=f"sweep-{k}-{i}")
-                d = sfg.decode_lookahead(cl, prompts[i], args.tokens, la)
-                res[i] = (d.wall_seconds, d.tokens_committed, d.steps)
+                pool = sfg.NGramPool(3, 1 << 20)
+                p = np.asarray(prompts[i], dtype=np.int32)
+                d = C.c_void_p()
+                tp = time.time()
+                sfg._lib.check(L.sfg_decoder_create(cl.h, C.byref(la_c), pool.h, p.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                    len(p), args.tokens + 64, C.byref(d)))
+                prefill = time.time() - tp
+                committed = np.zeros(16, dtype=np.int32)
+                n, b = C.c_int32(), C.c_int32()
+                gate.wait()
+                t0 = time.time()
+                toks, steps = 0, 0
+                while toks < args.tokens:
+                    sfg._lib.check(L.sfg_decoder_step(d, committed.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(n),
+                                                      C.byref(b)))
+                    toks += n.value
+                    steps += 1
+                res[i] = (time.time() - t0, toks, steps, prefill)
             except Exception as e:
                 errs.append(repr(e))
+                try:
+                    gate.abort()
+                except Exception:
+                    pass
+            finally:
+                if d is not None and d.value:
+                    L.sfg_decoder_destroy(d)
 
         ts = [threading.Thread(target=client, args=(i,)) for i in range(k)]
         tw = time.time()
@@ -75,16 +106,18 @@ def main():
         for t in ts:
             t.join()
         if errs:
-            print(json.dumps({"sessions": k, "error": errs[0]}), flush=True)
+            print(json.dumps({"sessions": k, "gpus": ndev, "context": args.ctx, "error": errs[0]}), flush=True)
             continue
         dec = max(r[0] for r in res)
         toks = sum(r[1] for r in res)
         st = bq.stats()
         print(json.dumps({"sessions": k, "gpus": ndev, "context": args.ctx,
                           "aggregate_tok_s": toks / dec, "per_session_step_ms": dec / (sum(r[2] for r in res) / k) * 1e3,
+                          "prefill_s_mean": round(float(np.mean([r[3] for r in res])), 3),
                           "placement": router.load(), "frames_per_server_batch": st["frames"] / max(1, st["batches"]),
                           "max_server_batch": st["max_batch"],
                           "shared_weight_passes": [s.shared_passes() for s in servers],
+                          "attention": os.environ.get("SFG_ATTN", "rows"),
                           "wall_s": round(time.time() - tw, 1)}), flush=True)
         del bq, router, servers
 
