@@ -241,7 +241,8 @@ def config_dict(args, ws):
                         "W=5 N=3 G=5, forced B=16 (seeded n-gram pool)",
             "model_shape": SHAPE_TEXT[args.model], "rows_per_step": 16,
             "prompt_len": PROMPT_LEN, "rtt_ms": args.rtt_ms, "math": args.math, "wire": "f16",
-            "attention": os.environ.get("SFG_ATTN", "rows"),
+            "attention": os.environ.get("SFG_ATTN") or
+                         ("chunked (auto: >= 768 cached keys)" if PROMPT_LEN >= 768 else "rows (auto: < 768 cached keys)"),
             "sessions_per_gpu": 1 if args.tp == 1 else 1.0 / args.tp,
             "parallelism": f"replicas x{ws} (independent sessions)" if args.tp == 1 else
                            f"tp{args.tp} (one session, NCCL all-reduce of O/down over NVLink)",
@@ -625,10 +626,10 @@ def main():
     args = ap.parse_args()
     MODEL = MODELS[args.model]
     PROMPT_LEN = args.prompt_len
-    # attention kernel of the layer-stack: per-(row, kv head) items for short
-    # contexts, key-chunked items sharing K/V across rows for long ones (both
-    # batch invariant; fixed for the whole run)
-    os.environ.setdefault("SFG_ATTN", "chunked" if PROMPT_LEN >= 1024 else "rows")
+    # attention kernel of the layer-stack: the megakernel picks it per session
+    # from the cache length -- per-(row, kv head) items below 768 cached keys,
+    # key-chunked items sharing K/V across rows above (both batch invariant,
+    # fixed for a session's lifetime); SFG_ATTN=rows|chunked overrides it
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     ws, rank, local = dist_setup()
     if args.impl == "reference":

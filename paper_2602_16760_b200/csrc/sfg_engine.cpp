@@ -657,8 +657,9 @@ int Engine::forward_device(Bank& b, int lb, int le, int rows, Workspace& ws, cud
     const int prior = b.len();
     int n = 0;
     if (lb >= le) return 0;
+    // (the attention design is decided only for megakernel-sized steps, never at a prompt pass)
     if (fast() && (tp_size_ == 1 || tp_peer_.peer_inbox) && mega_env_enabled() && le - lb <= 50 &&
-        mega_supported(*this, rows, ws.additive_mask)) {
+        rows <= 16 && !ws.additive_mask && mega_supported(*this, rows, false, bank_rows_attention(b))) {
         for (int layer = lb; layer < le; ++layer)
             if (!layers_[layer].hosted) throw Error(Kind::internal, "layer not hosted by this engine");
         return mega_forward(*this, b, lb, le, rows, ws, s);

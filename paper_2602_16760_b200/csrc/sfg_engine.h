@@ -167,6 +167,9 @@ public:
     Engine& engine() { return eng_; }
     // per-bank state of the FAST megakernel (layer table, grid barrier)
     std::shared_ptr<void> mega;
+    // megakernel attention design: -1 undecided, 1 per-row, 0 key-chunked
+    // (bank_rows_attention: chosen at the first megakernel step, then fixed)
+    int attn_design = -1;
     // process-unique id (never reused, unlike the object's address): keys
     // the client's captured graphs that bake in this bank's device buffers
     uint64_t id() const { return id_; }
@@ -346,7 +349,7 @@ void* fast_build_head(Engine& e, const void* lm_head, cudaStream_t s);
 float* fast_partials(const ModelCfg& c, Workspace& ws);
 int* fast_counters(const ModelCfg& c, Workspace& ws);
 // FAST layer-stack megakernel (sfg_mega.cu)
-bool mega_supported(const Engine& e, int rows, bool additive_mask);
+bool mega_supported(const Engine& e, int rows, bool additive_mask, bool rows_attention);
 // rows of one cross-session layer-stack pass (32, or 16 where unsupported)
 int mega_batch_rows(const Engine& e);
 // banks/rowinfo (optional): rows of several sessions in one pass -- row r
@@ -354,7 +357,8 @@ int mega_batch_rows(const Engine& e);
 // rowinfo[3r+2] cached keys; b supplies the launch state (same layer range)
 int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cudaStream_t s,
                  const std::vector<Bank*>* banks = nullptr, const int32_t* rowinfo = nullptr);
-bool rows_attention();
+// the bank's attention design (decided at its first megakernel step, see sfg_mega.cu)
+bool bank_rows_attention(Bank& b);
 float* mega_ss(Bank& b, int which, int tilesH);
 bool& mega_trace_enabled();
 int mega_trace_read(Bank& b, unsigned long long* out, size_t n);

@@ -2147,12 +2147,28 @@ size_t smem_bytes(bool rows_attn, int stages, int hd, int group, int max_len, in
 
 }  // namespace mega
 
-bool rows_attention() {
+// Attention design of the layer-stack megakernel, per bank (session): decided
+// at the bank's first megakernel step from its cache length -- the per-row
+// design below kAutoChunkedKeys cached keys, the key-chunked design at or
+// above (measured crossover ~700 keys) -- and fixed for the bank's
+// lifetime, so every step of a session (lookahead or sequential) runs the same
+// arithmetic.  SFG_ATTN=rows|chunked overrides the choice for every bank.
+constexpr int kAutoChunkedKeys = 768;
+int attn_env() {
     static const int v = [] {
-        const char* e = getenv("SFG_ATTN");  // "chunked": key-chunked attention for long contexts
-        return e && std::string(e) == "chunked" ? 0 : 1;
+        const char* e = getenv("SFG_ATTN");
+        if (e && std::string(e) == "chunked") return 0;
+        if (e && std::string(e) == "rows") return 1;
+        return -1;
     }();
-    return v != 0;
+    return v;
+}
+bool bank_rows_attention(Bank& b) {
+    if (b.attn_design < 0) {
+        const int env = attn_env();
+        b.attn_design = env >= 0 ? env : (b.len() < kAutoChunkedKeys ? 1 : 0);
+    }
+    return b.attn_design == 1;
 }
 
 using namespace mega;
@@ -2167,14 +2183,13 @@ int mega_stages(bool ra, int hd, int group, int max_len, int RS, int cap) {
     return stages;
 }
 
-bool mega_supported(const Engine& e, int rows, bool additive_mask) {
+bool mega_supported(const Engine& e, int rows, bool additive_mask, bool ra) {
     if (rows < 1 || rows > tc::kRows || additive_mask) return false;
     const ModelCfg& c = e.cfg();
     const int group = c.n_heads / c.n_kv_heads;
     if (group > kMaxGroup || !(c.head_dim == 32 || c.head_dim == 64 || c.head_dim == 128 || c.head_dim == 160)) return false;
     if (group > 4 && c.head_dim > 64) return false;  // register budget of the attention phase
     if (c.hidden_dim % tc::kKB || c.q_dim() % tc::kKB || c.ffn_dim % tc::kKB) return false;
-    const bool ra = rows_attention();
     const size_t sm = smem_bytes(ra, 4, c.head_dim, c.n_heads / c.n_kv_heads, c.max_seq_len);
     if (sm > dyn_smem_budget(ra)) return false;
     if (!ra) {  // the chunked design stages a whole key chunk in the lent ring; at most 64 chunks merge
@@ -2191,7 +2206,7 @@ bool mega_supported(const Engine& e, int rows, bool additive_mask) {
 // N = 96) with the per-row attention design when its shared memory fits,
 // else 16.
 int mega_batch_rows(const Engine& e) {
-    if (!mega_supported(e, 1, false) || !rows_attention() || e.tp_size() > 1) return tc::kRows;
+    if (!mega_supported(e, 1, false, true) || e.tp_size() > 1) return tc::kRows;  // wide passes: per-row design
     const ModelCfg& c = e.cfg();
     const size_t sm = smem_bytes(true, 4, c.head_dim, c.n_heads / c.n_kv_heads, c.max_seq_len, kMaxRows);
     return sm <= dyn_smem_budget(true) ? kMaxRows : tc::kRows;
@@ -2336,7 +2351,7 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
             SFG_CUDA(cudaMalloc(&st.flags, sizeof(unsigned) * st.nflags));
             // chunked attention partials (per kv head, chunk, query): only that design uses them
             const int kc = c.head_dim <= 128 ? attn_kc<128>() : attn_kc<160>();
-            const size_t cpk = rows_attention() ? 1 : (c.max_seq_len + kc - 1) / kc;
+            const size_t cpk = bank_rows_attention(b) ? 1 : (c.max_seq_len + kc - 1) / kc;
             SFG_CUDA(cudaMalloc(&st.apart, sizeof(float) * c.n_kv_heads * cpk * 128 * (c.head_dim + 2)));
             SFG_CUDA(cudaMalloc(&st.acnt, sizeof(unsigned) * c.n_kv_heads * 16));
             SFG_CUDA(cudaMemset(st.acnt, 0, sizeof(unsigned) * c.n_kv_heads * 16));
@@ -2349,7 +2364,8 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     // row capacity of this launch: one 16-row block, or two for a
     // cross-session pass of more than 16 rows
     const int R = rows > tc::kRows ? kMaxRows : tc::kRows;
-    if (R > tc::kRows && (!rows_attention() || e.tp_size() > 1 || rows > kMaxRows))
+    const bool ra = bank_rows_attention(b);
+    if (R > tc::kRows && (!ra || e.tp_size() > 1 || rows > kMaxRows))
         throw Error(Kind::internal, "a wide (> 16-row) pass needs <= 32 rows, the per-row attention and no tensor parallelism");
     if (stp->rcap < R) {  // (re)size the row-strided buffers
         SFG_CUDA(cudaDeviceSynchronize());
@@ -2374,7 +2390,6 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         return v ? std::min(std::max(atoi(v), 2), kMaxStages) : kMaxStages;
     }();
     const int RS = stp->rcap;      // the buffers' row stride (>= R)
-    const bool ra = rows_attention();
     const void* kfn = !ra ? reinterpret_cast<const void*>(mega_kernel<false, kRows>)
                       : RS == kRows ? reinterpret_cast<const void*>(mega_kernel<true, kRows>)
                                     : reinterpret_cast<const void*>(mega_kernel<true, kMaxRows>);
@@ -2439,6 +2454,9 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
     if (banks && rowinfo) {  // cross-session pass
         if (banks->size() > static_cast<size_t>(kMaxBanks) || !ra)
             throw Error(Kind::internal, "cross-session pass needs <= 16 banks and the per-row attention");
+        for (Bank* bi : *banks)
+            if (!bank_rows_attention(*bi))
+                throw Error(Kind::internal, "cross-session pass over a bank with the key-chunked attention");
         for (size_t i = 0; i < banks->size(); ++i) {
             Bank* bi = (*banks)[i];
             if (bi->layer_begin() != b.layer_begin() || bi->layer_end() != b.layer_end() ||

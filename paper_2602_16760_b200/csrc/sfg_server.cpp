@@ -401,8 +401,8 @@ void Server::handle_batch(int n, const uint8_t* const* reqs, const size_t* lens,
     resps.assign(static_cast<size_t>(n), {});
     // the shared pass is the layer-stack megakernel; one-by-one steps take it
     // too for these shapes, so responses stay bitwise those of handle()
-    const bool batchable = eng_.fast() && eng_.tp_size() == 1 && rows_attention() && mega_mode() == 1 &&
-                           mega_supported(eng_, 1, false) && cfg_.layer_end - cfg_.layer_begin <= 50;
+    const bool batchable = eng_.fast() && eng_.tp_size() == 1 && mega_mode() == 1 &&
+                           mega_supported(eng_, 1, false, true) && cfg_.layer_end - cfg_.layer_begin <= 50;
     // rows one shared weight pass carries: two sessions' 16-row lookahead
     // batches (32) when the layer stack supports it
     const int pass_rows = batchable ? mega_batch_rows(eng_) : tc_rows();
@@ -433,7 +433,8 @@ void Server::handle_batch(int n, const uint8_t* const* reqs, const size_t* lens,
             auto sess = find_session(f.h.session_id);
             bool dup = false;
             for (StepState* st : group) dup = dup || st->sess == sess;
-            shared = sess && !dup;
+            // only per-row-attention sessions share a weight pass
+            shared = sess && !dup && bank_rows_attention(*sess->bank);
         }
         if (!shared) {
             flush();

@@ -101,8 +101,24 @@ def _run_long_context(port):
 
 
 def test_long_context_rows_attention(port):
-    if os.environ.get("SFG_ATTN", "rows") != "rows":
+    # at 2048 cached keys the automatic choice is the chunked design: the
+    # per-row design is forced in a child process (the choice is read once)
+    if os.environ.get("SFG_ATTN") == "rows":
+        print("rel errors (prefill, step, step after resolve):", _run_long_context(port))
+        return
+    if os.environ.get("SFG_ATTN") == "chunked":
         pytest.skip("this process runs the chunked design")
+    env = dict(os.environ, SFG_ATTN="rows")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu",
+                        os.path.join(ROOT, "tests", "test_gpu_long_context.py") + "::test_long_context_rows_attention"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_long_context_auto_attention(port):
+    """No SFG_ATTN: the session picks the key-chunked design at 2048 cached keys."""
+    if os.environ.get("SFG_ATTN"):
+        pytest.skip("a design is forced in this process")
     print("rel errors (prefill, step, step after resolve):", _run_long_context(port))
 
 

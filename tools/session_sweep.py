@@ -117,7 +117,7 @@ def main():
                           "placement": router.load(), "frames_per_server_batch": st["frames"] / max(1, st["batches"]),
                           "max_server_batch": st["max_batch"],
                           "shared_weight_passes": [s.shared_passes() for s in servers],
-                          "attention": os.environ.get("SFG_ATTN", "rows"),
+                          "attention": os.environ.get("SFG_ATTN", "auto"),
                           "wall_s": round(time.time() - tw, 1)}), flush=True)
         del bq, router, servers
 
