@@ -94,7 +94,7 @@ for out_id, in_id in ((6, 5), (8, 7), (9, 8), (10, 9)):
 # complete, against the phase's weight bytes at the measured HBM peak
 H, QD, KVD, F = 4096, 4096, 1024, 14336
 wbytes = {"QKV": H * (QD + 2 * KVD) * 2, "ATTN": 0, "O": QD * H * 2, "GU": 2 * H * F * 2, "DOWN": F * H * 2}
-print("phase      start    end   dur  ideal@6.4TB/s  over")
+print("phase      start    end   dur  ideal@6.55TB/s over")
 tot = over_tot = 0.0
 for l in range(1, NL - 1):
     for k, ph in enumerate(("QKV", "ATTN", "O", "GU", "DOWN")):
@@ -102,7 +102,7 @@ for l in range(1, NL - 1):
         in_id = out_id - 1
         s0 = (tr[:, in_id, 2].max() - t0) / 1000
         s1 = (tr[:, out_id, 2].max() - t0) / 1000
-        ideal = wbytes[ph] / 6.4336e12 * 1e6
+        ideal = wbytes[ph] / 6.5488e12 * 1e6  # MEASURED_PEAKS.json hbm_gbs
         print(f"L{l} {ph:5s} {s0:7.1f} {s1:7.1f} {s1 - s0:5.1f} {ideal:8.1f} {s1 - s0 - ideal:6.1f}")
         tot += s1 - s0
         over_tot += s1 - s0 - ideal
