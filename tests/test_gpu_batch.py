@@ -6,12 +6,18 @@ Bar: every response is BITWISE the response ServerEngine.handle gives for
 the same frame one by one on an identical server (batch invariance of the
 FAST kernels), error frames included, and every session ends in the same
 state (server.hpp:49-59 SessionView)."""
+import os
+
 import numpy as np
 import pytest
 
 import paper_2602_16760_b200 as sfg
 import pyoracle as po
 import wirepy
+
+# key-chunked sessions (forced by SFG_ATTN=chunked) never share a weight pass by design;
+# their responses must still equal handle()'s bitwise
+SHARES = 0 if os.environ.get("SFG_ATTN") == "chunked" else 1
 
 pytestmark = pytest.mark.gpu
 
@@ -101,7 +107,7 @@ def test_handle_batch_bitwise_equals_one_by_one(desk_fast):
     ]
     rounds.append(r3)
     a = _run_pair(cfg, m, eng, rounds)
-    assert a.shared_passes() >= 3
+    assert a.shared_passes() >= 3 * SHARES
 
 
 def test_handle_batch_continues_decoding(desk_fast):
@@ -125,7 +131,7 @@ def test_handle_batch_continues_decoding(desk_fast):
             lens[k] = L + 3
         rounds.append(rnd)
     a = _run_pair(cfg, m, eng, rounds)
-    assert a.shared_passes() >= 6
+    assert a.shared_passes() >= 6 * SHARES
 
 
 def test_handle_batch_seven_b_width():
@@ -173,7 +179,7 @@ def test_handle_batch_seven_b_width():
         for i, (g, w) in enumerate(zip(got, want)):
             assert wirepy.decode(g)[0]["kind"] == "response", wirepy.decode(g)[0]
             assert wirepy.strip_srv_ms(g) == wirepy.strip_srv_ms(w), (step, i)
-    assert a.shared_passes() >= 3
+    assert a.shared_passes() >= 3 * SHARES
     for sid in sids:
         assert a.session_view(sid) == b.session_view(sid)
 
@@ -198,4 +204,4 @@ def test_handle_batch_two_full_lookahead_batches(desk_fast):
             lens[sid] = prior + 16
         rounds.append(rnd)
     a = _run_pair(cfg, m, eng, rounds)
-    assert a.shared_passes() >= 4
+    assert a.shared_passes() >= 4 * SHARES
