@@ -820,7 +820,7 @@ __device__ __forceinline__ float* ring_base() {
 // publish an item's (m, l, o) rows: one chunk -> the final attention rows and
 // O-projection image; several -> partials, then the chunks of this (kv head,
 // query group) merge in chunk order, each CTA a slice of the queries
-template <int HD>
+template <int HD, bool kContig = false>  // kContig: lane owns head dims 4 lane .. 4 lane + 3 (else lane + 32 d)
 __device__ __forceinline__ void attn_publish(const MegaArgs& a, int l, int kvh, int chunk, int nchunks, int qg, int at,
                                              float* part, float* scratch, const float (&mx)[8], const float (&sm)[8],
                                              const float (&o)[8][HD / 32]) {
@@ -853,7 +853,7 @@ __device__ __forceinline__ void attn_publish(const MegaArgs& a, int l, int kvh, 
                     dst[1] = sm[i];
                 }
 #pragma unroll
-                for (int d = 0; d < DPL; ++d) dst[2 + lane + 32 * d] = o[i][d];
+                for (int d = 0; d < DPL; ++d) dst[2 + (kContig ? 4 * lane + d : lane + 32 * d)] = o[i][d];
             }
         named_sync(3, 256);
         unsigned* cnt = fptr(a, l, K_ATT, a.n_kv + 1 + 2 * kvh + qg);
@@ -956,7 +956,7 @@ __device__ __forceinline__ void attn_publish(const MegaArgs& a, int l, int kvh, 
                     const float lsum = sm[i];
                     if (d == 0 && lane == 0 && !(lsum > 0.0f)) atomicOr(a.status, ST_EMPTY_ROW);
                     const float val = fmaf(o[i][d], 1.0f, 0.0f) / lsum;
-                    const int f = (kvh * group + g) * HD + lane + 32 * d;
+                    const int f = (kvh * group + g) * HD + (kContig ? 4 * lane + d : lane + 32 * d);
                     a.att[static_cast<size_t>(r) * a.qd + f] = val;
                     put_split<kRows>(a.xim[P_O], f, r, val);
                 }
@@ -1416,9 +1416,8 @@ __device__ __noinline__ void attention_tile_tc(const MegaArgs& a, int l, int kvh
             const float4 p0 = sP4[j * 16 + ((q0 >> 2) ^ (j & 15))];
             const float4 p1 = sP4[j * 16 + (((q0 >> 2) + 1) ^ (j & 15))];
             const float pp[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-            float v[DPL];
-#pragma unroll
-            for (int d = 0; d < DPL; ++d) v[d] = sV[j * HD + lane + 32 * d];
+            const float4 v4 = reinterpret_cast<const float4*>(sV + j * HD)[lane];  // dims 4 lane .. + 3
+            const float v[DPL] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
             for (int i = 0; i < 8; i += 2)
 #pragma unroll
@@ -1434,7 +1433,7 @@ __device__ __noinline__ void attention_tile_tc(const MegaArgs& a, int l, int kvh
                 const int r = min(qbase + q0 + i, NQ - 1) / group;
                 const float* vr = sVt + (sh_tail[r][min(ki - prior, kRows - 1)] - prior) * HD;
 #pragma unroll
-                for (int d = 0; d < DPL; ++d) o[i][d] = fmaf(pp[i], vr[lane + 32 * d], o[i][d]);
+                for (int d = 0; d < DPL; ++d) o[i][d] = fmaf(pp[i], vr[4 * lane + d], o[i][d]);
             }
         }
     }
@@ -1444,7 +1443,7 @@ __device__ __noinline__ void attention_tile_tc(const MegaArgs& a, int l, int kvh
         named_sync(3, 256);
         if (at == 0) mbar_arrive(retb);
     }
-    attn_publish<HD>(a, l, kvh, chunk, nchunks, qg, at, part, sTS, mx, sm, o);
+    attn_publish<HD, true>(a, l, kvh, chunk, nchunks, qg, at, part, sTS, mx, sm, o);
 }
 
 __device__ __forceinline__ int attn_chunks(const MegaArgs& a) {
