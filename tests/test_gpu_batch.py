@@ -205,3 +205,47 @@ def test_handle_batch_two_full_lookahead_batches(desk_fast):
         rounds.append(rnd)
     a = _run_pair(cfg, m, eng, rounds)
     assert a.shared_passes() >= 4 * SHARES
+
+
+def test_handle_batch_matches_reference_server(desk_fast, ref):
+    """Cross-session weight passes against the UNMODIFIED reference server
+    (oracle/_ref, server.cpp:226-265 one frame at a time): two sessions'
+    16-row lookahead-tree frames share one 32-row pass on the GPU.  Response
+    headers (srv_ms aside) and session state equal the reference's; hidden
+    rows are within the FAST tolerance (per-row relative L2 <= 1e-5)."""
+    cfg, m, eng = desk_fast
+    mr = ref.model(cfg, bf16=True)
+    split = 1
+    gs = sfg.ServerEngine(eng, sfg.ServerConfig(split, cfg.n_layers - split))
+    rs = ref.server(mr, split, cfg.n_layers - split)
+    rng = np.random.default_rng(21)
+    ids = lambda n: rng.integers(0, cfg.vocab_size, n).tolist()  # noqa: E731
+    p = {"s0": ids(6), "s1": ids(11)}
+    lens = {k: len(v) for k, v in p.items()}
+    rounds = [[_prompt(k, v) for k, v in p.items()]]
+    for rnd_i in range(3):
+        rnd = []
+        for k in p:
+            keep = None if rnd_i == 0 else [0]  # commit the previous step's row 0
+            rnd.append((lambda k=k, t=ids(16), L=lens[k], kp=keep: lambda mm: _step(mm, k, L, t, keep=kp, tree=True))())
+            lens[k] += 1
+        rounds.append(rnd)
+    worst = 0.0
+    for rnd in rounds:
+        frames = [f(m) for f in rnd]
+        got = gs.handle_batch(frames)
+        want = [rs.handle(f) for f in frames]
+        for g, w in zip(got, want):
+            hg, rg = wirepy.response_rows(g, cfg.hidden_dim)
+            hw, rw = wirepy.response_rows(w, cfg.hidden_dim)
+            hg.pop("srv_ms", None)
+            hw.pop("srv_ms", None)
+            assert hg == hw
+            if rw is not None:
+                err = float(np.max(np.linalg.norm(rg - rw, axis=-1) / np.maximum(np.linalg.norm(rw, axis=-1), 1e-30)))
+                worst = max(worst, err)
+                assert err <= 1e-5, err
+    for sid in p:
+        assert gs.session_view(sid) == rs.session_view(sid)
+    assert gs.shared_passes() >= 3 * SHARES
+    print("worst per-row relative error vs the reference server:", worst)
