@@ -325,6 +325,13 @@ void sfg_debug_set_mega(int32_t on);
 void sfg_debug_mega_trace(int32_t on);
 int32_t sfg_debug_mega_trace_read(sfg_bank* b, uint64_t* out, size_t n);
 int32_t sfg_debug_bank_buffer(sfg_bank* b, int32_t which, float* out, int32_t n);
+/* the server's frame-mask parser (mask_from_frame, server.cpp:148-171): f16
+ * mask [q x kv] -> per-row visible runs [start, end) in row_off / starts /
+ * ends (capacity max_runs); returns 0, or the protocol status for an entry
+ * other than 0 / -0 / -inf; any_empty_row flags a row with no visible
+ * position (host code, no device needed: CPU tests).                      */
+int32_t sfg_debug_mask_runs(const uint16_t* mask, int32_t q, int32_t kv, int32_t* row_off, int32_t* starts,
+                            int32_t* ends, int32_t max_runs, int32_t* n_runs, int32_t* any_empty_row);
 void sfg_profiler_reset(void);
 int32_t sfg_profiler_stats(int32_t cls, int64_t* count, double* ms, double* bytes, double* flops);
 

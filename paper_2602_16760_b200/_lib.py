@@ -163,6 +163,7 @@ def lib() -> C.CDLL:
         "sfg_set_graphs": (None, [i32]),
         "sfg_copy_bytes": (None, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "sfg_profiler_enable": (None, [i32]),
+        "sfg_debug_mask_runs": (i32, [C.POINTER(C.c_uint16), i32, i32, i32p, i32p, i32p, i32, i32p, i32p]),
         "sfg_debug_set_mega": (None, [i32]),
         "sfg_debug_mega_trace": (None, [i32]),
         "sfg_debug_mega_trace_read": (i32, [vp, C.POINTER(C.c_uint64), C.c_size_t]),

@@ -409,6 +409,21 @@ int32_t sfg_debug_mega_trace_read(sfg_bank* b, uint64_t* out, size_t n) {
     return mega_trace_read(*b->b, reinterpret_cast<unsigned long long*>(out), n);
 }
 
+int32_t sfg_debug_mask_runs(const uint16_t* mask, int32_t q, int32_t kv, int32_t* row_off, int32_t* starts,
+                            int32_t* ends, int32_t max_runs, int32_t* n_runs, int32_t* any_empty_row) {
+    SFG_GUARD({
+        const MaskRuns r = runs_from_f16_mask(mask, q, kv);
+        if (static_cast<int>(r.runs.size()) > max_runs) throw Error(Kind::capacity, "run buffer too small");
+        for (int i = 0; i <= q; ++i) row_off[i] = r.row_off[i];
+        for (size_t i = 0; i < r.runs.size(); ++i) {
+            starts[i] = r.runs[i].start;
+            ends[i] = r.runs[i].end;
+        }
+        *n_runs = static_cast<int32_t>(r.runs.size());
+        *any_empty_row = r.any_empty_row ? 1 : 0;
+    });
+}
+
 int32_t sfg_debug_bank_buffer(sfg_bank* b, int32_t which, float* out, int32_t n) {
     SFG_GUARD({
         Workspace& ws = b->b->ws();
