@@ -36,9 +36,9 @@ allus = sum(tot.values())
 with open(os.path.join(out, f"{tag}_ncu_launches_summary.txt"), "w") as f:
     f.write("ncu --metrics gpu__time_duration.sum --clock-control none, decode-step kernels of "
             "`bench.py --steps 2 --warmup 3 --no-sweep --no-cpu`\n")
-    f.write("(cold, serialised launches under ncu: use the SHARE, not the absolute times; fast::gemm_kernel = the "
-            "24-token prompt prefill on the per-GEMM path, outside the timed decode steps; mega_kernel = the 2+28+2 "
-            "layer stacks of each decode step)\n")
+    f.write("(cold, serialised launches under ncu: use the SHARE, not the absolute times; fast::pgemm_kernel = the "
+            "prompt prefill GEMMs, outside the timed decode steps; mega_kernel = the 2+28+2 layer stacks of each "
+            "decode step; fast::gemm_kernel<3,1> = the LM head with fused argmax partials)\n")
     f.write(f"{'kernel':60s} {'launches':>9s} {'total_us':>10s} {'share':>6s}\n")
     for k in sorted(tot, key=lambda k: -tot[k]):
         f.write(f"{k[:60]:60s} {cnt[k]:9d} {tot[k]:10.1f} {100 * tot[k] / allus:5.1f}%\n")
