@@ -1263,6 +1263,7 @@ __device__ __noinline__ void attention_tile_tc(const MegaArgs& a, int l, int kvh
     // split.  (Loading the cached K before this step's QKV tiles are done was
     // measured slower: the loads compete with the QKV weight stream for HBM.)
     wait_head_qkv(a, l, kvh, at);
+    if (tr) *tslot(a, blockIdx.x, 230 + l, 14) = gtimer();  // this step's q / K / V tiles are published
     {
         float4 kx[16], qx[8], tx2[2];
 #pragma unroll
@@ -1276,6 +1277,7 @@ __device__ __noinline__ void attention_tile_tc(const MegaArgs& a, int l, int kvh
             const int f = at + 256 * i;
             put3x4(sKp, 32768, 16384, f >> 5, 4 * (f & 31), kx[i]);
         }
+        if (tr) *tslot(a, blockIdx.x, 230 + l, 15) = gtimer();  // thread 0's K rows loaded and split
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int f = at + 256 * i, qi = f >> 5, c = f & 31, q = qbase + qi;

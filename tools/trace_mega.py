@@ -166,6 +166,8 @@ for l in range(1, NL - 1):
     def md(x):
         return f"{np.median(x) / 1000:5.2f}/{x.max() / 1000:5.2f}"
     seg = [("K land", 0, 1), ("scores", 1, 2), ("P+V", 2, 3), ("PV", 3, 5)]
+    if (T[:, 14] > 0).all() and (T[:, 15] > 0).all():  # tensor-core path: QKV wait | K load + split | Q + rest
+        seg = [("QKV wait", 0, 14), ("K load+split", 14, 15), ("Q split+MMA in", 15, 1)] + seg[1:]
     parts = ", ".join(f"{n} {md(T[:, b] - T[:, a])}" for n, a, b in seg)
     has6 = T[:, 6] > 0
     if has6.any():
