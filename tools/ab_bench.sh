@@ -9,7 +9,7 @@ for spec in "$@"; do
   lib=$(echo "$envs" | tr ' ' '\n' | sed -n 's/^LIB=//p')
   if [ -n "$lib" ]; then cp "$lib" $SO; else cp /tmp/libsfg_orig.so $SO; fi
   envs=$(echo "$envs" | tr ' ' '\n' | grep -v '^LIB=' | tr '\n' ' ')
-  env $envs timeout 600 python bench.py --no-sweep --no-cpu --steps 10 > gpurun_out/ab_$label.txt 2> gpurun_out/ab_$label.err
+  env $envs timeout 600 python bench.py --no-sweep --no-cpu --steps 10 $BENCH_ARGS > gpurun_out/ab_$label.txt 2> gpurun_out/ab_$label.err
   python - "$label" <<'PY'
 import json, sys
 label = sys.argv[1]
