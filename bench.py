@@ -245,7 +245,7 @@ def config_dict(args, ws):
                          ("chunked (auto: >= 768 cached keys)" if PROMPT_LEN >= 768 else "rows (auto: < 768 cached keys)"),
             "sessions_per_gpu": 1 if args.tp == 1 else 1.0 / args.tp,
             "parallelism": f"replicas x{ws} (independent sessions)" if args.tp == 1 else
-                           f"tp{args.tp} (one session, NCCL all-reduce of O/down over NVLink)",
+                           f"tp{args.tp} (one session, O/down partial tiles exchanged over NVLink peer memory inside the layer-stack kernel)",
             "l2": "inputs larger than L2 (the middle-layer weights, >10 GB, are streamed every step)"}
 
 

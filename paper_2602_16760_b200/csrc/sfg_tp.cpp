@@ -1,5 +1,8 @@
 // Tensor parallelism (SURVEY.md §8e, configs[3]: the 12B shape at TP=2):
-// NCCL all-reduce of the row-parallel projections' partial outputs.
+// the NCCL group (IPC-handle exchange for the megakernel's peer-memory inbox,
+// sfg_engine.cpp) and the NCCL all-reduce of the row-parallel projections'
+// partial outputs on the per-GEMM (prompt) path.  The decode step's
+// layer-stack kernel exchanges its O/down partials over peer memory instead.
 //
 // NCCL is bound at run time (dlopen of the libnccl.so.2 already in the
 // process — torch's — or the system one), so libsfg.so does not pin a second
