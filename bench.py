@@ -279,6 +279,9 @@ def run_ours(args, ws, rank, local):
         # one tensor-parallel group over all ranks: rank 0 makes the NCCL id
         if ws != args.tp:
             raise SystemExit("--tp N runs as one group: launch exactly N ranks")
+        # the sweeps drive many independent sessions per rank; a TP group must
+        # make the same forward calls on every rank, so they run at TP=1 only
+        args.no_sweep = True
         import torch
         import torch.distributed as dist
         buf = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")

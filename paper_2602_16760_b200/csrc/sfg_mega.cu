@@ -2215,12 +2215,15 @@ int mega_batch_rows(const Engine& e) {
 
 // per-phase CTA split (phase_ctas) and whole tiles (whole_tiles) of a launch,
 // shared by the launch and by MegaState's partial-buffer sizing
-static int mega_align_pct() {
+// Default 85 %; 70 % under tensor parallelism, whose half-width phases have
+// fewer tiles (TP=2 NeMo-12B step: 4.87 -> 4.72 ms; at TP=1 70 % is slower,
+// 5.04 -> 5.23 ms; tools/tp_knob_sweep.sh)
+static int mega_align_pct(int tp) {
     static const int v = [] {
         const char* e = getenv("SFG_MEGA_ALIGN");
-        return e ? atoi(e) : 85;
+        return e ? atoi(e) : -1;
     }();
-    return v;
+    return v >= 0 ? v : (tp > 1 ? 70 : 85);
 }
 static bool mega_whole_on() {
     static const int v = [] {
@@ -2229,19 +2232,19 @@ static bool mega_whole_on() {
     }();
     return v != 0;
 }
-static void mega_split(const Dims& dl, int nsm, int (&G)[4], int (&W)[4], int (&tiles)[4]) {
+static void mega_split(const Dims& dl, int nsm, int tp, int (&G)[4], int (&W)[4], int (&tiles)[4]) {
     const int tQ = (dl.qd + 2 * dl.kvd + tc::kM - 1) / tc::kM, tH = (dl.H + tc::kM - 1) / tc::kM;
     const int t_of[4] = {tQ, tH, dl.F / 64, tH};
     const int kb_of[4] = {dl.H / tc::kKB, dl.qd / tc::kKB, dl.H / tc::kKB, dl.F / tc::kKB};
     for (int p = 0; p < 4; ++p) {
         tiles[p] = t_of[p];
-        G[p] = phase_ctas(t_of[p], kb_of[p], nsm, mega_align_pct());
+        G[p] = phase_ctas(t_of[p], kb_of[p], nsm, mega_align_pct(tp));
         W[p] = mega_whole_on() ? whole_tiles(t_of[p], kb_of[p], G[p]) : 0;
     }
 }
 static int mega_split_tiles_max(const Engine& e) {
     int G[4], W[4], t[4];
-    mega_split(e.dims(), device_sm_count(), G, W, t);
+    mega_split(e.dims(), device_sm_count(), e.tp_size(), G, W, t);
     int m = 0;
     for (int p = 0; p < 4; ++p) m = std::max(m, t[p] - W[p] * G[p]);
     return m;
@@ -2527,7 +2530,7 @@ int mega_forward(Engine& e, Bank& b, int lb, int le, int rows, Workspace& ws, cu
         }();
         a.noload = noload_env;
         int tiles_of[4];
-        mega_split(dl, nsm, a.G, a.W, tiles_of);
+        mega_split(dl, nsm, e.tp_size(), a.G, a.W, tiles_of);
         const int tQ = tiles_of[P_QKV], tH = tiles_of[P_O];
         // flag layout (must match kind_tiles): statistics tiles + counter, then
         // per layer QKV, attention kv heads, O, gate|up, down tiles + counter each
