@@ -2215,15 +2215,16 @@ int mega_batch_rows(const Engine& e) {
 
 // per-phase CTA split (phase_ctas) and whole tiles (whole_tiles) of a launch,
 // shared by the launch and by MegaState's partial-buffer sizing
-// Default 85 %; 70 % under tensor parallelism, whose half-width phases have
-// fewer tiles (TP=2 NeMo-12B step: 4.87 -> 4.72 ms; at TP=1 70 % is slower,
-// 5.04 -> 5.23 ms; tools/tp_knob_sweep.sh)
+// Default 85 %; 50 % under tensor parallelism, whose half-width phases have
+// fewer tiles: every TP=2 NeMo-12B phase then runs tile-aligned (O and down on
+// 80 CTAs, one 1/2 k piece each; step 4.87 -> 4.46 ms), while at TP=1 lower
+// thresholds are slower (70 %: 5.04 -> 5.23 ms; tools/tp_knob_sweep.sh)
 static int mega_align_pct(int tp) {
     static const int v = [] {
         const char* e = getenv("SFG_MEGA_ALIGN");
         return e ? atoi(e) : -1;
     }();
-    return v >= 0 ? v : (tp > 1 ? 70 : 85);
+    return v >= 0 ? v : (tp > 1 ? 50 : 85);
 }
 static bool mega_whole_on() {
     static const int v = [] {
