@@ -1,4 +1,5 @@
-cd $GRAFT_REPO_ROOT
+cd ${GRAFT_REPO_ROOT:-.}
+# NeMo-12B step under SFG_MEGA_ALIGN settings at TP=2 and TP=1 (2-GPU box)
 p() { python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(round(d['ms_per_step'],4), round(d['server_ms_per_step'],4))"; }
 port=29600
 for al in 85 70 50 0; do
