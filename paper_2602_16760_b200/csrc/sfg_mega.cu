@@ -33,6 +33,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <cstdio>
 #include <cstring>
 #include <string>
 
@@ -2219,11 +2221,17 @@ int mega_batch_rows(const Engine& e) {
 // fewer tiles: every TP=2 NeMo-12B phase then runs tile-aligned (O and down on
 // 80 CTAs, one 1/2 k piece each; step 4.87 -> 4.46 ms), while at TP=1 lower
 // thresholds are slower (70 %: 5.04 -> 5.23 ms; tools/tp_knob_sweep.sh)
-static int mega_align_pct(int tp) {
+static int mega_align_pct(int tp, int p) {
     static const int v = [] {
         const char* e = getenv("SFG_MEGA_ALIGN");
         return e ? atoi(e) : -1;
     }();
+    static const std::array<int, 4> vp = [] {  // dev knob: per phase "qkv,o,gu,down"
+        std::array<int, 4> r{-1, -1, -1, -1};
+        if (const char* e = getenv("SFG_MEGA_ALIGN4")) sscanf(e, "%d,%d,%d,%d", &r[0], &r[1], &r[2], &r[3]);
+        return r;
+    }();
+    if (vp[p] >= 0) return vp[p];
     return v >= 0 ? v : (tp > 1 ? 50 : 85);
 }
 static bool mega_whole_on() {
@@ -2239,7 +2247,7 @@ static void mega_split(const Dims& dl, int nsm, int tp, int (&G)[4], int (&W)[4]
     const int kb_of[4] = {dl.H / tc::kKB, dl.qd / tc::kKB, dl.H / tc::kKB, dl.F / tc::kKB};
     for (int p = 0; p < 4; ++p) {
         tiles[p] = t_of[p];
-        G[p] = phase_ctas(t_of[p], kb_of[p], nsm, mega_align_pct(tp));
+        G[p] = phase_ctas(t_of[p], kb_of[p], nsm, mega_align_pct(tp, p));
         W[p] = mega_whole_on() ? whole_tiles(t_of[p], kb_of[p], G[p]) : 0;
     }
 }
